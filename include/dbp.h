@@ -1,0 +1,170 @@
+/*
+ * dbp.h -- C ABI of libdbp, the B200-native (sm_100a) hot path of
+ * "Decentralized Baseband Processing for Massive MU-MIMO Systems"
+ * (K. Li, R. Sharan, Y. Chen, T. Goldstein, J. R. Cavallaro, C. Studer,
+ * arXiv 1702.04458).  Citations "P<n>" are lines of PAPER.md.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  * Complex numbers are dbp_cf32 = {float re, im} (== torch.complex64 ==
+ *    cuFloatComplex), stored row-major, interleaved.
+ *  * Clusters are partitioned row-wise over ranks (P149-155): rank r of
+ *    `world` owns clusters [r*C/world, (r+1)*C/world); C % world == 0.
+ *    Every per-cluster array below holds only the caller rank's C_loc =
+ *    C/world clusters; per-subcarrier consensus arrays are full and
+ *    replicated on every rank.
+ *  * Pointers may be DEVICE pointers (the normal case; torch owns them) or
+ *    HOST pointers (pageable or pinned).  Host buffers are staged through a
+ *    library-owned device buffer with cudaMemcpyAsync on `stream`, so the
+ *    host->device and device->host copies are part of the call (used by the
+ *    end-to-end measurement).  All pointers of one call must be of the same
+ *    kind.  Alignment: 16 bytes for complex arrays.
+ *  * `ws` is a caller-owned device workspace of at least
+ *    dbp_workspace_bytes() bytes (NULL allowed when that size is 0).
+ *  * All compute is enqueued asynchronously on `stream` (a cudaStream_t;
+ *    NULL = legacy default stream).  Host-pointer calls synchronise `stream`
+ *    before returning.
+ *  * Ownership: the caller owns every buffer and the workspace; the library
+ *    owns only the context, its NCCL communicator, the device error flag,
+ *    host-I/O staging buffers and cached launch state.
+ *  * Errors: invalid arguments are detected synchronously BEFORE any launch
+ *    and return DBP_ERR_INVALID_ARG with nothing enqueued; shapes outside the
+ *    supported envelope return DBP_ERR_UNSUPPORTED.  A non-positive or
+ *    non-finite Cholesky pivot found on the device (SPEC S44) sets a device
+ *    flag; dbp_sync() then returns DBP_ERR_NOT_HPD and the outputs of the
+ *    calls since the last dbp_sync() are undefined.  dbp_last_error() gives a
+ *    thread-local message for the last non-OK status.
+ *  * Supported envelope (v1): 1 <= U <= 32 (users are zero-padded to the
+ *    next of 4/8/16/32 internally, which is exact), 1 <= S <= 64, N_sym <= 16.
+ *  * Threading: a context is not thread-safe; use one per rank and thread.
+ */
+#ifndef DBP_H
+#define DBP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct { float re, im; } dbp_cf32;
+
+typedef enum {
+    DBP_OK = 0,
+    DBP_ERR_INVALID_ARG = 1,
+    DBP_ERR_UNSUPPORTED = 2,
+    DBP_ERR_NOT_HPD = 3,
+    DBP_ERR_CUDA = 4,
+    DBP_ERR_NCCL = 5,
+    DBP_ERR_WORKSPACE = 6
+} dbp_status;
+
+/* Regulariser g(s) of the equalisation problem (E0) (P205-218) and its
+ * proximal step (E2-*) (P335-344).  BOX with DBP_BPSK is the real-line
+ * projection of P344. */
+typedef enum { DBP_REG_MMSE = 0, DBP_REG_ZF = 1, DBP_REG_BOX = 2 } dbp_reg;
+
+/* Gray-mapped constellation O (P143), Es = 1; value = bits per symbol. */
+typedef enum { DBP_BPSK = 1, DBP_QPSK = 2, DBP_QAM16 = 4, DBP_QAM64 = 6 } dbp_mod;
+
+typedef enum { DBP_ALGO_ADMM_UL = 0, DBP_ALGO_CG_UL = 1, DBP_ALGO_ADMM_DL = 2 } dbp_algo;
+
+/* C = total clusters (all ranks), S = B_c antennas per cluster (P150),
+ * U users, N subcarriers, N_sym symbols sharing one channel (P706-709).
+ * B = C*S. */
+typedef struct { int32_t C, S, U, N, N_sym; } dbp_dims;
+
+typedef struct dbp_ctx dbp_ctx;
+
+/* Counters since dbp_ctx_create (host-side bookkeeping). */
+typedef struct {
+    int64_t allreduce_calls;   /* NCCL collectives issued (0 at world == 1)            */
+    int64_t allreduce_bytes;   /* NCCL payload bytes per rank, sum over calls (P625)  */
+    int64_t kernel_launches;   /* libdbp kernels enqueued                              */
+    int64_t consensus_rounds;  /* algorithmic consensus rounds: ADMM-UL T, CG T+1,
+                                  ADMM-DL T-1 per call (SPEC S389-390), any world     */
+} dbp_stats;
+
+/* Options for dbp_set_option(). */
+typedef enum {
+    /* 0 (default): at world == 1 use the fused single-GPU kernels; 1: always
+     * use the per-iteration (multi-kernel + collective) path, as at world > 1. */
+    DBP_OPT_FORCE_SPLIT = 1
+} dbp_option;
+
+/* NCCL bootstrap: fills 128 bytes (an ncclUniqueId) on rank 0; broadcast it to
+ * the other ranks (e.g. over torch.distributed) before dbp_ctx_create. */
+dbp_status dbp_get_unique_id(uint8_t id[128]);
+
+/* Create a context bound to CUDA `device` for `rank` of `world`.  `id` is the
+ * rank-0 unique id (ignored and may be NULL when world == 1).  Collective
+ * over all ranks when world > 1 (ncclCommInitRank). */
+dbp_status dbp_ctx_create(dbp_ctx** ctx, int device, int rank, int world, const uint8_t* id);
+dbp_status dbp_ctx_destroy(dbp_ctx* ctx);
+dbp_status dbp_set_option(dbp_ctx* ctx, int option, int64_t value);
+dbp_status dbp_get_stats(const dbp_ctx* ctx, dbp_stats* out);
+
+/* Thread-local message describing the last non-OK status ("" if none). */
+const char* dbp_last_error(void);
+
+/* Device workspace needed by one call of `algo` with `dims` on this context
+ * (depends on world and options).  Deterministic; 0 is a valid answer. */
+dbp_status dbp_workspace_bytes(const dbp_ctx* ctx, const dbp_dims* dims, int algo, size_t* bytes);
+
+/* Algorithm 1 (P282-318): decentralized ADMM uplink data detection.
+ *   H      [C_loc][N][S][U]     uplink H_c (P151)                      (read)
+ *   y      [C_loc][N][N_sym][S] receive vectors y_c (eq. (1), P152)    (read)
+ *   rho > 0 ADMM penalty (P234); gamma > 0 step (P245, 1 = default);
+ *   N0 >= 0 noise variance, Es > 0 symbol energy (MMSE regulariser, P212);
+ *   reg    prox of step (E2) (P335-344); mod: constellation for BOX radius
+ *          and for the hard decisions;
+ *   T >= 1 iterations incl. the init t = 1 (Alg. 1 loop from t = 2; T
+ *          consensus collectives per call);
+ *   s_hat  [N][N_sym][U] soft output x_hat = s^(T) (P316), identical on
+ *          every rank                                                   (write)
+ *   hard   NULL or [N][N_sym][U] Gray bit labels of the nearest point,
+ *          [I bits | Q bits], ties toward the negative level (P210)     (write)
+ * The U x U form of step (E1), eq. (3) (P272), is used for every S (the S x S
+ * form eq. (4) gives the same iterates; reading 7). */
+dbp_status dbp_detect_admm(dbp_ctx* ctx, const dbp_dims* dims, const dbp_cf32* H,
+                           const dbp_cf32* y, float rho, float gamma, float N0, float Es,
+                           int reg, int mod, int32_t T, dbp_cf32* s_hat, uint8_t* hard,
+                           void* ws, size_t ws_bytes, void* stream);
+
+/* Algorithm 2 (P383-413): decentralized conjugate-gradient uplink detection.
+ *   rho >= 0: N0/Es for MMSE, 0 for ZF (P376);  T >= 1 CG iterations
+ *   (T + 1 consensus collectives: y^MRC and one per iteration);
+ *   x_hat  [N][N_sym][U] soft output (P411), replicated;  hard as above.
+ * Line 11 is read with e^(t) (reading 1); alpha uses Re(p^H e)
+ * (reading 3); ||r||^2 == 0 freezes the iterate (reading 4). */
+dbp_status dbp_detect_cg(dbp_ctx* ctx, const dbp_dims* dims, const dbp_cf32* H,
+                         const dbp_cf32* y, float rho, int mod, int32_t T, dbp_cf32* x_hat,
+                         uint8_t* hard, void* ws, size_t ws_bytes, void* stream);
+
+/* Algorithm 3 (P491-527): decentralized ADMM downlink beamforming, eps = 0
+ * (Alg. 3 as printed; eps > 0 = Lemma 2 returns DBP_ERR_UNSUPPORTED in v1).
+ *   Hd  [C_loc][N][U][S]     downlink H_c^d = (H_c^u)^T (P174, P181)   (read)
+ *   s   [N][N_sym][U]        transmit symbols s^d, replicated (P172)   (read)
+ *   rho > 0, gamma > 0 (P457);  T >= 1 (T - 1 consensus collectives: the
+ *   first iteration is local, P811);
+ *   x   [C_loc][N][N_sym][S] local beamforming vectors x_c^(T) (P525)  (write) */
+dbp_status dbp_beamform_admm(dbp_ctx* ctx, const dbp_dims* dims, const dbp_cf32* Hd,
+                             const dbp_cf32* s, float rho, float gamma, float eps, int32_t T,
+                             dbp_cf32* x, void* ws, size_t ws_bytes, void* stream);
+
+/* Hard slicer alone (P210): bits[i] = Gray label of the nearest point of `mod`
+ * to x[i] (decided in fp32, same rule as the detectors' `hard`).  Device or
+ * host pointers as above. */
+dbp_status dbp_slice(dbp_ctx* ctx, int mod, int64_t count, const dbp_cf32* x, uint8_t* bits,
+                     void* stream);
+
+/* Synchronise `stream`; returns DBP_ERR_NOT_HPD if a Cholesky pivot failed in
+ * any call since the previous dbp_sync (and clears the flag), or
+ * DBP_ERR_CUDA / DBP_ERR_NCCL for deferred runtime errors. */
+dbp_status dbp_sync(dbp_ctx* ctx, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DBP_H */

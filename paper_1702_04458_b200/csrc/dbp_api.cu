@@ -1,0 +1,561 @@
+// dbp_api.cu -- the C ABI of include/dbp.h: validation, workspace layout,
+// host-pointer staging, the per-call launch schedules and the NCCL consensus
+// collective (one in-place ncclAllReduce of the N x N_sym x U partial sums per
+// iteration, P311, P401, P513, P744-746).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/dbp.h"
+#include "dbp_internal.h"
+
+using namespace dbp;
+
+struct dbp_ctx {
+    int device = 0, rank = 0, world = 1;
+    ncclComm_t comm = nullptr;
+    int* d_flag = nullptr;
+    int64_t launches = 0;
+    int64_t allreduce_calls = 0, allreduce_bytes = 0, consensus_rounds = 0;
+    int force_split = 0;
+    void* stage = nullptr;       // host-I/O staging (device)
+    size_t stage_bytes = 0;
+    void* iws = nullptr;         // internal workspace when ws == NULL
+    size_t iws_bytes = 0;
+    int max_smem = 0;
+};
+
+static thread_local std::string g_err;
+
+static dbp_status fail(dbp_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+#define CU(call)                                                                            \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess) return fail(DBP_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+#define NC(call)                                                                            \
+    do {                                                                                    \
+        ncclResult_t r_ = (call);                                                           \
+        if (r_ != ncclSuccess) return fail(DBP_ERR_NCCL, "%s: %s", #call, ncclGetErrorString(r_)); \
+    } while (0)
+
+extern "C" const char* dbp_last_error(void) { return g_err.c_str(); }
+
+static int pad_users(int U) { return U <= 4 ? 4 : U <= 8 ? 8 : U <= 16 ? 16 : 32; }
+static size_t al(size_t b) { return (b + 255) & ~(size_t)255; }
+
+extern "C" dbp_status dbp_get_unique_id(uint8_t id[128]) {
+    if (!id) return fail(DBP_ERR_INVALID_ARG, "id is NULL");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId u;
+    NC(ncclGetUniqueId(&u));
+    memcpy(id, &u, 128);
+    g_err.clear();
+    return DBP_OK;
+}
+
+extern "C" dbp_status dbp_ctx_create(dbp_ctx** out, int device, int rank, int world, const uint8_t* id) {
+    if (!out) return fail(DBP_ERR_INVALID_ARG, "ctx out-pointer is NULL");
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world) return fail(DBP_ERR_INVALID_ARG, "bad rank %d / world %d", rank, world);
+    if (world > 1 && !id) return fail(DBP_ERR_INVALID_ARG, "world > 1 needs the rank-0 unique id");
+    int ndev = 0;
+    CU(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(DBP_ERR_INVALID_ARG, "device %d of %d", device, ndev);
+    CU(cudaSetDevice(device));
+    dbp_ctx* c = new dbp_ctx();
+    c->device = device;
+    c->rank = rank;
+    c->world = world;
+    cudaError_t e = cudaMalloc(&c->d_flag, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(c->d_flag, 0, sizeof(int));
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    if (e != cudaSuccess) {
+        delete c;
+        return fail(DBP_ERR_CUDA, "context setup: %s", cudaGetErrorString(e));
+    }
+    if (world > 1) {
+        ncclUniqueId u;
+        memcpy(&u, id, 128);
+        ncclResult_t r = ncclCommInitRank(&c->comm, world, u, rank);
+        if (r != ncclSuccess) {
+            cudaFree(c->d_flag);
+            delete c;
+            return fail(DBP_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+        }
+    }
+    *out = c;
+    g_err.clear();
+    return DBP_OK;
+}
+
+extern "C" dbp_status dbp_ctx_destroy(dbp_ctx* c) {
+    if (!c) return DBP_OK;
+    cudaSetDevice(c->device);
+    if (c->comm) ncclCommDestroy(c->comm);
+    cudaFree(c->d_flag);
+    if (c->stage) cudaFree(c->stage);
+    if (c->iws) cudaFree(c->iws);
+    delete c;
+    return DBP_OK;
+}
+
+extern "C" dbp_status dbp_set_option(dbp_ctx* c, int option, int64_t value) {
+    if (!c) return fail(DBP_ERR_INVALID_ARG, "ctx is NULL");
+    if (option == DBP_OPT_FORCE_SPLIT) { c->force_split = value ? 1 : 0; return DBP_OK; }
+    return fail(DBP_ERR_INVALID_ARG, "unknown option %d", option);
+}
+
+extern "C" dbp_status dbp_get_stats(const dbp_ctx* c, dbp_stats* s) {
+    if (!c || !s) return fail(DBP_ERR_INVALID_ARG, "NULL argument");
+    s->allreduce_calls = c->allreduce_calls;
+    s->allreduce_bytes = c->allreduce_bytes;
+    s->kernel_launches = c->launches;
+    s->consensus_rounds = c->consensus_rounds;
+    return DBP_OK;
+}
+
+// ----------------------------------------------------------------- shapes
+struct Shape {
+    int C, C_loc, S, U, UP, N, J;
+    long pairs() const { return (long)C_loc * N; }
+};
+
+static dbp_status check_dims(const dbp_ctx* c, const dbp_dims* d, Shape* sh) {
+    if (!c) return fail(DBP_ERR_INVALID_ARG, "ctx is NULL");
+    if (!d) return fail(DBP_ERR_INVALID_ARG, "dims is NULL");
+    if (d->C < 1 || d->S < 1 || d->U < 1 || d->N < 1 || d->N_sym < 1)
+        return fail(DBP_ERR_INVALID_ARG, "dims must be >= 1 (C=%d S=%d U=%d N=%d N_sym=%d)", d->C, d->S, d->U, d->N, d->N_sym);
+    if (d->C % c->world) return fail(DBP_ERR_INVALID_ARG, "C=%d not divisible by world=%d (SPEC S107)", d->C, c->world);
+    if (d->U > 32 || d->S > 64 || d->N_sym > 16)
+        return fail(DBP_ERR_UNSUPPORTED, "v1 envelope: U<=32, S<=64, N_sym<=16 (got U=%d S=%d N_sym=%d)", d->U, d->S, d->N_sym);
+    sh->C = d->C;
+    sh->C_loc = d->C / c->world;
+    sh->S = d->S;
+    sh->U = d->U;
+    sh->UP = pad_users(d->U);
+    sh->N = d->N;
+    sh->J = d->N_sym;
+    if ((long)sh->C_loc * sh->N > (1L << 31) - 1) return fail(DBP_ERR_UNSUPPORTED, "too many pairs");
+    return DBP_OK;
+}
+
+// Fused single-GPU schedule: NT subcarriers x C clusters per CTA, IT = UP/2
+// threads per pair, <= 1024 threads and the shared-memory budget.
+static bool fused_cfg(const dbp_ctx* c, const Shape& sh, int* NT) {
+    if (c->world != 1 || c->force_split) return false;
+    const int per_n = sh.C_loc * (sh.UP / 2);
+    if (per_n > 1024) return false;
+    int nt = std::max(1, std::min(256 / per_n, 1024 / per_n));
+    while (nt > 1 && admm_fused_smem(sh.UP, nt, sh.C_loc) > (size_t)c->max_smem) --nt;
+    if (admm_fused_smem(sh.UP, nt, sh.C_loc) > (size_t)c->max_smem) return false;
+    *NT = nt;
+    return true;
+}
+
+static void split_cfg(const Shape& sh, int* NT, int* CCH) {
+    const int it = sh.UP / 2;
+    int cch = std::min(sh.C_loc, std::max(1, 256 / it));
+    int nt = std::max(1, 256 / (cch * it));
+    nt = std::min(nt, sh.N);
+    *NT = nt;
+    *CCH = cch;
+}
+
+// Workspace layout (256-byte aligned segments).
+struct Layout {
+    size_t off[8];
+    size_t total;
+};
+
+static Layout layout(const Shape& sh, int algo) {
+    const size_t T = (size_t)sh.UP * (sh.UP + 1) / 2;
+    const size_t P = (size_t)sh.pairs();
+    const size_t vecp = P * sh.J * sh.UP * 8;      // per pair per symbol vectors
+    const size_t vecn = (size_t)sh.N * sh.J * sh.UP * 8;
+    Layout L{};
+    size_t sz[8] = {0};
+    if (algo == DBP_ALGO_ADMM_UL) {
+        sz[0] = P * T * 8;   // X
+        sz[1] = vecp;        // yreg
+        sz[2] = vecp;        // lam
+        sz[3] = vecp;        // z
+        sz[4] = vecn;        // wbuf
+    } else if (algo == DBP_ALGO_CG_UL) {
+        sz[0] = P * T * 8;                 // per-pair Gram
+        sz[1] = vecp;                      // per-pair matched filter
+        sz[2] = (size_t)sh.N * T * 8;      // G_loc
+        sz[3] = vecn;                      // wbuf
+        sz[4] = vecn;                      // x
+        sz[5] = vecn;                      // r
+        sz[6] = vecn;                      // p
+        sz[7] = (size_t)sh.N * sh.J * 4;   // rr
+    } else {
+        sz[0] = P * T * 8;   // X
+        sz[1] = vecp;        // m
+        sz[2] = vecp;        // lam
+        sz[3] = vecn;        // wbuf
+    }
+    size_t o = 0;
+    for (int i = 0; i < 8; ++i) { L.off[i] = o; o += al(sz[i]); }
+    L.total = o;
+    return L;
+}
+
+extern "C" dbp_status dbp_workspace_bytes(const dbp_ctx* c, const dbp_dims* d, int algo, size_t* bytes) {
+    if (!bytes) return fail(DBP_ERR_INVALID_ARG, "bytes is NULL");
+    if (algo < 0 || algo > 2) return fail(DBP_ERR_INVALID_ARG, "algo %d", algo);
+    Shape sh;
+    dbp_status st = check_dims(c, d, &sh);
+    if (st) return st;
+    *bytes = layout(sh, algo).total;
+    return DBP_OK;
+}
+
+// ------------------------------------------------------- pointer handling
+static bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+struct Io {                     // one host<->device staged buffer
+    const void* host_in;
+    void* host_out;
+    size_t bytes;
+    void* dev;
+};
+
+static dbp_status ensure_stage(dbp_ctx* c, size_t bytes) {
+    if (c->stage_bytes >= bytes) return DBP_OK;
+    if (c->stage) cudaFree(c->stage);
+    c->stage = nullptr;
+    c->stage_bytes = 0;
+    CU(cudaMalloc(&c->stage, bytes));
+    c->stage_bytes = bytes;
+    return DBP_OK;
+}
+
+static dbp_status ensure_iws(dbp_ctx* c, size_t bytes) {
+    if (c->iws_bytes >= bytes) return DBP_OK;
+    if (c->iws) cudaFree(c->iws);
+    c->iws = nullptr;
+    c->iws_bytes = 0;
+    CU(cudaMalloc(&c->iws, bytes));
+    c->iws_bytes = bytes;
+    return DBP_OK;
+}
+
+// Resolve the device workspace and the host/device kind of the I/O pointers.
+// In host mode, inputs are copied H2D into the staging buffer here.
+struct Call {
+    bool host = false;
+    Io io[5];
+    int nio = 0;
+    char* ws = nullptr;
+};
+
+static dbp_status begin_call(dbp_ctx* c, Call& k, const Layout& L, void* ws, size_t ws_bytes, cudaStream_t st) {
+    bool any_dev = false, any_host = false;
+    for (int i = 0; i < k.nio; ++i) {
+        const void* p = k.io[i].host_in ? k.io[i].host_in : k.io[i].host_out;
+        if (!p) continue;
+        (is_device_ptr(p) ? any_dev : any_host) = true;
+    }
+    if (any_dev && any_host) return fail(DBP_ERR_INVALID_ARG, "mixed host and device pointers in one call");
+    k.host = any_host;
+    if (ws) {
+        if (ws_bytes < L.total) return fail(DBP_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, L.total);
+        if (!is_device_ptr(ws)) return fail(DBP_ERR_INVALID_ARG, "workspace must be device memory");
+        k.ws = static_cast<char*>(ws);
+    } else if (L.total) {
+        dbp_status s = ensure_iws(c, L.total);
+        if (s) return s;
+        k.ws = static_cast<char*>(c->iws);
+    }
+    if (!k.host) {
+        for (int i = 0; i < k.nio; ++i) k.io[i].dev = k.io[i].host_in ? const_cast<void*>(k.io[i].host_in) : k.io[i].host_out;
+        return DBP_OK;
+    }
+    size_t need = 0;
+    for (int i = 0; i < k.nio; ++i) need += al(k.io[i].bytes);
+    dbp_status s = ensure_stage(c, need);
+    if (s) return s;
+    size_t o = 0;
+    for (int i = 0; i < k.nio; ++i) {
+        k.io[i].dev = (k.io[i].host_in || k.io[i].host_out) ? static_cast<char*>(c->stage) + o : nullptr;
+        o += al(k.io[i].bytes);
+        if (k.io[i].host_in) CU(cudaMemcpyAsync(k.io[i].dev, k.io[i].host_in, k.io[i].bytes, cudaMemcpyHostToDevice, st));
+    }
+    return DBP_OK;
+}
+
+static dbp_status end_call(dbp_ctx*, Call& k, cudaStream_t st) {
+    if (!k.host) return DBP_OK;
+    for (int i = 0; i < k.nio; ++i)
+        if (k.io[i].host_out) CU(cudaMemcpyAsync(k.io[i].host_out, k.io[i].dev, k.io[i].bytes, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    return DBP_OK;
+}
+
+static dbp_status allreduce(dbp_ctx* c, float2* buf, size_t nfloat2, cudaStream_t st) {
+    c->consensus_rounds += 1;
+    if (c->world == 1) return DBP_OK;
+    NC(ncclAllReduce(buf, buf, nfloat2 * 2, ncclFloat32, ncclSum, c->comm, st));
+    c->allreduce_calls += 1;
+    c->allreduce_bytes += (int64_t)(nfloat2 * 8);
+    return DBP_OK;
+}
+
+#define KL(call)                                                                               \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess) return fail(DBP_ERR_CUDA, "launch %s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+static Prox make_prox(int reg, int mod, int C, float rho, float N0, float Es) {
+    Prox p;
+    p.reg = reg;
+    p.inv_c = (float)(1.0 / C);
+    p.mmse_scale = (float)(1.0 / ((double)N0 / ((double)rho * Es) + C));
+    p.r = modem_of(mod).radius;
+    p.bpsk = mod == DBP_BPSK;
+    return p;
+}
+
+static bool mod_ok(int mod) { return mod == DBP_BPSK || mod == DBP_QPSK || mod == DBP_QAM16 || mod == DBP_QAM64; }
+
+// ============================================================ Algorithm 1
+extern "C" dbp_status dbp_detect_admm(dbp_ctx* c, const dbp_dims* d, const dbp_cf32* H, const dbp_cf32* y,
+                                      float rho, float gamma, float N0, float Es, int reg, int mod, int32_t T,
+                                      dbp_cf32* s_hat, uint8_t* hard, void* ws, size_t ws_bytes, void* stream) {
+    Shape sh;
+    dbp_status st = check_dims(c, d, &sh);
+    if (st) return st;
+    if (!H || !y || !s_hat) return fail(DBP_ERR_INVALID_ARG, "H, y and s_hat are required");
+    if (!(rho > 0.f) || !std::isfinite(rho)) return fail(DBP_ERR_INVALID_ARG, "rho must be > 0 (SPEC S54)");
+    if (!(gamma > 0.f) || !std::isfinite(gamma)) return fail(DBP_ERR_INVALID_ARG, "gamma must be > 0");
+    if (!(Es > 0.f) || !(N0 >= 0.f) || !std::isfinite(N0) || !std::isfinite(Es)) return fail(DBP_ERR_INVALID_ARG, "need N0 >= 0, Es > 0");
+    if (reg < 0 || reg > 2) return fail(DBP_ERR_INVALID_ARG, "reg %d", reg);
+    if (!mod_ok(mod)) return fail(DBP_ERR_INVALID_ARG, "mod %d", mod);
+    if (T < 1) return fail(DBP_ERR_INVALID_ARG, "T must be >= 1");
+    if (pre_smem(sh.UP, sh.S, sh.U, sh.J, PRE_ADMM_) > (size_t)c->max_smem) return fail(DBP_ERR_UNSUPPORTED, "S too large for the preprocessing tile");
+    CU(cudaSetDevice(c->device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const Layout Lw = layout(sh, DBP_ALGO_ADMM_UL);
+    Call k;
+    k.io[0] = {H, nullptr, (size_t)sh.pairs() * sh.S * sh.U * 8, nullptr};
+    k.io[1] = {y, nullptr, (size_t)sh.pairs() * sh.J * sh.S * 8, nullptr};
+    k.io[2] = {nullptr, s_hat, (size_t)sh.N * sh.J * sh.U * 8, nullptr};
+    k.io[3] = {nullptr, hard, hard ? (size_t)sh.N * sh.J * sh.U : 0, nullptr};
+    k.nio = 4;
+    if ((st = begin_call(c, k, Lw, ws, ws_bytes, s))) return st;
+    const float2* dH = static_cast<const float2*>(k.io[0].dev);
+    const float2* dy = static_cast<const float2*>(k.io[1].dev);
+    float2* X = reinterpret_cast<float2*>(k.ws + Lw.off[0]);
+    float2* yreg = reinterpret_cast<float2*>(k.ws + Lw.off[1]);
+    LaunchCtx L{s, c->d_flag, &c->launches};
+
+    // a1-a3: Gram + Cholesky inverse + matched filter (Alg. 1 lines 2-8)
+    KL(launch_pre(L, sh.UP, PRE_ADMM_, dH, dy, sh.S, sh.U, sh.J, sh.pairs(), rho, X, yreg));
+
+    AdmmArgs a{};
+    a.X = X; a.yreg = yreg;
+    a.lam = reinterpret_cast<float2*>(k.ws + Lw.off[2]);
+    a.z = reinterpret_cast<float2*>(k.ws + Lw.off[3]);
+    a.wbuf = reinterpret_cast<float2*>(k.ws + Lw.off[4]);
+    a.s_hat = static_cast<float2*>(k.io[2].dev);
+    a.hard = static_cast<uint8_t*>(k.io[3].dev);
+    a.C_loc = sh.C_loc; a.N = sh.N; a.J = sh.J; a.U = sh.U; a.T = T;
+    a.rho = rho; a.gamma = gamma;
+    a.px = make_prox(reg, mod, sh.C, rho, N0, Es);
+    a.md = modem_of(mod);
+    int NT;
+    if (fused_cfg(c, sh, &NT)) {
+        // a4-a8 fused: all T iterations with X_c on chip (world == 1)
+        a.NT = NT; a.CCH = sh.C_loc;
+        KL(launch_admm_fused(L, sh.UP, a));
+        c->consensus_rounds += T;
+    } else {
+        int CCH;
+        split_cfg(sh, &NT, &CCH);
+        a.NT = NT; a.CCH = CCH;
+        const size_t nw = (size_t)sh.N * sh.J * sh.UP;
+        for (int t = 1; t <= T; ++t) {
+            a.init = (t == 1);
+            KL(launch_admm_step(L, sh.UP, a));                       // lines 12-18 (t = 1: line 10)
+            if ((st = allreduce(c, a.wbuf, nw, s))) return st;       // line 18 consensus
+        }
+        KL(launch_prox_out(L, sh.UP, a.wbuf, sh.N, sh.J, sh.U, a.px, a.md, a.s_hat, a.hard));  // line 19, output
+    }
+    return end_call(c, k, s);
+}
+
+// ============================================================ Algorithm 2
+extern "C" dbp_status dbp_detect_cg(dbp_ctx* c, const dbp_dims* d, const dbp_cf32* H, const dbp_cf32* y, float rho,
+                                    int mod, int32_t T, dbp_cf32* x_hat, uint8_t* hard, void* ws, size_t ws_bytes,
+                                    void* stream) {
+    Shape sh;
+    dbp_status st = check_dims(c, d, &sh);
+    if (st) return st;
+    if (!H || !y || !x_hat) return fail(DBP_ERR_INVALID_ARG, "H, y and x_hat are required");
+    if (!(rho >= 0.f) || !std::isfinite(rho)) return fail(DBP_ERR_INVALID_ARG, "rho must be >= 0 (P376)");
+    if (!mod_ok(mod)) return fail(DBP_ERR_INVALID_ARG, "mod %d", mod);
+    if (T < 1) return fail(DBP_ERR_INVALID_ARG, "T must be >= 1");
+    if (pre_smem(sh.UP, sh.S, sh.U, sh.J, PRE_CG_) > (size_t)c->max_smem) return fail(DBP_ERR_UNSUPPORTED, "S too large for the preprocessing tile");
+    CU(cudaSetDevice(c->device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const Layout Lw = layout(sh, DBP_ALGO_CG_UL);
+    Call k;
+    k.io[0] = {H, nullptr, (size_t)sh.pairs() * sh.S * sh.U * 8, nullptr};
+    k.io[1] = {y, nullptr, (size_t)sh.pairs() * sh.J * sh.S * 8, nullptr};
+    k.io[2] = {nullptr, x_hat, (size_t)sh.N * sh.J * sh.U * 8, nullptr};
+    k.io[3] = {nullptr, hard, hard ? (size_t)sh.N * sh.J * sh.U : 0, nullptr};
+    k.nio = 4;
+    if ((st = begin_call(c, k, Lw, ws, ws_bytes, s))) return st;
+    LaunchCtx L{s, c->d_flag, &c->launches};
+    float2* Gp = reinterpret_cast<float2*>(k.ws + Lw.off[0]);
+    float2* mf = reinterpret_cast<float2*>(k.ws + Lw.off[1]);
+    CgArgs a{};
+    a.Gloc = reinterpret_cast<float2*>(k.ws + Lw.off[2]);
+    a.wbuf = reinterpret_cast<float2*>(k.ws + Lw.off[3]);
+    a.x = reinterpret_cast<float2*>(k.ws + Lw.off[4]);
+    a.r = reinterpret_cast<float2*>(k.ws + Lw.off[5]);
+    a.p = reinterpret_cast<float2*>(k.ws + Lw.off[6]);
+    a.rr = reinterpret_cast<float*>(k.ws + Lw.off[7]);
+    a.x_hat = static_cast<float2*>(k.io[2].dev);
+    a.hard = static_cast<uint8_t*>(k.io[3].dev);
+    a.N = sh.N; a.J = sh.J; a.U = sh.U; a.T = T; a.rho = rho;
+    a.md = modem_of(mod);
+
+    // b1: per-pair Gram H_c^H H_c and matched filter H_c^H y_c, then the
+    // per-GPU sums (G_loc, local y^MRC) in fixed cluster order.
+    KL(launch_pre(L, sh.UP, PRE_CG_, static_cast<const float2*>(k.io[0].dev), static_cast<const float2*>(k.io[1].dev),
+                  sh.S, sh.U, sh.J, sh.pairs(), 0.f, Gp, mf));
+    KL(launch_cg_gsum(L, sh.UP, Gp, mf, sh.C_loc, sh.N, sh.J, const_cast<float2*>(a.Gloc), a.wbuf));
+    const size_t nw = (size_t)sh.N * sh.J * sh.UP;
+    if ((st = allreduce(c, a.wbuf, nw, s))) return st;              // line 4: y^MRC consensus
+    if (c->world == 1 && !c->force_split) {
+        KL(launch_cg_it(L, sh.UP, true, a));                          // lines 6-18, all T iterations
+        c->consensus_rounds += T;
+    } else {
+        for (int t = 0; t <= T; ++t) {
+            a.step = t;
+            KL(launch_cg_it(L, sh.UP, false, a));
+            if (t < T && (st = allreduce(c, a.wbuf, nw, s))) return st;   // line 11 consensus
+        }
+    }
+    return end_call(c, k, s);
+}
+
+// ============================================================ Algorithm 3
+extern "C" dbp_status dbp_beamform_admm(dbp_ctx* c, const dbp_dims* d, const dbp_cf32* Hd, const dbp_cf32* sv,
+                                        float rho, float gamma, float eps, int32_t T, dbp_cf32* x, void* ws,
+                                        size_t ws_bytes, void* stream) {
+    Shape sh;
+    dbp_status st = check_dims(c, d, &sh);
+    if (st) return st;
+    if (!Hd || !sv || !x) return fail(DBP_ERR_INVALID_ARG, "Hd, s and x are required");
+    if (!(rho > 0.f) || !std::isfinite(rho)) return fail(DBP_ERR_INVALID_ARG, "rho must be > 0");
+    if (!(gamma > 0.f) || !std::isfinite(gamma)) return fail(DBP_ERR_INVALID_ARG, "gamma must be > 0");
+    if (!(eps >= 0.f)) return fail(DBP_ERR_INVALID_ARG, "eps must be >= 0");
+    if (eps > 0.f) return fail(DBP_ERR_UNSUPPORTED, "eps > 0 (Lemma 2 shrink) is not in v1");
+    if (T < 1) return fail(DBP_ERR_INVALID_ARG, "T must be >= 1");
+    if (pre_smem(sh.UP, sh.S, sh.U, sh.J, PRE_BF_) > (size_t)c->max_smem) return fail(DBP_ERR_UNSUPPORTED, "S too large for the preprocessing tile");
+    CU(cudaSetDevice(c->device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const Layout Lw = layout(sh, DBP_ALGO_ADMM_DL);
+    Call k;
+    k.io[0] = {Hd, nullptr, (size_t)sh.pairs() * sh.S * sh.U * 8, nullptr};
+    k.io[1] = {sv, nullptr, (size_t)sh.N * sh.J * sh.U * 8, nullptr};
+    k.io[2] = {nullptr, x, (size_t)sh.pairs() * sh.J * sh.S * 8, nullptr};
+    k.nio = 3;
+    if ((st = begin_call(c, k, Lw, ws, ws_bytes, s))) return st;
+    LaunchCtx L{s, c->d_flag, &c->launches};
+    BfArgs a{};
+    a.Hd = static_cast<const float2*>(k.io[0].dev);
+    a.s = static_cast<const float2*>(k.io[1].dev);
+    a.X = reinterpret_cast<float2*>(k.ws + Lw.off[0]);
+    a.m = reinterpret_cast<float2*>(k.ws + Lw.off[1]);
+    a.lam = reinterpret_cast<float2*>(k.ws + Lw.off[2]);
+    a.wbuf = reinterpret_cast<float2*>(k.ws + Lw.off[3]);
+    a.xout = static_cast<float2*>(k.io[2].dev);
+    a.C_loc = sh.C_loc; a.C = sh.C; a.N = sh.N; a.J = sh.J; a.U = sh.U; a.S = sh.S; a.T = T;
+    a.rho_inv = (float)(1.0 / rho);
+    a.gamma = gamma;
+    a.a0 = (float)std::max((double)sh.U / ((double)sh.C * sh.S), 1.0 / sh.C);   // Alg. 3 line 8 (P507)
+    a.inv_c = (float)(1.0 / sh.C);
+
+    // c1: B_c = H_c H_c^H + rho^{-1} I_U, Cholesky inverse (Alg. 3 lines 2-6)
+    KL(launch_pre(L, sh.UP, PRE_BF_, a.Hd, nullptr, sh.S, sh.U, sh.J, sh.pairs(), a.rho_inv,
+                  const_cast<float2*>(a.X), nullptr));
+    int NT;
+    if (fused_cfg(c, sh, &NT)) {
+        a.NT = NT; a.CCH = sh.C_loc;
+        KL(launch_bf_fused(L, sh.UP, a));
+        c->consensus_rounds += T - 1;
+    } else {
+        int CCH;
+        split_cfg(sh, &NT, &CCH);
+        a.NT = NT; a.CCH = CCH;
+        const size_t nw = (size_t)sh.N * sh.J * sh.UP;
+        for (int t = 2; t <= T; ++t) {
+            a.step = t;
+            KL(launch_bf_step(L, sh.UP, a));                           // lines 11-12 (+14-15 of t-1)
+            if ((st = allreduce(c, a.wbuf, nw, s))) return st;         // line 13 consensus
+        }
+        a.step = T + 1;
+        KL(launch_bf_step(L, sh.UP, a));                               // output x_c^(T) (P525)
+    }
+    return end_call(c, k, s);
+}
+
+// ============================================================ utilities
+extern "C" dbp_status dbp_slice(dbp_ctx* c, int mod, int64_t count, const dbp_cf32* x, uint8_t* bits, void* stream) {
+    if (!c) return fail(DBP_ERR_INVALID_ARG, "ctx is NULL");
+    if (!mod_ok(mod)) return fail(DBP_ERR_INVALID_ARG, "mod %d", mod);
+    if (count < 0 || (count > 0 && (!x || !bits))) return fail(DBP_ERR_INVALID_ARG, "bad count/pointers");
+    if (count == 0) return DBP_OK;
+    CU(cudaSetDevice(c->device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Call k;
+    k.io[0] = {x, nullptr, (size_t)count * 8, nullptr};
+    k.io[1] = {nullptr, bits, (size_t)count, nullptr};
+    k.nio = 2;
+    Layout Lw{};
+    dbp_status st = begin_call(c, k, Lw, nullptr, 0, s);
+    if (st) return st;
+    LaunchCtx L{s, c->d_flag, &c->launches};
+    KL(launch_slice(L, static_cast<const float2*>(k.io[0].dev), count, modem_of(mod), static_cast<uint8_t*>(k.io[1].dev)));
+    return end_call(c, k, s);
+}
+
+extern "C" dbp_status dbp_sync(dbp_ctx* c, void* stream) {
+    if (!c) return fail(DBP_ERR_INVALID_ARG, "ctx is NULL");
+    CU(cudaSetDevice(c->device));
+    CU(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    int flag = 0;
+    CU(cudaMemcpy(&flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost));
+    if (flag) {
+        CU(cudaMemset(c->d_flag, 0, sizeof(int)));
+        return fail(DBP_ERR_NOT_HPD, "a Cholesky pivot was not positive/finite (non-HPD or non-finite input)");
+    }
+    CU(cudaGetLastError());
+    return DBP_OK;
+}

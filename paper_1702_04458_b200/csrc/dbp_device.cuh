@@ -1,0 +1,338 @@
+// dbp_device.cuh -- device building blocks of libdbp (sm_100a).
+//
+// Complex arithmetic on float2, packed-triangular indexing, the TMA bulk-copy
+// (cp.async.bulk + mbarrier) helpers, the per-pair dense linear algebra used
+// by the preprocessing kernels (Gram tiles, Cholesky, triangular inverse,
+// triangular mat-vecs) and the constellation slicer / proximal operators.
+//
+// A "pair" is one (cluster c, subcarrier n) of the paper's per-cluster,
+// per-subcarrier local problem (P149-155, P706).  Inside a CTA a pair is
+// served by a team of TPP consecutive threads of one warp; all teams of a
+// warp run the same phase in lock-step, so __syncwarp() orders them.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dbp {
+
+// ----------------------------------------------------------------- complex
+__device__ __forceinline__ float2 c_add(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 c_sub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 c_scale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__device__ __forceinline__ float2 c_conj(float2 a) { return make_float2(a.x, -a.y); }
+__device__ __forceinline__ float2 c_mul(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+// acc += a * b
+__device__ __forceinline__ void c_fma(float2& acc, float2 a, float2 b) {
+    acc.x = fmaf(a.x, b.x, acc.x); acc.x = fmaf(-a.y, b.y, acc.x);
+    acc.y = fmaf(a.x, b.y, acc.y); acc.y = fmaf(a.y, b.x, acc.y);
+}
+// acc += conj(a) * b
+__device__ __forceinline__ void c_fmac(float2& acc, float2 a, float2 b) {
+    acc.x = fmaf(a.x, b.x, acc.x); acc.x = fmaf(a.y, b.y, acc.x);
+    acc.y = fmaf(a.x, b.y, acc.y); acc.y = fmaf(-a.y, b.x, acc.y);
+}
+// acc += a * conj(b)
+__device__ __forceinline__ void c_fmacb(float2& acc, float2 a, float2 b) {
+    acc.x = fmaf(a.x, b.x, acc.x); acc.x = fmaf(a.y, b.y, acc.x);
+    acc.y = fmaf(a.y, b.x, acc.y); acc.y = fmaf(-a.x, b.y, acc.y);
+}
+__device__ __forceinline__ float c_norm2(float2 a) { return fmaf(a.x, a.x, a.y * a.y); }
+
+// Packed lower-triangular storage, row-major: (i, j), j <= i.
+__host__ __device__ constexpr int tri(int n) { return n * (n + 1) / 2; }
+__host__ __device__ __forceinline__ int pidx(int i, int j) { return (i * (i + 1)) / 2 + j; }
+
+// ------------------------------------------------------- TMA bulk copies
+// 1-D bulk tensor copy global -> shared, completion tracked by an mbarrier
+// (cp.async.bulk ... mbarrier::complete_tx::bytes; SASS UBLKCP).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;"
+                 ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+// ------------------------------------------------------------ constellation
+// Gray QAM with Es = 1 (reading 17): per-axis levels
+// (2k - (m-1)) / sqrt(norm).  The decision is taken in fp32 with explicit
+// round-to-nearest ops (no fma contraction), reading 19:
+// k = clamp(ceil((x*scale + m)/2) - 1, 0, m-1), ties toward the negative level.
+struct Modem { int m; int bpa; int naxes; float scale; float radius; };
+
+__host__ __device__ inline Modem modem_of(int mod) {
+    switch (mod) {
+        case 1: return {2, 1, 1, 1.0f, 1.0f};
+        case 2: return {2, 1, 2, 1.41421356f, 0.70710678f};
+        case 4: return {4, 2, 2, 3.16227766f, 0.94868330f};
+        default: return {8, 3, 2, 6.48074070f, 1.08012345f};
+    }
+}
+
+__device__ __forceinline__ unsigned slice_axis(float x, const Modem& md) {
+    float t = __fmul_rn(x, md.scale);
+    float u = __fmul_rn(__fadd_rn(t, (float)md.m), 0.5f);
+    float k = ceilf(u) - 1.0f;
+    if (!(k >= 0.0f)) return 0u;
+    if (k > (float)(md.m - 1)) return (unsigned)(md.m - 1);
+    return (unsigned)k;
+}
+__device__ __forceinline__ uint8_t slice_bits(float2 v, const Modem& md) {
+    unsigned ki = slice_axis(v.x, md);
+    unsigned gi = ki ^ (ki >> 1);
+    if (md.naxes == 1) return (uint8_t)gi;
+    unsigned kq = slice_axis(v.y, md);
+    unsigned gq = kq ^ (kq >> 1);
+    return (uint8_t)((gi << md.bpa) | gq);
+}
+
+// Proximal step (E2) applied to the consensus sum w (Lemma 1, P325-344):
+// MMSE: s = w / (N0/(rho Es) + C)  (Alg. 1 line 13), ZF: w / C,
+// BOX: per-axis clamp of w / C to [-r, r], BPSK: real clamp, imag 0.
+struct Prox { int reg; float inv_c; float mmse_scale; float r; int bpsk; };
+__device__ __forceinline__ float2 prox(float2 w, const Prox& p) {
+    if (p.reg == 0) return c_scale(w, p.mmse_scale);
+    float2 v = c_scale(w, p.inv_c);
+    if (p.reg == 1) return v;
+    v.x = fminf(fmaxf(v.x, -p.r), p.r);
+    v.y = p.bpsk ? 0.0f : fminf(fmaxf(v.y, -p.r), p.r);
+    return v;
+}
+
+// --------------------------------------------------- per-pair dense algebra
+// Work split of the packed lower triangle of a UP x UP Hermitian Gram matrix
+// into 4x4 tiles: NOFF strictly-lower off-diagonal tiles (a > b) plus NDIAG
+// jobs that each own two diagonal tiles (2e, 2e+1) -- or the single diagonal
+// tile when UP == 4.  Every job costs 64 real FMAs per antenna row (16
+// complex MACs, or 2 x (4 real + 6 complex) MACs), and off-diagonal and
+// diagonal jobs live in different warps, so no warp diverges.
+template <int UP>
+struct Tiles {
+    static constexpr int NB = UP / 4;
+    static constexpr int NOFF = NB * (NB - 1) / 2;
+    static constexpr int NDIAG = NB >= 2 ? NB / 2 : 1;
+};
+
+__device__ __forceinline__ void off_tile_coords(int q, int& a, int& b) {
+    a = 1;
+    while (q >= a) { q -= a; ++a; }
+    b = q;
+}
+
+// Row `s` of the per-pair channel tile in shared memory, 4 users starting at
+// u0.  UL: tile is S x U row-major (element (s,u) at s*U+u).  DL: tile is
+// U x S row-major (H^d, element (u,s) at u*S+s) and the Gram is formed on its
+// transpose.  FULL: U == UP (no padding mask, vector loads in UL).
+template <bool DL, bool FULL>
+__device__ __forceinline__ void load4(const float2* tile, int s, int u0, int U, int S, float2 (&v)[4]) {
+    if (!DL && FULL) {
+        const float4* p = reinterpret_cast<const float4*>(tile + s * U + u0);
+        float4 a = p[0], b = p[1];
+        v[0] = make_float2(a.x, a.y); v[1] = make_float2(a.z, a.w);
+        v[2] = make_float2(b.x, b.y); v[3] = make_float2(b.z, b.w);
+    } else {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            int u = u0 + r;
+            if (FULL || u < U) v[r] = DL ? tile[u * S + s] : tile[s * U + u];
+            else v[r] = make_float2(0.f, 0.f);
+        }
+    }
+}
+
+// Off-diagonal tile (a > b): G[4a+r][4b+c] = sum_s conj(h_s,4a+r) h_s,4b+c.
+template <bool DL, bool FULL>
+__device__ __forceinline__ void gram_off(const float2* tile, int S, int U, int a, int b, float2 (&acc)[16]) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc[k] = make_float2(0.f, 0.f);
+#pragma unroll 2
+    for (int s = 0; s < S; ++s) {
+        float2 A[4], B[4];
+        load4<DL, FULL>(tile, s, 4 * a, U, S, A);
+        load4<DL, FULL>(tile, s, 4 * b, U, S, B);
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) c_fmac(acc[r * 4 + c], A[r], B[c]);
+    }
+}
+
+// Two diagonal tiles d0, d1 (lower parts, real diagonals); d1 < 0 = none.
+// acc layout: [tile][10]: (r, c) with c <= r in row-major packed order.
+template <bool DL, bool FULL>
+__device__ __forceinline__ void gram_diag(const float2* tile, int S, int U, int d0, int d1, float2 (&acc)[20]) {
+#pragma unroll
+    for (int k = 0; k < 20; ++k) acc[k] = make_float2(0.f, 0.f);
+#pragma unroll 2
+    for (int s = 0; s < S; ++s) {
+        float2 A[4], B[4];
+        load4<DL, FULL>(tile, s, 4 * d0, U, S, A);
+        if (d1 >= 0) load4<DL, FULL>(tile, s, 4 * d1, U, S, B);
+        else { B[0] = B[1] = B[2] = B[3] = make_float2(0.f, 0.f); }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+#pragma unroll
+            for (int c = 0; c < r; ++c) {
+                c_fmac(acc[pidx(r, c)], A[r], A[c]);
+                c_fmac(acc[10 + pidx(r, c)], B[r], B[c]);
+            }
+            acc[pidx(r, r)].x = fmaf(A[r].x, A[r].x, fmaf(A[r].y, A[r].y, acc[pidx(r, r)].x));
+            acc[10 + pidx(r, r)].x = fmaf(B[r].x, B[r].x, fmaf(B[r].y, B[r].y, acc[10 + pidx(r, r)].x));
+        }
+    }
+}
+
+// Team-cooperative Cholesky B = L L^H in place on packed lower storage.
+// Returns false if a pivot is not positive and finite (the caller flags
+// DBP_ERR_NOT_HPD); the factorisation then continues with 0 scales so no
+// NaN/Inf is produced by the kernel itself.
+template <int UP, int TPP>
+__device__ __forceinline__ bool team_cholesky(float2* L, int t) {
+    bool ok = true;
+    for (int k = 0; k < UP; ++k) {
+        float d = L[pidx(k, k)].x;
+        bool good = (d > 0.f) && (d < INFINITY);
+        ok = ok && good;
+        float l = good ? sqrtf(d) : 0.f;
+        float il = good ? 1.0f / l : 0.f;
+        __syncwarp();
+        for (int i = k + 1 + t; i < UP; i += TPP) L[pidx(i, k)] = c_scale(L[pidx(i, k)], il);
+        if (t == 0) L[pidx(k, k)] = make_float2(l, 0.f);
+        __syncwarp();
+        // trailing update, rows paired (k+1+g, UP-1-g) for balance
+        const int m = UP - 1 - k;
+        for (int g = t; 2 * g < m; g += TPP) {
+            int r1 = k + 1 + g, r2 = UP - 1 - g;
+            float2 l1 = L[pidx(r1, k)];
+            for (int j = k + 1; j <= r1; ++j) c_fmacb(L[pidx(r1, j)], make_float2(-l1.x, -l1.y), L[pidx(j, k)]);
+            if (r2 != r1) {
+                float2 l2 = L[pidx(r2, k)];
+                for (int j = k + 1; j <= r2; ++j) c_fmacb(L[pidx(r2, j)], make_float2(-l2.x, -l2.y), L[pidx(j, k)]);
+            }
+        }
+        __syncwarp();
+    }
+    return ok;
+}
+
+// In-place triangular inverse X = L^{-1} (lower), row by row:
+// X[i][i] = 1/L[i][i], X[i][j] = -X[i][i] sum_{k=j}^{i-1} L[i][k] X[k][j].
+template <int UP, int TPP>
+__device__ __forceinline__ void team_tri_inverse(float2* L, int t) {
+    constexpr int NJ = (UP + TPP - 1) / TPP;
+    for (int i = 0; i < UP; ++i) {
+        float lii = L[pidx(i, i)].x;
+        float xii = lii > 0.f ? 1.0f / lii : 0.f;
+        float2 out[NJ];
+#pragma unroll
+        for (int q = 0; q < NJ; ++q) {
+            int j = t + q * TPP;
+            float2 acc = make_float2(0.f, 0.f);
+            if (j < i) {
+                for (int k = j; k < i; ++k) c_fma(acc, L[pidx(i, k)], L[pidx(k, j)]);
+                acc = c_scale(acc, -xii);
+            }
+            out[q] = acc;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < NJ; ++q) {
+            int j = t + q * TPP;
+            if (j < i) L[pidx(i, j)] = out[q];
+        }
+        if (t == 0) L[pidx(i, i)] = make_float2(xii, 0.f);
+        __syncwarp();
+    }
+}
+
+// Row ownership for triangular mat-vecs: a row pair {g, UP-1-g} has UP+1
+// terms in both X v and X^H v.  TR threads share a row pair (split terms),
+// each thread owns RPT row pairs.
+template <int UP, int TPP>
+struct RowMap {
+    static constexpr int RP = UP / 2;
+    static constexpr int TR = TPP > RP ? TPP / RP : 1;   // threads per row pair
+    static constexpr int RPT = RP > TPP ? RP / TPP : 1;  // row pairs per thread
+    static constexpr int NR = 2 * RPT;                   // rows owned per thread
+    __device__ static int row(int t, int k) {            // k-th owned row of thread t
+        int g = (t / TR) * RPT + (k >> 1);
+        return (k & 1) ? (UP - 1 - g) : g;
+    }
+    __device__ static int sub(int t) { return t % TR; }
+};
+
+// out_r = sum_{k<=r} X[r][k] v_k for the owned rows (team-local).
+template <int UP, int TPP>
+__device__ __forceinline__ void tri_mv(const float2* X, const float2* v, int t, float2 (&out)[RowMap<UP, TPP>::NR]) {
+    using RM = RowMap<UP, TPP>;
+    const int sb = RM::sub(t);
+#pragma unroll
+    for (int k = 0; k < RM::NR; ++k) {
+        int r = RM::row(t, k);
+        float2 acc = make_float2(0.f, 0.f);
+        for (int j = sb; j <= r; j += RM::TR) c_fma(acc, X[pidx(r, j)], v[j]);
+        if (RM::TR > 1) {
+#pragma unroll
+            for (int o = 1; o < RM::TR; o <<= 1) {
+                acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+                acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+            }
+        }
+        out[k] = acc;
+    }
+}
+
+// out_r = sum_{k>=r} conj(X[k][r]) v_k for the owned rows (X^H v).
+template <int UP, int TPP>
+__device__ __forceinline__ void tri_mv_h(const float2* X, const float2* v, int t, float2 (&out)[RowMap<UP, TPP>::NR]) {
+    using RM = RowMap<UP, TPP>;
+    const int sb = RM::sub(t);
+#pragma unroll
+    for (int k = 0; k < RM::NR; ++k) {
+        int r = RM::row(t, k);
+        float2 acc = make_float2(0.f, 0.f);
+        for (int j = r + sb; j < UP; j += RM::TR) c_fmac(acc, X[pidx(j, r)], v[j]);
+        if (RM::TR > 1) {
+#pragma unroll
+            for (int o = 1; o < RM::TR; o <<= 1) {
+                acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+                acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+            }
+        }
+        out[k] = acc;
+    }
+}
+
+// Hermitian mat-vec with a packed lower Hermitian matrix G (row r of G v).
+template <int UP>
+__device__ __forceinline__ float2 herm_mv_row(const float2* G, const float2* v, int r) {
+    float2 acc = make_float2(0.f, 0.f);
+    for (int j = 0; j <= r; ++j) c_fma(acc, G[pidx(r, j)], v[j]);
+    for (int j = r + 1; j < UP; ++j) c_fmac(acc, G[pidx(j, r)], v[j]);
+    return acc;
+}
+
+}  // namespace dbp

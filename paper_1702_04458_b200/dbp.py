@@ -1,0 +1,242 @@
+"""ctypes binding of libdbp (include/dbp.h) -- argument marshalling only.
+
+Every step of the hot path runs in libdbp's sm_100a kernels; this module
+converts torch tensors (device pointers, the caller's current CUDA stream) or
+numpy arrays (host pointers, staged by the library inside the call) into the
+C-ABI arguments and raises ``DbpError`` on a non-OK status.  There is no CPU
+fallback: if ``libdbp.so`` is missing or no GPU is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdbp.so")
+
+STATUS = {0: "DBP_OK", 1: "DBP_ERR_INVALID_ARG", 2: "DBP_ERR_UNSUPPORTED", 3: "DBP_ERR_NOT_HPD",
+          4: "DBP_ERR_CUDA", 5: "DBP_ERR_NCCL", 6: "DBP_ERR_WORKSPACE"}
+REG = {"mmse": 0, "zf": 1, "box": 2}
+MOD = {"bpsk": 1, "qpsk": 2, "qam16": 4, "qam64": 6}
+ALGO = {"admm_ul": 0, "cg_ul": 1, "admm_dl": 2}
+OPT_FORCE_SPLIT = 1
+
+EXPORTS = ["dbp_get_unique_id", "dbp_ctx_create", "dbp_ctx_destroy", "dbp_set_option", "dbp_get_stats",
+           "dbp_last_error", "dbp_workspace_bytes", "dbp_detect_admm", "dbp_detect_cg",
+           "dbp_beamform_admm", "dbp_slice", "dbp_sync"]
+
+
+class DbpError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Dims(ctypes.Structure):
+    _fields_ = [("C", ctypes.c_int32), ("S", ctypes.c_int32), ("U", ctypes.c_int32),
+                ("N", ctypes.c_int32), ("N_sym", ctypes.c_int32)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("allreduce_calls", ctypes.c_int64), ("allreduce_bytes", ctypes.c_int64),
+                ("kernel_launches", ctypes.c_int64), ("consensus_rounds", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libdbp.so (raises if it was not built; no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise DbpError(4, f"{LIB_PATH} not built (run __graft_entry__.build())")
+    lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+    P, I, F = ctypes.c_void_p, ctypes.c_int, ctypes.c_float
+    S, I64 = ctypes.c_size_t, ctypes.c_int64
+    sigs = {
+        "dbp_get_unique_id": [P],
+        "dbp_ctx_create": [P, I, I, I, P],
+        "dbp_ctx_destroy": [P],
+        "dbp_set_option": [P, I, I64],
+        "dbp_get_stats": [P, P],
+        "dbp_workspace_bytes": [P, P, I, P],
+        "dbp_detect_admm": [P, P, P, P, F, F, F, F, I, I, ctypes.c_int32, P, P, P, S, P],
+        "dbp_detect_cg": [P, P, P, P, F, I, ctypes.c_int32, P, P, P, S, P],
+        "dbp_beamform_admm": [P, P, P, P, F, F, F, ctypes.c_int32, P, P, S, P],
+        "dbp_slice": [P, I, I64, P, P, P],
+        "dbp_sync": [P, P],
+    }
+    for name, args in sigs.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    lib.dbp_last_error.argtypes = []
+    lib.dbp_last_error.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def _check(st: int):
+    if st != 0:
+        raise DbpError(st, load().dbp_last_error().decode())
+
+
+def get_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(load().dbp_get_unique_id(buf))
+    return bytes(buf)
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if _is_torch(x):
+        return ctypes.c_void_p(x.data_ptr())
+    return x.ctypes.data_as(ctypes.c_void_p)
+
+
+def _stream(stream, ref):
+    if stream is not None:
+        return ctypes.c_void_p(int(stream))
+    if ref is not None and _is_torch(ref) and ref.is_cuda:
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream(ref.device).cuda_stream)
+    return ctypes.c_void_p(0)
+
+
+def _empty_like_io(ref, shape, kind):
+    """Output buffer on the same side (device tensor / host array) as `ref`."""
+    if _is_torch(ref):
+        import torch
+        dt = torch.complex64 if kind == "c" else torch.uint8
+        return torch.empty(shape, dtype=dt, device=ref.device)
+    return np.empty(shape, dtype=np.complex64 if kind == "c" else np.uint8)
+
+
+def _need_contig(*xs):
+    for x in xs:
+        if x is None:
+            continue
+        ok = x.is_contiguous() if _is_torch(x) else x.flags["C_CONTIGUOUS"]
+        dt = str(x.dtype)
+        if not ok:
+            raise ValueError("arrays must be contiguous")
+        if "complex64" not in dt and "uint8" not in dt:
+            raise ValueError(f"complex64 (or uint8) required, got {dt}")
+
+
+class Context:
+    """One libdbp context (one per rank); NCCL communicator when world > 1."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, unique_id: bytes | None = None):
+        lib = load()
+        self._h = ctypes.c_void_p()
+        uid = None
+        if unique_id is not None:
+            uid = (ctypes.c_uint8 * 128).from_buffer_copy(unique_id)
+        _check(lib.dbp_ctx_create(ctypes.byref(self._h), device, rank, world, uid))
+        self.device, self.rank, self.world = device, rank, world
+
+    def close(self):
+        if self._h:
+            load().dbp_ctx_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_option(self, opt: int, value: int):
+        _check(load().dbp_set_option(self._h, opt, value))
+
+    def stats(self) -> dict:
+        s = Stats()
+        _check(load().dbp_get_stats(self._h, ctypes.byref(s)))
+        return {k: getattr(s, k) for k, _ in Stats._fields_}
+
+    def workspace_bytes(self, C, S, U, N, N_sym, algo: str) -> int:
+        d = Dims(C, S, U, N, N_sym)
+        out = ctypes.c_size_t()
+        _check(load().dbp_workspace_bytes(self._h, ctypes.byref(d), ALGO[algo], ctypes.byref(out)))
+        return out.value
+
+    def sync(self, stream=None):
+        _check(load().dbp_sync(self._h, _stream(stream, None) if stream is not None else _cur_stream()))
+
+
+def _cur_stream():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    except Exception:
+        pass
+    return ctypes.c_void_p(0)
+
+
+def detect_admm(ctx: Context, H, y, *, rho=1.0, gamma=1.0, N0=0.0, Es=1.0, reg="mmse", mod="qam64", T=5,
+                s_hat=None, hard=None, want_hard=True, ws=None, stream=None):
+    """Algorithm 1.  H [C_loc][N][S][U], y [C_loc][N][N_sym][S] -> (s_hat [N][N_sym][U], hard)."""
+    C_loc, N, S, U = H.shape
+    J = y.shape[2]
+    if s_hat is None:
+        s_hat = _empty_like_io(H, (N, J, U), "c")
+    if hard is None and want_hard:
+        hard = _empty_like_io(H, (N, J, U), "u")
+    _need_contig(H, y, s_hat, hard)
+    d = Dims(C_loc * ctx.world, S, U, N, J)
+    wsb = 0 if ws is None else (ws.numel() * ws.element_size() if _is_torch(ws) else ws.nbytes)
+    _check(load().dbp_detect_admm(ctx._h, ctypes.byref(d), _ptr(H), _ptr(y), rho, gamma, N0, Es, REG[reg],
+                                  MOD[mod], T, _ptr(s_hat), _ptr(hard), _ptr(ws), wsb, _stream(stream, H)))
+    return s_hat, hard
+
+
+def detect_cg(ctx: Context, H, y, *, rho=0.0, mod="qam64", T=5, x_hat=None, hard=None, want_hard=True,
+              ws=None, stream=None):
+    """Algorithm 2.  -> (x_hat [N][N_sym][U], hard)."""
+    C_loc, N, S, U = H.shape
+    J = y.shape[2]
+    if x_hat is None:
+        x_hat = _empty_like_io(H, (N, J, U), "c")
+    if hard is None and want_hard:
+        hard = _empty_like_io(H, (N, J, U), "u")
+    _need_contig(H, y, x_hat, hard)
+    d = Dims(C_loc * ctx.world, S, U, N, J)
+    wsb = 0 if ws is None else (ws.numel() * ws.element_size() if _is_torch(ws) else ws.nbytes)
+    _check(load().dbp_detect_cg(ctx._h, ctypes.byref(d), _ptr(H), _ptr(y), rho, MOD[mod], T, _ptr(x_hat),
+                                _ptr(hard), _ptr(ws), wsb, _stream(stream, H)))
+    return x_hat, hard
+
+
+def beamform_admm(ctx: Context, Hd, s, *, rho=1.0, gamma=1.0, eps=0.0, T=5, x=None, ws=None, stream=None):
+    """Algorithm 3.  Hd [C_loc][N][U][S], s [N][N_sym][U] -> x [C_loc][N][N_sym][S]."""
+    C_loc, N, U, S = Hd.shape
+    J = s.shape[1]
+    if x is None:
+        x = _empty_like_io(Hd, (C_loc, N, J, S), "c")
+    _need_contig(Hd, s, x)
+    d = Dims(C_loc * ctx.world, S, U, N, J)
+    wsb = 0 if ws is None else (ws.numel() * ws.element_size() if _is_torch(ws) else ws.nbytes)
+    _check(load().dbp_beamform_admm(ctx._h, ctypes.byref(d), _ptr(Hd), _ptr(s), rho, gamma, eps, T, _ptr(x),
+                                    _ptr(ws), wsb, _stream(stream, Hd)))
+    return x
+
+
+def slice_bits(ctx: Context, x, mod: str, out=None, stream=None):
+    """Hard slicer (P210) on device or host complex64 data."""
+    if out is None:
+        out = _empty_like_io(x, tuple(x.shape), "u")
+    _need_contig(x, out)
+    n = x.numel() if _is_torch(x) else x.size
+    _check(load().dbp_slice(ctx._h, MOD[mod], n, _ptr(x), _ptr(out), _stream(stream, x)))
+    return out

@@ -1,0 +1,66 @@
+"""C-ABI library: builds, loads and exports every symbol include/dbp.h declares
+(no compute calls without a GPU); host-side validation paths that need no
+device."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "dbp.h")).read()
+    return sorted(set(re.findall(r"^(?:dbp_status|const char\*)\s+(dbp_\w+)\s*\(", src, re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1702_04458_b200 import build, dbp
+    build.build()
+    return dbp.load()
+
+
+def test_header_declares_expected_api():
+    syms = declared_symbols()
+    for s in ["dbp_detect_admm", "dbp_detect_cg", "dbp_beamform_admm", "dbp_ctx_create", "dbp_sync",
+              "dbp_workspace_bytes", "dbp_get_unique_id", "dbp_last_error", "dbp_slice"]:
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(lib):
+    from paper_1702_04458_b200 import dbp
+    for s in declared_symbols():
+        assert hasattr(lib, s), s
+    assert sorted(dbp.EXPORTS) == declared_symbols()
+
+
+def test_library_is_sm100a(lib):
+    import subprocess
+    from paper_1702_04458_b200 import dbp
+    out = subprocess.run(["cuobjdump", "--list-elf", dbp.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_null_context_is_rejected_without_gpu(lib):
+    from paper_1702_04458_b200 import dbp
+    d = dbp.Dims(2, 16, 4, 16, 1)
+    out = ctypes.c_size_t()
+    assert lib.dbp_workspace_bytes(None, ctypes.byref(d), 0, ctypes.byref(out)) == 1
+    assert b"ctx" in lib.dbp_last_error()
+    assert lib.dbp_detect_admm(None, ctypes.byref(d), None, None, 1.0, 1.0, 0.1, 1.0, 0, 2, 5,
+                               None, None, None, 0, None) == 1
+    assert lib.dbp_sync(None, None) == 1
+    assert lib.dbp_get_unique_id(None) == 1
+
+
+def test_product_package_does_not_import_oracle():
+    """The product path never touches oracle/ (DESIGN.md section 4)."""
+    pkg = os.path.join(ROOT, "paper_1702_04458_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, f
+                assert "dbp_oracle" not in txt, f

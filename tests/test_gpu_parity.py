@@ -1,0 +1,329 @@
+"""GPU parity: libdbp (through the C ABI) vs the fp64 oracle, element by element.
+
+Bar (BASELINE.json north star): relative L2 <= 1e-4 on
+soft outputs; hard decisions bit-exact except where the oracle's soft value is
+within tau = 1e-3 d_min of a decision boundary (reading 20).  Small cases run
+the whole oracle; BASELINE full-size configurations compare sampled
+subcarriers (the oracle is independent per subcarrier).
+"""
+import numpy as np
+import pytest
+
+from paper_1702_04458_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import oracle
+    from paper_1702_04458_b200 import dbp
+    ctx = dbp.Context(device=0)
+    yield dbp, ctx, oracle, torch
+    ctx.close()
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-30))
+
+
+_LV = {"bpsk": (2, 1.0), "qpsk": (2, 2.0), "qam16": (4, 10.0), "qam64": (8, 42.0)}
+
+
+def check_hard(hard_gpu, hard_ref, soft_ref, mod):
+    """Bit-exact except at ties (oracle value within 1e-3 d_min of a boundary)."""
+    mism = np.nonzero(hard_gpu != hard_ref)
+    if len(mism[0]) == 0:
+        return 0
+    m, norm = _LV[mod]
+    dmin = 2.0 / np.sqrt(norm)
+    tau = 1e-3 * dmin
+    v = soft_ref[mism]
+    def near(x):
+        t = x * np.sqrt(norm)              # boundaries at even integers in |t| < m-1
+        b = 2 * np.round(t / 2)
+        return (np.abs(t - b) * (1 / np.sqrt(norm)) < tau) & (np.abs(b) <= m - 2)
+    ok = near(v.real) | near(v.imag)
+    assert ok.all(), f"{(~ok).sum()} hard mismatches away from decision boundaries"
+    return int(len(v))
+
+
+def run_admm(env, cfg, split=False, reg="mmse", T=None, host=False):
+    dbp, ctx, oracle, torch = env
+    T = cfg.T if T is None else T
+    H, y, _ = synth.uplink_frame(cfg)
+    ctx.set_option(dbp.OPT_FORCE_SPLIT, int(split))
+    if host:
+        s, hard = dbp.detect_admm(ctx, H, y, rho=cfg.rho, N0=cfg.N0, reg=reg, mod=cfg.mod, T=T)
+    else:
+        s, hard = dbp.detect_admm(ctx, torch.from_numpy(H).cuda(), torch.from_numpy(y).cuda(), rho=cfg.rho,
+                                  N0=cfg.N0, reg=reg, mod=cfg.mod, T=T)
+        ctx.sync()
+        s, hard = s.cpu().numpy(), hard.cpu().numpy()
+    ctx.set_option(dbp.OPT_FORCE_SPLIT, 0)
+    s_ref, hard_ref = oracle.detect_admm(H, y, rho=cfg.rho, N0=cfg.N0, reg=reg, mod=cfg.mod, T=T)
+    return s, hard, s_ref, hard_ref
+
+
+SMALL_UL = [
+    synth.CONFIGS["A"],
+    synth.CONFIGS["C"].scaled(N=40),                          # C, S, U as config C, ragged tiles
+    synth.CONFIGS["C"].scaled(N=9, C=4),
+    synth.CONFIGS["E"].scaled(N=5, C=8),                      # U = 32
+    synth.CONFIGS["B"].scaled(N=33, mod="qam16"),
+    synth.Config("odd", "admm_ul", C=3, S=7, U=5, N=11, mod="qam16", snr_db=20),   # padding, S*U odd
+    synth.Config("s<u", "admm_ul", C=4, S=4, U=12, N=6, mod="qpsk", snr_db=15),    # S < U
+    synth.Config("nsym", "admm_ul", C=2, S=16, U=8, N=10, N_sym=3, mod="qam64", snr_db=30),
+    synth.Config("u20", "admm_ul", C=2, S=24, U=20, N=7, mod="qam16", snr_db=25),
+]
+
+
+@pytest.mark.parametrize("cfg", SMALL_UL, ids=lambda c: f"{c.name}-C{c.C}S{c.S}U{c.U}N{c.N}J{c.N_sym}")
+@pytest.mark.parametrize("split", [False, True], ids=["fused", "split"])
+def test_admm_parity(env, cfg, split):
+    s, hard, s_ref, hard_ref = run_admm(env, cfg, split)
+    assert rel(s, s_ref) < TOL
+    check_hard(hard, hard_ref, s_ref, cfg.mod)
+
+
+@pytest.mark.parametrize("reg", ["zf", "box"])
+@pytest.mark.parametrize("T", [1, 2, 9])
+def test_admm_regs_and_T(env, reg, T):
+    cfg = synth.Config("r", "admm_ul", C=4, S=8, U=8, N=12, mod="qpsk", snr_db=5)
+    for split in (False, True):
+        s, hard, s_ref, hard_ref = run_admm(env, cfg, split, reg=reg, T=T)
+        assert rel(s, s_ref) < TOL
+        check_hard(hard, hard_ref, s_ref, cfg.mod)
+
+
+def test_admm_bpsk_box(env):
+    cfg = synth.Config("bpsk", "admm_ul", C=2, S=8, U=4, N=8, mod="bpsk", snr_db=5)
+    s, hard, s_ref, hard_ref = run_admm(env, cfg, False, reg="box", T=6)
+    assert rel(s, s_ref) < TOL
+    assert np.all(s.imag == 0)
+    check_hard(hard, hard_ref, s_ref, "bpsk")
+
+
+def test_admm_host_pointers_match_device(env):
+    cfg = synth.CONFIGS["C"].scaled(N=12)
+    s_h, hard_h, s_ref, _ = run_admm(env, cfg, host=True)
+    s_d, hard_d, _, _ = run_admm(env, cfg, host=False)
+    assert np.array_equal(s_h, s_d) and np.array_equal(hard_h, hard_d)
+    assert rel(s_h, s_ref) < TOL
+
+
+def run_cg(env, cfg, split=False, T=None):
+    dbp, ctx, oracle, torch = env
+    T = cfg.T if T is None else T
+    H, y, _ = synth.uplink_frame(cfg)
+    ctx.set_option(dbp.OPT_FORCE_SPLIT, int(split))
+    x, hard = dbp.detect_cg(ctx, torch.from_numpy(H).cuda(), torch.from_numpy(y).cuda(), rho=cfg.N0,
+                            mod=cfg.mod, T=T)
+    ctx.sync()
+    ctx.set_option(dbp.OPT_FORCE_SPLIT, 0)
+    x_ref, hard_ref = oracle.detect_cg(H, y, rho=cfg.N0, mod=cfg.mod, T=T)
+    return x.cpu().numpy(), hard.cpu().numpy(), x_ref, hard_ref
+
+
+SMALL_CG = [
+    synth.CONFIGS["B"].scaled(N=37),
+    synth.CONFIGS["C"].scaled(N=9, mod="qam64"),
+    synth.CONFIGS["E"].scaled(N=4, C=8),
+    synth.CONFIGS["A"],
+    synth.Config("odd", "cg_ul", C=3, S=7, U=5, N=11, mod="qam16", snr_db=20),
+    synth.Config("nsym", "cg_ul", C=2, S=16, U=8, N=10, N_sym=4, mod="qam64", snr_db=30),
+]
+
+
+@pytest.mark.parametrize("cfg", SMALL_CG, ids=lambda c: f"{c.name}-C{c.C}S{c.S}U{c.U}N{c.N}J{c.N_sym}")
+@pytest.mark.parametrize("split", [False, True], ids=["fused", "split"])
+def test_cg_parity(env, cfg, split):
+    x, hard, x_ref, hard_ref = run_cg(env, cfg, split)
+    assert rel(x, x_ref) < TOL
+    check_hard(hard, hard_ref, x_ref, cfg.mod)
+
+
+@pytest.mark.parametrize("T", [1, 2, 16])
+def test_cg_iteration_counts(env, T):
+    cfg = synth.CONFIGS["B"].scaled(N=20)
+    for split in (False, True):
+        x, _, x_ref, _ = run_cg(env, cfg, split, T=T)
+        assert rel(x, x_ref) < TOL
+
+
+def test_cg_zero_input(env):
+    dbp, ctx, oracle, torch = env
+    cfg = synth.CONFIGS["B"].scaled(N=8)
+    H, y, _ = synth.uplink_frame(cfg)
+    x, _ = dbp.detect_cg(ctx, torch.from_numpy(H).cuda(), torch.zeros(y.shape, dtype=torch.complex64, device="cuda"),
+                         rho=0.1, mod=cfg.mod, T=3)
+    ctx.sync()
+    assert torch.all(x == 0)
+
+
+def run_bf(env, cfg, split=False, T=None):
+    dbp, ctx, oracle, torch = env
+    T = cfg.T if T is None else T
+    Hd, s = synth.downlink_frame(cfg)
+    ctx.set_option(dbp.OPT_FORCE_SPLIT, int(split))
+    x = dbp.beamform_admm(ctx, torch.from_numpy(Hd).cuda(), torch.from_numpy(s).cuda(), rho=cfg.rho, T=T)
+    ctx.sync()
+    ctx.set_option(dbp.OPT_FORCE_SPLIT, 0)
+    x_ref = oracle.beamform_admm(Hd, s, rho=cfg.rho, T=T)
+    return x.cpu().numpy(), x_ref
+
+
+SMALL_DL = [
+    synth.CONFIGS["D"].scaled(N=40),
+    synth.CONFIGS["D"].scaled(N=9, C=4),
+    synth.CONFIGS["E"].scaled(N=4, C=8, algo="admm_dl"),
+    synth.CONFIGS["A"].scaled(algo="admm_dl"),
+    synth.Config("odd", "admm_dl", C=3, S=7, U=5, N=11, mod="qam16"),
+    synth.Config("s<u", "admm_dl", C=4, S=4, U=12, N=6, mod="qpsk"),
+    synth.Config("nsym", "admm_dl", C=2, S=16, U=8, N=10, N_sym=3, mod="qam64"),
+]
+
+
+@pytest.mark.parametrize("cfg", SMALL_DL, ids=lambda c: f"{c.name}-C{c.C}S{c.S}U{c.U}N{c.N}J{c.N_sym}")
+@pytest.mark.parametrize("split", [False, True], ids=["fused", "split"])
+def test_bf_parity(env, cfg, split):
+    x, x_ref = run_bf(env, cfg, split)
+    assert rel(x, x_ref) < TOL
+
+
+@pytest.mark.parametrize("T", [1, 2, 12])
+def test_bf_iteration_counts(env, T):
+    cfg = synth.CONFIGS["D"].scaled(N=10, C=8)
+    for split in (False, True):
+        x, x_ref = run_bf(env, cfg, split, T=T)
+        assert rel(x, x_ref) < TOL
+
+
+def test_consensus_round_counts(env):
+    """ADMM-UL T, CG T+1, ADMM-DL T-1 consensus rounds per call (SPEC S389-390)."""
+    dbp, ctx, oracle, torch = env
+    cfg = synth.CONFIGS["A"]
+    H, y, _ = synth.uplink_frame(cfg)
+    Hd, s = synth.downlink_frame(cfg)
+    Hg, yg = torch.from_numpy(H).cuda(), torch.from_numpy(y).cuda()
+    for split in (0, 1):
+        ctx.set_option(dbp.OPT_FORCE_SPLIT, split)
+        for T in (1, 4):
+            r0 = ctx.stats()["consensus_rounds"]
+            dbp.detect_admm(ctx, Hg, yg, N0=cfg.N0, mod=cfg.mod, T=T)
+            r1 = ctx.stats()["consensus_rounds"]
+            dbp.detect_cg(ctx, Hg, yg, rho=cfg.N0, mod=cfg.mod, T=T)
+            r2 = ctx.stats()["consensus_rounds"]
+            dbp.beamform_admm(ctx, torch.from_numpy(Hd).cuda(), torch.from_numpy(s).cuda(), T=T)
+            r3 = ctx.stats()["consensus_rounds"]
+            assert (r1 - r0, r2 - r1, r3 - r2) == (T, T + 1, T - 1)
+    ctx.set_option(dbp.OPT_FORCE_SPLIT, 0)
+    ctx.sync()
+
+
+def test_slicer_bit_exact(env):
+    """Device slicer == oracle slicer on identical fp32 inputs (incl. exact boundaries)."""
+    dbp, ctx, oracle, torch = env
+    rng = np.random.default_rng(3)
+    for mod, (m, norm) in _LV.items():
+        x = (rng.standard_normal(50000) + 1j * rng.standard_normal(50000)) * 0.9
+        b = (2 * rng.integers(-(m // 2), m // 2 + 1, 2000)) / np.sqrt(norm)     # exact boundaries
+        x = np.concatenate([x, b + 1j * b[::-1], [0, np.nan, np.inf, -np.inf]]).astype(np.complex64)
+        got = dbp.slice_bits(ctx, torch.from_numpy(x).cuda(), mod).cpu().numpy()
+        assert np.array_equal(got, oracle.slice_bits(x, mod)), mod
+
+
+def test_not_hpd_flag(env):
+    dbp, ctx, oracle, torch = env
+    cfg = synth.CONFIGS["A"]
+    H, y, _ = synth.uplink_frame(cfg)
+    H[1, 3, 2, 1] = np.nan
+    dbp.detect_admm(ctx, torch.from_numpy(H).cuda(), torch.from_numpy(y).cuda(), N0=cfg.N0, mod=cfg.mod, T=2)
+    with pytest.raises(dbp.DbpError) as ei:
+        ctx.sync()
+    assert ei.value.status == 3
+    ctx.sync()   # flag cleared
+
+
+def test_invalid_arguments(env):
+    dbp, ctx, oracle, torch = env
+    cfg = synth.CONFIGS["A"]
+    H, y, _ = synth.uplink_frame(cfg)
+    Hg, yg = torch.from_numpy(H).cuda(), torch.from_numpy(y).cuda()
+    for kw in (dict(rho=0.0), dict(rho=-1.0), dict(gamma=0.0), dict(T=0), dict(Es=0.0), dict(N0=-1.0)):
+        with pytest.raises(dbp.DbpError) as ei:
+            dbp.detect_admm(ctx, Hg, yg, mod="qpsk", **kw)
+        assert ei.value.status == 1
+    with pytest.raises(dbp.DbpError) as ei:
+        dbp.detect_cg(ctx, Hg, yg, rho=-0.5, mod="qpsk")
+    assert ei.value.status == 1
+    Hd, s = synth.downlink_frame(cfg)
+    with pytest.raises(dbp.DbpError) as ei:
+        dbp.beamform_admm(ctx, torch.from_numpy(Hd).cuda(), torch.from_numpy(s).cuda(), eps=0.1)
+    assert ei.value.status == 2
+    big = torch.zeros((1, 2, 4, 33), dtype=torch.complex64, device="cuda")
+    with pytest.raises(dbp.DbpError) as ei:
+        dbp.detect_admm(ctx, big, torch.zeros((1, 2, 1, 4), dtype=torch.complex64, device="cuda"))
+    assert ei.value.status == 2
+
+
+# ------------------------------------------------------- full BASELINE sizes
+@pytest.mark.parametrize("name", ["B", "C", "D"])
+def test_full_size_sampled(env, name):
+    """BASELINE configs at full size in the bench launch configuration; the
+    oracle checks 24 sampled subcarriers (each subcarrier is independent)."""
+    dbp, ctx, oracle, torch = env
+    cfg = synth.CONFIGS[name]
+    rng = np.random.default_rng(7)
+    ns = np.sort(rng.choice(cfg.N, 24, replace=False))
+    if cfg.algo == "admm_dl":
+        Hd, s = synth.downlink_frame(cfg)
+        x = dbp.beamform_admm(ctx, torch.from_numpy(Hd).cuda(), torch.from_numpy(s).cuda(), rho=cfg.rho, T=cfg.T)
+        ctx.sync()
+        x = x.cpu().numpy()[:, ns]
+        x_ref = oracle.beamform_admm(Hd[:, ns], s[ns], rho=cfg.rho, T=cfg.T)
+        assert rel(x, x_ref) < TOL
+        return
+    H, y, _ = synth.uplink_frame(cfg)
+    Hg, yg = torch.from_numpy(H).cuda(), torch.from_numpy(y).cuda()
+    for algo in ("admm", "cg"):
+        if algo == "admm":
+            out, hard = dbp.detect_admm(ctx, Hg, yg, rho=cfg.rho, N0=cfg.N0, mod=cfg.mod, T=cfg.T)
+            ref, hard_ref = oracle.detect_admm(H[:, ns], y[:, ns], rho=cfg.rho, N0=cfg.N0, mod=cfg.mod, T=cfg.T)
+        else:
+            out, hard = dbp.detect_cg(ctx, Hg, yg, rho=cfg.N0, mod=cfg.mod, T=cfg.T)
+            ref, hard_ref = oracle.detect_cg(H[:, ns], y[:, ns], rho=cfg.N0, mod=cfg.mod, T=cfg.T)
+        ctx.sync()
+        out = out.cpu().numpy()[ns]
+        assert rel(out, ref) < TOL, algo
+        check_hard(hard.cpu().numpy()[ns], hard_ref, ref, cfg.mod)
+
+
+def test_config_E_shape_sampled(env):
+    """Config E cluster/user shape (C=128, S=32, U=32) on a 48-subcarrier slice."""
+    dbp, ctx, oracle, torch = env
+    cfg = synth.CONFIGS["E"]
+    H, y, _ = synth.uplink_frame(cfg, n0=0, n1=48)
+    sub = cfg.scaled(N=48)
+    Hg, yg = torch.from_numpy(H).cuda(), torch.from_numpy(y).cuda()
+    ns = np.arange(0, 48, 6)
+    out, hard = dbp.detect_admm(ctx, Hg, yg, rho=sub.rho, N0=sub.N0, mod=sub.mod, T=sub.T)
+    out2, hard2 = dbp.detect_cg(ctx, Hg, yg, rho=sub.N0, mod=sub.mod, T=sub.T)
+    ctx.sync()
+    ref, hard_ref = oracle.detect_admm(H[:, ns], y[:, ns], rho=sub.rho, N0=sub.N0, mod=sub.mod, T=sub.T)
+    ref2, _ = oracle.detect_cg(H[:, ns], y[:, ns], rho=sub.N0, mod=sub.mod, T=sub.T)
+    assert rel(out.cpu().numpy()[ns], ref) < TOL
+    assert rel(out2.cpu().numpy()[ns], ref2) < TOL
+    check_hard(hard.cpu().numpy()[ns], hard_ref, ref, sub.mod)
+
+
+def test_deterministic(env):
+    """Fixed-order sums: two runs are bitwise identical."""
+    a = run_admm(env, synth.CONFIGS["C"].scaled(N=16))[0]
+    b = run_admm(env, synth.CONFIGS["C"].scaled(N=16))[0]
+    assert np.array_equal(a, b)
