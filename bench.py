@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""bench.py -- detected Gbit/s per frame (and per-iteration latency) of libdbp.
+
+Workload: one TDD slot on the B = 1024-antenna array of
+BASELINE configs C and D -- C = 32 clusters of S = 32 antennas, U = 16 users,
+N = 1200 subcarriers, N_sym = 1, T = 5 iterations, rho = 1.  A step runs the
+whole hot path (every SURVEY 8(a) row) on one synthetic frame:
+  * uplink 64-QAM frame (SNR 25 dB) detected by ADMM (Alg. 1) and by
+    decentralized CG (Alg. 2);
+  * downlink 16-QAM frame precoded by ADMM beamforming (Alg. 3).
+value = (bits detected by ADMM + bits detected by CG + bits precoded) / step
+time, bits = U * N * N_sym * log2|O| per solver (P753, P800).  Clusters are
+split over the ranks (strong scaling) with one NCCL allreduce per consensus
+round -- the only communication (P744-746).
+
+Timing: W untimed warm-up steps; then exactly K steps, each bracketed by CUDA
+events on the launch stream, with an untimed 256 MiB L2-flush write between
+steps; barrier + synchronize on both sides; max over ranks.  The end-to-end
+figure (e2e) calls the same C ABI with pinned HOST buffers, so every step
+includes the host->device copy of its inputs and the device->host copy of
+its outputs.  `--impl reference` times the fp64 oracle (oracle/) on the
+host cores instead (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1702_04458_b200 import synth  # noqa: E402
+
+METRIC = "detected Gbit/s per frame (and per-iteration latency) at 1/2/4/8 B200"
+UL = synth.CONFIGS["C"]
+DL = synth.CONFIGS["D"]
+BITS = {"admm_ul": UL.bits_per_frame, "cg_ul": UL.bits_per_frame, "admm_dl": DL.bits_per_frame}
+BITS_PER_STEP = sum(BITS.values())
+
+
+def workload_config(world: int) -> dict:
+    return {"workload": "TDD slot on configs C+D: B=1024 (C=32 x S=32), U=16, N=1200, N_sym=1, T=5; "
+                        "ADMM-UL + CG-UL on a 64-QAM uplink frame (SNR 25 dB), ADMM-DL on a 16-QAM "
+                        "downlink frame",
+            "B": UL.B, "C": UL.C, "S": UL.S, "U": UL.U, "N": UL.N, "N_sym": UL.N_sym, "T": UL.T,
+            "rho": UL.rho, "mod_ul": UL.mod, "mod_dl": DL.mod, "snr_db": UL.snr_db,
+            "bits_per_step": BITS_PER_STEP, "parallelism": f"clusters split over {world} GPU(s), "
+                                                             f"{UL.C // world} per GPU",
+            "l2": "256 MiB L2-flush write between timed steps (untimed); each input > 126 MB L2"}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "50", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        self.proc.wait()
+        self.th.join(timeout=2)
+        rows = [r for r in self.rows if len(r) >= 9]
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ oracle legs
+def _oracle_sample(n_sub: int):
+    """Oracle on subcarriers [0, n_sub) of the same workload; returns (seconds, bits)."""
+    import oracle
+    ul, dl = UL.scaled(N=n_sub), DL.scaled(N=n_sub)
+    H, y, _ = synth.uplink_frame(UL, n0=0, n1=n_sub)
+    Hd, s = synth.downlink_frame(DL, n0=0, n1=n_sub)
+    t0 = time.perf_counter()
+    oracle.detect_admm(H, y, rho=ul.rho, N0=ul.N0, mod=ul.mod, T=ul.T)
+    oracle.beamform_admm(Hd, s, rho=dl.rho, T=dl.T)
+    oracle.detect_cg(H, y, rho=ul.N0, mod=ul.mod, T=ul.T)
+    dt = time.perf_counter() - t0
+    bits = 2 * ul.bits_per_frame + dl.bits_per_frame
+    return dt, bits
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(budget_s: float = 12.0, n_sub: int = 120) -> dict:
+    import oracle
+    oracle.build()
+    tot_t, tot_b, reps = 0.0, 0, 0
+    while tot_t < budget_s and reps < 50:
+        dt, b = _oracle_sample(n_sub)
+        tot_t += dt
+        tot_b += b
+        reps += 1
+    return {"value": tot_b / tot_t / 1e9, "unit": "Gbit/s", "cores": host_cores(), "kind": "oracle",
+            "sample": f"{n_sub} of {UL.N} subcarriers x all 3 solvers (all 32 clusters), {reps} repetition(s), "
+                      f"{tot_t:.1f} s of fp64 C oracle with OpenMP over subcarriers"}
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    n_sub = args.ref_subcarriers
+    for _ in range(args.warmup):
+        _oracle_sample(n_sub)
+    times, bits = [], 0
+    for _ in range(args.steps):
+        dt, b = _oracle_sample(n_sub)
+        times.append(dt)
+        bits = b
+    tot = sum(times)
+    value = bits * len(times) / tot / 1e9
+    sample = (f"{n_sub} of {UL.N} subcarriers x all 3 solvers per step (all 32 clusters); fp64 C oracle, "
+              f"OpenMP over subcarriers")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(world),
+            "cpu_baseline": {"value": value, "unit": "Gbit/s", "cores": host_cores(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ roofline model
+def algorithmic_bytes(kernel: str, C_loc: int) -> float:
+    """Algorithmic HBM bytes per launch (DESIGN.md section 5 table)."""
+    S, U, N, J = UL.S, UL.U, UL.N, UL.N_sym
+    tri = U * (U + 1) // 2
+    P = C_loc * N
+    c8 = 8
+    table = {
+        # k_gram: read H_c (+ y_c), write packed Gram (+ matched filter)
+        "gram_ul": P * (S * U + J * S + tri + J * U) * c8,
+        "gram_cg": P * (S * U + J * S + tri + J * U) * c8,
+        "gram_dl": P * (S * U + tri) * c8,
+        # k_inv: read packed G (+ mf), write packed G^{-1} (+ yreg)
+        "inv_ul": P * (2 * tri + 2 * J * U) * c8,
+        "inv_dl": P * (2 * tri) * c8,
+        # fused iterations: read G^{-1} rows (+ yreg / s, H_c for the DL output), write outputs
+        "admm_fused": P * (tri + J * U) * c8 + N * J * U * (c8 + 1),
+        "bf_fused": P * (tri + S * U + J * S) * c8 + N * J * U * c8,
+        "cg_gsum": P * (tri + J * U) * c8 + N * (tri + J * U) * c8,
+        "cg_fused": N * (tri + J * U) * c8 + N * J * U * (c8 + 1),
+    }
+    return float(table.get(kernel, 0.0))
+
+
+def load_traffic() -> dict:
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return {}
+    return {}
+
+
+# ------------------------------------------------------------------ main arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="dbp", choices=["dbp", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-subcarriers", type=int, default=60)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if "RANK" not in os.environ:
+        world = 1
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_1702_04458_b200 import dbp
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    uid = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        obj = [dbp.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    ctx = dbp.Context(device=local, rank=rank, world=world, unique_id=uid)
+
+    c0, c1 = synth.cluster_range(UL.C, rank, world)
+    H, y, _ = synth.uplink_frame(UL, c0, c1)
+    Hd, s = synth.downlink_frame(DL, c0, c1)
+    C_loc = c1 - c0
+    Hg, yg = torch.from_numpy(H).to(dev), torch.from_numpy(y).to(dev)
+    Hdg, sg = torch.from_numpy(Hd).to(dev), torch.from_numpy(s).to(dev)
+    s_hat = torch.empty((UL.N, UL.N_sym, UL.U), dtype=torch.complex64, device=dev)
+    hard = torch.empty((UL.N, UL.N_sym, UL.U), dtype=torch.uint8, device=dev)
+    x_hat = torch.empty_like(s_hat)
+    hard2 = torch.empty_like(hard)
+    xbf = torch.empty((C_loc, DL.N, DL.N_sym, DL.S), dtype=torch.complex64, device=dev)
+    ws = {a: torch.empty(max(1, ctx.workspace_bytes(UL.C, UL.S, UL.U, UL.N, UL.N_sym, a)), dtype=torch.uint8,
+                         device=dev) for a in ("admm_ul", "cg_ul", "admm_dl")}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def solver(name, T):
+        if name == "admm_ul":
+            dbp.detect_admm(ctx, Hg, yg, rho=UL.rho, N0=UL.N0, mod=UL.mod, T=T, s_hat=s_hat, hard=hard,
+                            ws=ws["admm_ul"])
+        elif name == "admm_dl":
+            dbp.beamform_admm(ctx, Hdg, sg, rho=DL.rho, T=T, x=xbf, ws=ws["admm_dl"])
+        else:
+            dbp.detect_cg(ctx, Hg, yg, rho=UL.N0, mod=UL.mod, T=T, x_hat=x_hat, hard=hard2, ws=ws["cg_ul"])
+
+    order = ["admm_ul", "admm_dl", "cg_ul"]   # BF between the two uplink passes: no L2 reuse of H
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def timed_region(K, T, names):
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)] for _ in range(K)]
+        barrier()
+        torch.cuda.synchronize()
+        for k in range(K):
+            flush.fill_(k & 0xFF)
+            ev[k][0].record(stream)
+            for i, nm in enumerate(names):
+                solver(nm, T)
+                ev[k][i + 1].record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        per = np.zeros(len(names))
+        for k in range(K):
+            for i in range(len(names)):
+                per[i] += ev[k][i].elapsed_time(ev[k][i + 1])
+        return per  # ms summed over K steps, per solver
+
+    for _ in range(args.warmup):
+        for nm in order:
+            solver(nm, UL.T)
+    ctx.sync()
+
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.15)
+    ctx.set_option(dbp.OPT_KERNEL_TIMING, 1)
+    ctx.kernel_times(reset=True)
+    st0 = ctx.stats()
+    per = timed_region(args.steps, UL.T, order)
+    st1 = ctx.stats()
+    ktimes = ctx.kernel_times(reset=True)
+    ctx.set_option(dbp.OPT_KERNEL_TIMING, 0)
+    clocks = clk.stop()
+    ctx.sync()
+
+    # per-iteration latency: (L(T) - L(1)) / (T - 1), per solver
+    K1 = min(args.steps, 200)
+    per1 = timed_region(K1, 1, order)
+
+    def mx(v):
+        if world == 1:
+            return np.asarray(v, dtype=np.float64)
+        t = torch.tensor(np.asarray(v, dtype=np.float64), device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.cpu().numpy()
+
+    per = mx(per)
+    per1 = mx(per1)
+    total_ms = float(per.sum())
+    ms_step = total_ms / args.steps
+    value = BITS_PER_STEP / (ms_step * 1e-3) / 1e9
+    solvers = {}
+    for i, nm in enumerate(order):
+        msT = per[i] / args.steps
+        ms1 = per1[i] / K1
+        solvers[nm] = {"ms": msT, "gbps": BITS[nm] / (msT * 1e-3) / 1e9, "ms_T1": ms1,
+                       "per_iter_us": 1e3 * (msT - ms1) / (UL.T - 1)}
+
+    # dominant kernel and its roofline (algorithmic bytes / average launch time)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s (B200_PROFILING.md)"
+    kern = {k: {"launches": int(v[0]), "avg_us": 1e3 * v[1] / max(v[0], 1), "share": v[1] / max(total_ms, 1e-9)}
+            for k, v in ktimes.items()}
+    dom = max(ktimes, key=lambda k: ktimes[k][1]) if ktimes else None
+    roof = None
+    if dom:
+        avg_s = ktimes[dom][1] / ktimes[dom][0] * 1e-3
+        ab = algorithmic_bytes(dom, C_loc)
+        traffic = load_traffic().get(dom)
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ab / avg_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                "frac": ab / avg_s / 1e9 / hbm_peak, "traffic": traffic, "algorithmic_bytes": ab,
+                "avg_launch_us": avg_s * 1e6, "peak_source": peak_src}
+
+    # end to end through the C ABI with pinned host buffers
+    e2e = None
+    if args.e2e_steps > 0:
+        pin = lambda a: torch.from_numpy(a).pin_memory().numpy()
+        Hh, yh, Hdh, sh = pin(H), pin(y), pin(Hd), pin(s)
+        o1 = torch.empty(tuple(s_hat.shape), dtype=torch.complex64).pin_memory().numpy()
+        o2 = torch.empty(tuple(hard.shape), dtype=torch.uint8).pin_memory().numpy()
+        o3 = torch.empty(tuple(s_hat.shape), dtype=torch.complex64).pin_memory().numpy()
+        o4 = torch.empty(tuple(hard.shape), dtype=torch.uint8).pin_memory().numpy()
+        o5 = torch.empty(tuple(xbf.shape), dtype=torch.complex64).pin_memory().numpy()
+
+        def e2e_step():
+            dbp.detect_admm(ctx, Hh, yh, rho=UL.rho, N0=UL.N0, mod=UL.mod, T=UL.T, s_hat=o1, hard=o2)
+            dbp.beamform_admm(ctx, Hdh, sh, rho=DL.rho, T=DL.T, x=o5)
+            dbp.detect_cg(ctx, Hh, yh, rho=UL.N0, mod=UL.mod, T=UL.T, x_hat=o3, hard=o4)
+
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        barrier()
+        dt = float(mx([time.perf_counter() - t0])[0]) / args.e2e_steps
+        h2d = 2 * (Hh.nbytes + yh.nbytes) + Hdh.nbytes + sh.nbytes
+        d2h = o1.nbytes + o2.nbytes + o3.nbytes + o4.nbytes + o5.nbytes
+        e2e = {"value": BITS_PER_STEP / dt / 1e9, "unit": "Gbit/s", "ms_per_step": dt * 1e3,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "how": "same C-ABI calls on pinned host numpy buffers; library stages H2D/D2H on the stream; "
+                      "host wall clock, max over ranks"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline()
+
+    if rank == 0:
+        launches = st1["kernel_launches"] - st0["kernel_launches"]
+        line = {"metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Philox-4x32: i.i.d. Rayleigh "
+                "CN(0,1) channels, uniform Gray QAM, AWGN)", "config": workload_config(world),
+                "solvers": solvers, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(launches), "gpu_launches_per_step": launches / args.steps,
+                "consensus_rounds_per_step": (st1["consensus_rounds"] - st0["consensus_rounds"]) / args.steps,
+                "allreduce_calls_per_step": (st1["allreduce_calls"] - st0["allreduce_calls"]) / args.steps,
+                "kernels": kern, "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

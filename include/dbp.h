@@ -90,8 +90,18 @@ typedef struct {
 typedef enum {
     /* 0 (default): at world == 1 use the fused single-GPU kernels; 1: always
      * use the per-iteration (multi-kernel + collective) path, as at world > 1. */
-    DBP_OPT_FORCE_SPLIT = 1
+    DBP_OPT_FORCE_SPLIT = 1,
+    /* 1: bracket every libdbp kernel launch with CUDA events on its stream and
+     * accumulate per-kernel device time (read with dbp_get_kernel_times). */
+    DBP_OPT_KERNEL_TIMING = 2
 } dbp_option;
+
+/* Per-kernel device time accumulated under DBP_OPT_KERNEL_TIMING. */
+typedef struct {
+    char name[40];
+    int64_t launches;
+    double total_ms;
+} dbp_kernel_time;
 
 /* NCCL bootstrap: fills 128 bytes (an ncclUniqueId) on rank 0; broadcast it to
  * the other ranks (e.g. over torch.distributed) before dbp_ctx_create. */
@@ -158,6 +168,11 @@ dbp_status dbp_beamform_admm(dbp_ctx* ctx, const dbp_dims* dims, const dbp_cf32*
  * host pointers as above. */
 dbp_status dbp_slice(dbp_ctx* ctx, int mod, int64_t count, const dbp_cf32* x, uint8_t* bits,
                      void* stream);
+
+/* Resolve the recorded events (blocks until they complete) and return up to
+ * `max_entries` per-kernel totals; `reset` != 0 clears the totals. */
+dbp_status dbp_get_kernel_times(dbp_ctx* ctx, dbp_kernel_time* out, int max_entries, int* n_entries,
+                                int reset);
 
 /* Synchronise `stream`; returns DBP_ERR_NOT_HPD if a Cholesky pivot failed in
  * any call since the previous dbp_sync (and clears the flag), or

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/dbp.h"
 #include "dbp_internal.h"
@@ -29,7 +30,30 @@ struct dbp_ctx {
     void* iws = nullptr;         // internal workspace when ws == NULL
     size_t iws_bytes = 0;
     int max_smem = 0;
+    // per-kernel event timing (DBP_OPT_KERNEL_TIMING)
+    int timing = 0;
+    struct Pending { int k; cudaEvent_t e0, e1; };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> pool;
+    std::vector<std::string> knames;
+    std::vector<int64_t> kcount;
+    std::vector<double> kms;
 };
+
+static cudaEvent_t ev_get(dbp_ctx* c) {
+    if (!c->pool.empty()) { cudaEvent_t e = c->pool.back(); c->pool.pop_back(); return e; }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+static int kname_id(dbp_ctx* c, const char* name) {
+    for (size_t i = 0; i < c->knames.size(); ++i) if (c->knames[i] == name) return (int)i;
+    c->knames.push_back(name);
+    c->kcount.push_back(0);
+    c->kms.push_back(0.0);
+    return (int)c->knames.size() - 1;
+}
 
 static thread_local std::string g_err;
 
@@ -112,6 +136,8 @@ extern "C" dbp_status dbp_ctx_destroy(dbp_ctx* c) {
     cudaFree(c->d_flag);
     if (c->stage) cudaFree(c->stage);
     if (c->iws) cudaFree(c->iws);
+    for (auto& p : c->pending) { cudaEventDestroy(p.e0); cudaEventDestroy(p.e1); }
+    for (auto e : c->pool) cudaEventDestroy(e);
     delete c;
     return DBP_OK;
 }
@@ -119,6 +145,7 @@ extern "C" dbp_status dbp_ctx_destroy(dbp_ctx* c) {
 extern "C" dbp_status dbp_set_option(dbp_ctx* c, int option, int64_t value) {
     if (!c) return fail(DBP_ERR_INVALID_ARG, "ctx is NULL");
     if (option == DBP_OPT_FORCE_SPLIT) { c->force_split = value ? 1 : 0; return DBP_OK; }
+    if (option == DBP_OPT_KERNEL_TIMING) { c->timing = value ? 1 : 0; return DBP_OK; }
     return fail(DBP_ERR_INVALID_ARG, "unknown option %d", option);
 }
 
@@ -156,28 +183,6 @@ static dbp_status check_dims(const dbp_ctx* c, const dbp_dims* d, Shape* sh) {
     return DBP_OK;
 }
 
-// Fused single-GPU schedule: NT subcarriers x C clusters per CTA, IT = UP/2
-// threads per pair, <= 1024 threads and the shared-memory budget.
-static bool fused_cfg(const dbp_ctx* c, const Shape& sh, int* NT) {
-    if (c->world != 1 || c->force_split) return false;
-    const int per_n = sh.C_loc * (sh.UP / 2);
-    if (per_n > 1024) return false;
-    int nt = std::max(1, std::min(256 / per_n, 1024 / per_n));
-    while (nt > 1 && admm_fused_smem(sh.UP, nt, sh.C_loc) > (size_t)c->max_smem) --nt;
-    if (admm_fused_smem(sh.UP, nt, sh.C_loc) > (size_t)c->max_smem) return false;
-    *NT = nt;
-    return true;
-}
-
-static void split_cfg(const Shape& sh, int* NT, int* CCH) {
-    const int it = sh.UP / 2;
-    int cch = std::min(sh.C_loc, std::max(1, 256 / it));
-    int nt = std::max(1, 256 / (cch * it));
-    nt = std::min(nt, sh.N);
-    *NT = nt;
-    *CCH = cch;
-}
-
 // Workspace layout (256-byte aligned segments).
 struct Layout {
     size_t off[8];
@@ -192,11 +197,12 @@ static Layout layout(const Shape& sh, int algo) {
     Layout L{};
     size_t sz[8] = {0};
     if (algo == DBP_ALGO_ADMM_UL) {
-        sz[0] = P * T * 8;   // X
-        sz[1] = vecp;        // yreg
-        sz[2] = vecp;        // lam
-        sz[3] = vecp;        // z
-        sz[4] = vecn;        // wbuf
+        sz[0] = P * T * 8;   // G, then G^{-1} in place (split path)
+        sz[1] = vecp;        // matched filter H^H y
+        sz[2] = vecp;        // yreg
+        sz[3] = vecp;        // lam
+        sz[4] = vecp;        // z
+        sz[5] = vecn;        // wbuf
     } else if (algo == DBP_ALGO_CG_UL) {
         sz[0] = P * T * 8;                 // per-pair Gram
         sz[1] = vecp;                      // per-pair matched filter
@@ -207,7 +213,7 @@ static Layout layout(const Shape& sh, int algo) {
         sz[6] = vecn;                      // p
         sz[7] = (size_t)sh.N * sh.J * 4;   // rr
     } else {
-        sz[0] = P * T * 8;   // X
+        sz[0] = P * T * 8;   // B, then B^{-1} in place (split path)
         sz[1] = vecp;        // m
         sz[2] = vecp;        // lam
         sz[3] = vecn;        // wbuf
@@ -329,6 +335,19 @@ static dbp_status allreduce(dbp_ctx* c, float2* buf, size_t nfloat2, cudaStream_
         if (e_ != cudaSuccess) return fail(DBP_ERR_CUDA, "launch %s: %s", #call, cudaGetErrorString(e_)); \
     } while (0)
 
+// Launch with optional per-kernel event timing on the launch stream.
+#define KT(name, call)                                                                         \
+    do {                                                                                       \
+        cudaEvent_t e0_ = nullptr;                                                             \
+        if (c->timing) { e0_ = ev_get(c); cudaEventRecord(e0_, s); }                            \
+        KL(call);                                                                              \
+        if (c->timing) {                                                                       \
+            cudaEvent_t e1_ = ev_get(c);                                                       \
+            cudaEventRecord(e1_, s);                                                           \
+            c->pending.push_back({kname_id(c, name), e0_, e1_});                                \
+        }                                                                                      \
+    } while (0)
+
 static Prox make_prox(int reg, int mod, int C, float rho, float N0, float Es) {
     Prox p;
     p.reg = reg;
@@ -368,41 +387,44 @@ extern "C" dbp_status dbp_detect_admm(dbp_ctx* c, const dbp_dims* d, const dbp_c
     if ((st = begin_call(c, k, Lw, ws, ws_bytes, s))) return st;
     const float2* dH = static_cast<const float2*>(k.io[0].dev);
     const float2* dy = static_cast<const float2*>(k.io[1].dev);
-    float2* X = reinterpret_cast<float2*>(k.ws + Lw.off[0]);
-    float2* yreg = reinterpret_cast<float2*>(k.ws + Lw.off[1]);
+    float2* G = reinterpret_cast<float2*>(k.ws + Lw.off[0]);
+    float2* mf = reinterpret_cast<float2*>(k.ws + Lw.off[1]);
     LaunchCtx L{s, c->d_flag, &c->launches};
 
-    // a1-a3: Gram + Cholesky inverse + matched filter (Alg. 1 lines 2-8)
-    KL(launch_pre(L, sh.UP, PRE_ADMM_, dH, dy, sh.S, sh.U, sh.J, sh.pairs(), rho, X, yreg));
+    // a1, a3: G_c = H_c^H H_c + rho I and H_c^H y_c (Alg. 1 lines 7-8)
+    KT("gram_ul", launch_gram(L, sh.UP, PRE_ADMM_, dH, dy, sh.S, sh.U, sh.J, sh.pairs(), rho, G, mf));
 
-    AdmmArgs a{};
-    a.X = X; a.yreg = yreg;
-    a.lam = reinterpret_cast<float2*>(k.ws + Lw.off[2]);
-    a.z = reinterpret_cast<float2*>(k.ws + Lw.off[3]);
-    a.wbuf = reinterpret_cast<float2*>(k.ws + Lw.off[4]);
+    UlArgs a{};
+    a.G = G; a.mf = mf; a.Ginv = G;
+    a.yreg = reinterpret_cast<float2*>(k.ws + Lw.off[2]);
+    a.lam = reinterpret_cast<float2*>(k.ws + Lw.off[3]);
+    a.z = reinterpret_cast<float2*>(k.ws + Lw.off[4]);
+    a.wbuf = reinterpret_cast<float2*>(k.ws + Lw.off[5]);
     a.s_hat = static_cast<float2*>(k.io[2].dev);
     a.hard = static_cast<uint8_t*>(k.io[3].dev);
+    a.flag = c->d_flag;
     a.C_loc = sh.C_loc; a.N = sh.N; a.J = sh.J; a.U = sh.U; a.T = T;
     a.rho = rho; a.gamma = gamma;
     a.px = make_prox(reg, mod, sh.C, rho, N0, Es);
     a.md = modem_of(mod);
-    int NT;
-    if (fused_cfg(c, sh, &NT)) {
-        // a4-a8 fused: all T iterations with X_c on chip (world == 1)
-        a.NT = NT; a.CCH = sh.C_loc;
-        KL(launch_admm_fused(L, sh.UP, a));
+    int NT, CCH;
+    if (c->world == 1 && !c->force_split && iter_cfg(sh.UP, sh.C_loc, sh.N, c->max_smem, &NT)) {
+        // a2: B_c^{-1} and y^reg; a4-a8 fused: all T iterations on chip (world == 1)
+        KT("inv_ul", launch_inv_ul(L, sh.UP, a, sh.pairs()));
+        a.NT = NT;
+        KT("admm_fused", launch_admm_gj(L, sh.UP, a));
         c->consensus_rounds += T;
     } else {
-        int CCH;
-        split_cfg(sh, &NT, &CCH);
-        a.NT = NT; a.CCH = CCH;
+        KT("inv_ul", launch_inv_ul(L, sh.UP, a, sh.pairs()));              // a2 + yreg
+        split_cfg(sh.UP, sh.C_loc, sh.N, sh.J, &NT, &CCH);
+        a.NT = NT;
         const size_t nw = (size_t)sh.N * sh.J * sh.UP;
         for (int t = 1; t <= T; ++t) {
             a.init = (t == 1);
-            KL(launch_admm_step(L, sh.UP, a));                       // lines 12-18 (t = 1: line 10)
-            if ((st = allreduce(c, a.wbuf, nw, s))) return st;       // line 18 consensus
+            KT("admm_step", launch_admm_it(L, sh.UP, a, CCH));              // lines 12-17 (t = 1: line 10)
+            if ((st = allreduce(c, a.wbuf, nw, s))) return st;              // line 18 consensus
         }
-        KL(launch_prox_out(L, sh.UP, a.wbuf, sh.N, sh.J, sh.U, a.px, a.md, a.s_hat, a.hard));  // line 19, output
+        KT("prox_out", launch_prox_out(L, sh.UP, a.wbuf, sh.N, sh.J, sh.U, a.px, a.md, a.s_hat, a.hard));  // line 19
     }
     return end_call(c, k, s);
 }
@@ -446,18 +468,18 @@ extern "C" dbp_status dbp_detect_cg(dbp_ctx* c, const dbp_dims* d, const dbp_cf3
 
     // b1: per-pair Gram H_c^H H_c and matched filter H_c^H y_c, then the
     // per-GPU sums (G_loc, local y^MRC) in fixed cluster order.
-    KL(launch_pre(L, sh.UP, PRE_CG_, static_cast<const float2*>(k.io[0].dev), static_cast<const float2*>(k.io[1].dev),
-                  sh.S, sh.U, sh.J, sh.pairs(), 0.f, Gp, mf));
-    KL(launch_cg_gsum(L, sh.UP, Gp, mf, sh.C_loc, sh.N, sh.J, const_cast<float2*>(a.Gloc), a.wbuf));
+    KT("gram_cg", launch_gram(L, sh.UP, PRE_CG_, static_cast<const float2*>(k.io[0].dev),
+                               static_cast<const float2*>(k.io[1].dev), sh.S, sh.U, sh.J, sh.pairs(), 0.f, Gp, mf));
+    KT("cg_gsum", launch_cg_gsum(L, sh.UP, Gp, mf, sh.C_loc, sh.N, sh.J, const_cast<float2*>(a.Gloc), a.wbuf));
     const size_t nw = (size_t)sh.N * sh.J * sh.UP;
     if ((st = allreduce(c, a.wbuf, nw, s))) return st;              // line 4: y^MRC consensus
     if (c->world == 1 && !c->force_split) {
-        KL(launch_cg_it(L, sh.UP, true, a));                          // lines 6-18, all T iterations
+        KT("cg_fused", launch_cg_it(L, sh.UP, true, a));                          // lines 6-18, all T iterations
         c->consensus_rounds += T;
     } else {
         for (int t = 0; t <= T; ++t) {
             a.step = t;
-            KL(launch_cg_it(L, sh.UP, false, a));
+            KT("cg_step", launch_cg_it(L, sh.UP, false, a));
             if (t < T && (st = allreduce(c, a.wbuf, nw, s))) return st;   // line 11 consensus
         }
     }
@@ -488,40 +510,42 @@ extern "C" dbp_status dbp_beamform_admm(dbp_ctx* c, const dbp_dims* d, const dbp
     k.nio = 3;
     if ((st = begin_call(c, k, Lw, ws, ws_bytes, s))) return st;
     LaunchCtx L{s, c->d_flag, &c->launches};
-    BfArgs a{};
+    DlArgs a{};
     a.Hd = static_cast<const float2*>(k.io[0].dev);
     a.s = static_cast<const float2*>(k.io[1].dev);
-    a.X = reinterpret_cast<float2*>(k.ws + Lw.off[0]);
+    float2* G = reinterpret_cast<float2*>(k.ws + Lw.off[0]);
+    a.G = G; a.Binv = G;
     a.m = reinterpret_cast<float2*>(k.ws + Lw.off[1]);
     a.lam = reinterpret_cast<float2*>(k.ws + Lw.off[2]);
     a.wbuf = reinterpret_cast<float2*>(k.ws + Lw.off[3]);
-    a.xout = static_cast<float2*>(k.io[2].dev);
+    a.x = static_cast<float2*>(k.io[2].dev);
+    a.flag = c->d_flag;
     a.C_loc = sh.C_loc; a.C = sh.C; a.N = sh.N; a.J = sh.J; a.U = sh.U; a.S = sh.S; a.T = T;
     a.rho_inv = (float)(1.0 / rho);
     a.gamma = gamma;
     a.a0 = (float)std::max((double)sh.U / ((double)sh.C * sh.S), 1.0 / sh.C);   // Alg. 3 line 8 (P507)
     a.inv_c = (float)(1.0 / sh.C);
 
-    // c1: B_c = H_c H_c^H + rho^{-1} I_U, Cholesky inverse (Alg. 3 lines 2-6)
-    KL(launch_pre(L, sh.UP, PRE_BF_, a.Hd, nullptr, sh.S, sh.U, sh.J, sh.pairs(), a.rho_inv,
-                  const_cast<float2*>(a.X), nullptr));
-    int NT;
-    if (fused_cfg(c, sh, &NT)) {
-        a.NT = NT; a.CCH = sh.C_loc;
-        KL(launch_bf_fused(L, sh.UP, a));
+    // c1: B_c = H_c H_c^H + rho^{-1} I_U (Alg. 3 line 5)
+    KT("gram_dl", launch_gram(L, sh.UP, PRE_BF_, a.Hd, nullptr, sh.S, sh.U, sh.J, sh.pairs(), a.rho_inv, G, nullptr));
+    int NT, CCH;
+    if (c->world == 1 && !c->force_split && iter_cfg(sh.UP, sh.C_loc, sh.N, c->max_smem, &NT)) {
+        KT("inv_dl", launch_inv_dl(L, sh.UP, a, sh.pairs()));              // c1 inverse
+        a.NT = NT;
+        KT("bf_fused", launch_bf_gj(L, sh.UP, a));                         // c2-c4
         c->consensus_rounds += T - 1;
     } else {
-        int CCH;
-        split_cfg(sh, &NT, &CCH);
-        a.NT = NT; a.CCH = CCH;
+        KT("inv_dl", launch_inv_dl(L, sh.UP, a, sh.pairs()));              // c1 inverse
+        split_cfg(sh.UP, sh.C_loc, sh.N, sh.J, &NT, &CCH);
+        a.NT = NT;
         const size_t nw = (size_t)sh.N * sh.J * sh.UP;
         for (int t = 2; t <= T; ++t) {
             a.step = t;
-            KL(launch_bf_step(L, sh.UP, a));                           // lines 11-12 (+14-15 of t-1)
-            if ((st = allreduce(c, a.wbuf, nw, s))) return st;         // line 13 consensus
+            KT("bf_step", launch_bf_it(L, sh.UP, a, CCH));                 // lines 11-12 (+14-15 of t-1)
+            if ((st = allreduce(c, a.wbuf, nw, s))) return st;             // line 13 consensus
         }
         a.step = T + 1;
-        KL(launch_bf_step(L, sh.UP, a));                               // output x_c^(T) (P525)
+        KT("bf_final", launch_bf_it(L, sh.UP, a, CCH));                    // output x_c^(T) (P525)
     }
     return end_call(c, k, s);
 }
@@ -542,8 +566,37 @@ extern "C" dbp_status dbp_slice(dbp_ctx* c, int mod, int64_t count, const dbp_cf
     dbp_status st = begin_call(c, k, Lw, nullptr, 0, s);
     if (st) return st;
     LaunchCtx L{s, c->d_flag, &c->launches};
-    KL(launch_slice(L, static_cast<const float2*>(k.io[0].dev), count, modem_of(mod), static_cast<uint8_t*>(k.io[1].dev)));
+    KT("slice", launch_slice(L, static_cast<const float2*>(k.io[0].dev), count, modem_of(mod), static_cast<uint8_t*>(k.io[1].dev)));
     return end_call(c, k, s);
+}
+
+extern "C" dbp_status dbp_get_kernel_times(dbp_ctx* c, dbp_kernel_time* out, int max_entries, int* n_entries,
+                                           int reset) {
+    if (!c || !n_entries || max_entries < 0 || (max_entries > 0 && !out)) return fail(DBP_ERR_INVALID_ARG, "bad arguments");
+    CU(cudaSetDevice(c->device));
+    for (auto& p : c->pending) {
+        CU(cudaEventSynchronize(p.e1));
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, p.e0, p.e1));
+        c->kms[p.k] += ms;
+        c->kcount[p.k] += 1;
+        c->pool.push_back(p.e0);
+        c->pool.push_back(p.e1);
+    }
+    c->pending.clear();
+    int n = 0;
+    for (size_t i = 0; i < c->knames.size() && n < max_entries; ++i) {
+        if (!c->kcount[i]) continue;
+        memset(out[n].name, 0, sizeof out[n].name);
+        strncpy(out[n].name, c->knames[i].c_str(), sizeof out[n].name - 1);
+        out[n].launches = c->kcount[i];
+        out[n].total_ms = c->kms[i];
+        ++n;
+    }
+    *n_entries = n;
+    if (reset)
+        for (size_t i = 0; i < c->knames.size(); ++i) { c->kcount[i] = 0; c->kms[i] = 0.0; }
+    return DBP_OK;
 }
 
 extern "C" dbp_status dbp_sync(dbp_ctx* c, void* stream) {

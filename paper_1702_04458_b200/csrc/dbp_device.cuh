@@ -163,111 +163,6 @@ __device__ __forceinline__ void load4(const float2* tile, int s, int u0, int U, 
     }
 }
 
-// Off-diagonal tile (a > b): G[4a+r][4b+c] = sum_s conj(h_s,4a+r) h_s,4b+c.
-template <bool DL, bool FULL>
-__device__ __forceinline__ void gram_off(const float2* tile, int S, int U, int a, int b, float2 (&acc)[16]) {
-#pragma unroll
-    for (int k = 0; k < 16; ++k) acc[k] = make_float2(0.f, 0.f);
-#pragma unroll 2
-    for (int s = 0; s < S; ++s) {
-        float2 A[4], B[4];
-        load4<DL, FULL>(tile, s, 4 * a, U, S, A);
-        load4<DL, FULL>(tile, s, 4 * b, U, S, B);
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) c_fmac(acc[r * 4 + c], A[r], B[c]);
-    }
-}
-
-// Two diagonal tiles d0, d1 (lower parts, real diagonals); d1 < 0 = none.
-// acc layout: [tile][10]: (r, c) with c <= r in row-major packed order.
-template <bool DL, bool FULL>
-__device__ __forceinline__ void gram_diag(const float2* tile, int S, int U, int d0, int d1, float2 (&acc)[20]) {
-#pragma unroll
-    for (int k = 0; k < 20; ++k) acc[k] = make_float2(0.f, 0.f);
-#pragma unroll 2
-    for (int s = 0; s < S; ++s) {
-        float2 A[4], B[4];
-        load4<DL, FULL>(tile, s, 4 * d0, U, S, A);
-        if (d1 >= 0) load4<DL, FULL>(tile, s, 4 * d1, U, S, B);
-        else { B[0] = B[1] = B[2] = B[3] = make_float2(0.f, 0.f); }
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-#pragma unroll
-            for (int c = 0; c < r; ++c) {
-                c_fmac(acc[pidx(r, c)], A[r], A[c]);
-                c_fmac(acc[10 + pidx(r, c)], B[r], B[c]);
-            }
-            acc[pidx(r, r)].x = fmaf(A[r].x, A[r].x, fmaf(A[r].y, A[r].y, acc[pidx(r, r)].x));
-            acc[10 + pidx(r, r)].x = fmaf(B[r].x, B[r].x, fmaf(B[r].y, B[r].y, acc[10 + pidx(r, r)].x));
-        }
-    }
-}
-
-// Team-cooperative Cholesky B = L L^H in place on packed lower storage.
-// Returns false if a pivot is not positive and finite (the caller flags
-// DBP_ERR_NOT_HPD); the factorisation then continues with 0 scales so no
-// NaN/Inf is produced by the kernel itself.
-template <int UP, int TPP>
-__device__ __forceinline__ bool team_cholesky(float2* L, int t) {
-    bool ok = true;
-    for (int k = 0; k < UP; ++k) {
-        float d = L[pidx(k, k)].x;
-        bool good = (d > 0.f) && (d < INFINITY);
-        ok = ok && good;
-        float l = good ? sqrtf(d) : 0.f;
-        float il = good ? 1.0f / l : 0.f;
-        __syncwarp();
-        for (int i = k + 1 + t; i < UP; i += TPP) L[pidx(i, k)] = c_scale(L[pidx(i, k)], il);
-        if (t == 0) L[pidx(k, k)] = make_float2(l, 0.f);
-        __syncwarp();
-        // trailing update, rows paired (k+1+g, UP-1-g) for balance
-        const int m = UP - 1 - k;
-        for (int g = t; 2 * g < m; g += TPP) {
-            int r1 = k + 1 + g, r2 = UP - 1 - g;
-            float2 l1 = L[pidx(r1, k)];
-            for (int j = k + 1; j <= r1; ++j) c_fmacb(L[pidx(r1, j)], make_float2(-l1.x, -l1.y), L[pidx(j, k)]);
-            if (r2 != r1) {
-                float2 l2 = L[pidx(r2, k)];
-                for (int j = k + 1; j <= r2; ++j) c_fmacb(L[pidx(r2, j)], make_float2(-l2.x, -l2.y), L[pidx(j, k)]);
-            }
-        }
-        __syncwarp();
-    }
-    return ok;
-}
-
-// In-place triangular inverse X = L^{-1} (lower), row by row:
-// X[i][i] = 1/L[i][i], X[i][j] = -X[i][i] sum_{k=j}^{i-1} L[i][k] X[k][j].
-template <int UP, int TPP>
-__device__ __forceinline__ void team_tri_inverse(float2* L, int t) {
-    constexpr int NJ = (UP + TPP - 1) / TPP;
-    for (int i = 0; i < UP; ++i) {
-        float lii = L[pidx(i, i)].x;
-        float xii = lii > 0.f ? 1.0f / lii : 0.f;
-        float2 out[NJ];
-#pragma unroll
-        for (int q = 0; q < NJ; ++q) {
-            int j = t + q * TPP;
-            float2 acc = make_float2(0.f, 0.f);
-            if (j < i) {
-                for (int k = j; k < i; ++k) c_fma(acc, L[pidx(i, k)], L[pidx(k, j)]);
-                acc = c_scale(acc, -xii);
-            }
-            out[q] = acc;
-        }
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < NJ; ++q) {
-            int j = t + q * TPP;
-            if (j < i) L[pidx(i, j)] = out[q];
-        }
-        if (t == 0) L[pidx(i, i)] = make_float2(xii, 0.f);
-        __syncwarp();
-    }
-}
-
 // Row ownership for triangular mat-vecs: a row pair {g, UP-1-g} has UP+1
 // terms in both X v and X^H v.  TR threads share a row pair (split terms),
 // each thread owns RPT row pairs.

@@ -9,6 +9,15 @@
 
 namespace dbp {
 
+#define DBP_DISPATCH_UP(UP_, ...)                                    \
+    switch (UP_) {                                                   \
+        case 4: { constexpr int UPc = 4; __VA_ARGS__; } break;       \
+        case 8: { constexpr int UPc = 8; __VA_ARGS__; } break;       \
+        case 16: { constexpr int UPc = 16; __VA_ARGS__; } break;     \
+        default: { constexpr int UPc = 32; __VA_ARGS__; } break;     \
+    }
+
+
 struct LaunchCtx {
     cudaStream_t stream;
     int* flag;              // device error flag (Cholesky pivot)
@@ -17,20 +26,6 @@ struct LaunchCtx {
 };
 
 enum { PRE_ADMM_ = 0, PRE_BF_ = 1, PRE_CG_ = 2 };
-
-struct AdmmArgs {
-    const float2* X;      // [C_loc][N][tri(UP)]
-    const float2* yreg;   // [C_loc][N][J][UP]
-    float2* lam;          // [C_loc][N][J][UP]
-    float2* z;            // [C_loc][N][J][UP]
-    float2* wbuf;         // [N][J][UP] consensus buffer (allreduced between launches)
-    float2* s_hat;        // [N][J][U]
-    uint8_t* hard;        // [N][J][U] or null
-    int C_loc, N, J, U, T, NT, CCH, init;
-    float rho, gamma;
-    Prox px;
-    Modem md;
-};
 
 struct CgArgs {
     const float2* Gloc;   // [N][tri(UP)]
@@ -46,26 +41,13 @@ struct CgArgs {
     Modem md;
 };
 
-struct BfArgs {
-    const float2* Hd;     // [C_loc][N][U][S]
-    const float2* s;      // [N][J][U]
-    const float2* X;      // [C_loc][N][tri(UP)]
-    float2* m;            // [C_loc][N][J][UP]  state (split path)
-    float2* lam;          // [C_loc][N][J][UP]
-    float2* wbuf;         // [N][J][UP]
-    float2* xout;         // [C_loc][N][J][S]
-    int C_loc, C, N, J, U, S, T, NT, CCH, step;   // step: 2..T iteration, T+1 = final
-    float rho_inv, gamma, a0, inv_c;
-};
+
 
 size_t pre_smem(int UP, int S, int U, int J, int mode);
-cudaError_t launch_pre(const LaunchCtx& L, int UP, int mode, const float2* H, const float2* y, int S, int U,
-                       int J, long npairs, float delta, float2* Xout, float2* vout);
+// Gram (+ delta I) per pair -> Gout [pairs][tri(UP)]; matched filter -> mfout [pairs][J][UP] (not for BF)
+cudaError_t launch_gram(const LaunchCtx& L, int UP, int mode, const float2* H, const float2* y, int S, int U,
+                        int J, long npairs, float delta, float2* Gout, float2* mfout);
 
-size_t admm_step_smem(int UP, int NT, int CCH, int J);
-size_t admm_fused_smem(int UP, int NT, int C);
-cudaError_t launch_admm_step(const LaunchCtx& L, int UP, AdmmArgs a);
-cudaError_t launch_admm_fused(const LaunchCtx& L, int UP, AdmmArgs a);
 cudaError_t launch_prox_out(const LaunchCtx& L, int UP, const float2* wbuf, int N, int J, int U, Prox px,
                             Modem md, float2* s_hat, uint8_t* hard);
 cudaError_t launch_slice(const LaunchCtx& L, const float2* x, long count, Modem md, uint8_t* bits);
@@ -74,9 +56,46 @@ cudaError_t launch_cg_gsum(const LaunchCtx& L, int UP, const float2* Gp, const f
                            int J, float2* Gloc, float2* wbuf);
 cudaError_t launch_cg_it(const LaunchCtx& L, int UP, bool fused, CgArgs a);
 
-size_t bf_step_smem(int UP, int NT, int CCH, int J);
-size_t bf_fused_smem(int UP, int NT, int C);
-cudaError_t launch_bf_step(const LaunchCtx& L, int UP, BfArgs a);
-cudaError_t launch_bf_fused(const LaunchCtx& L, int UP, BfArgs a);
+struct UlArgs {
+    const float2* G;      // [C_loc][N][tri(UP)]  G = H^H H + rho I (packed lower)
+    const float2* mf;     // [C_loc][N][J][UP]    H^H y
+    float2* Ginv;         // split: [C_loc][N][tri(UP)] G^{-1} (packed lower)
+    float2* yreg;         // split: [C_loc][N][J][UP]
+    float2* lam;          // split state
+    float2* z;
+    float2* wbuf;         // [N][J][UP]
+    float2* s_hat;        // [N][J][U]
+    uint8_t* hard;
+    int* flag;
+    int C_loc, N, J, U, T, NT, init;
+    float rho, gamma;
+    Prox px;
+    Modem md;
+};
+
+struct DlArgs {
+    const float2* G;      // [C_loc][N][tri(UP)]  B = H H^H + rho^{-1} I (packed lower)
+    const float2* Hd;     // [C_loc][N][U][S]
+    const float2* s;      // [N][J][U]
+    float2* Binv;         // split: [C_loc][N][tri(UP)]
+    float2* m;            // split state [C_loc][N][J][UP]
+    float2* lam;
+    float2* wbuf;         // [N][J][UP]
+    float2* x;            // [C_loc][N][J][S]
+    int* flag;
+    int C_loc, C, N, J, U, S, T, NT, step;
+    float rho_inv, gamma, a0, inv_c;
+};
+
+size_t iter_smem(int UP, int NT, int C);
+bool iter_cfg(int UP, int C_loc, int N, int max_smem, int* NT);
+size_t split_smem(int UP, int NT, int CCH, int J);
+void split_cfg(int UP, int C_loc, int N, int J, int* NT, int* CCH);
+cudaError_t launch_inv_ul(const LaunchCtx& L, int UP, UlArgs a, long npairs);
+cudaError_t launch_admm_gj(const LaunchCtx& L, int UP, UlArgs a);
+cudaError_t launch_admm_it(const LaunchCtx& L, int UP, UlArgs a, int CCH);
+cudaError_t launch_inv_dl(const LaunchCtx& L, int UP, DlArgs a, long npairs);
+cudaError_t launch_bf_gj(const LaunchCtx& L, int UP, DlArgs a);
+cudaError_t launch_bf_it(const LaunchCtx& L, int UP, DlArgs a, int CCH);
 
 }  // namespace dbp

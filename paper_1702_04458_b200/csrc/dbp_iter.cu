@@ -1,0 +1,512 @@
+// dbp_iter.cu -- inverse + consensus iterations of ADMM-UL (Alg. 1) and
+// ADMM-DL (Alg. 3), SURVEY 8(a) rows a2, a4-a8 and c1-c4.
+//
+// Layout: one lane per row of the U x U operator ("lane = user"), UP lanes per
+// (cluster, subcarrier) pair, all lanes of a pair inside one warp.
+//
+//  * Inverse: Gauss-Jordan elimination on the HPD matrix G (no pivoting is
+//    needed for HPD input; a non-positive or non-finite pivot raises the
+//    DBP_ERR_NOT_HPD flag, the same condition as a failed Cholesky pivot,
+//    SPEC S44).  Each step broadcasts the pivot row through a per-pair
+//    shared-memory line (UP/2 LDS.128) and updates all UP entries of every
+//    row: no triangular waste, no shuffles, and the result -- row i of
+//    G^{-1} -- is exactly what the iterations need in lane i's registers.
+//    DESIGN.md section 5 discusses this against the paper's LU/Cholesky
+//    inversion (P704); the algebraic result is the same matrix.
+//  * Iterations: every local update is one row of a Hermitian mat-vec with
+//    the vector broadcast through shared memory; the consensus sum over the
+//    CTA's clusters is taken in fixed cluster order (deterministic).
+//  * Fused kernels (world == 1): inverse + all T iterations + outputs in one
+//    launch, G^{-1} never leaves the register file.  Split kernels (any
+//    world): k_inv writes G^{-1} (packed) once; each iteration launch reloads
+//    its rows and leaves the partial consensus sum for the NCCL allreduce.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "dbp_device.cuh"
+#include "dbp_internal.h"
+
+namespace dbp {
+
+// Row i of the Hermitian G from its packed lower triangle (global, read-only).
+template <int UP>
+__device__ __forceinline__ void load_herm_row(const float2* __restrict__ Gp, int i, float2 (&r)[UP]) {
+    const int base = (i * (i + 1)) / 2;
+#pragma unroll
+    for (int j = 0; j < UP; ++j) {
+        if (j <= i) r[j] = __ldg(Gp + base + j);
+        else { const float2 v = __ldg(Gp + (j * (j + 1)) / 2 + i); r[j] = make_float2(v.x, -v.y); }
+    }
+}
+
+template <int UP>
+__device__ __forceinline__ void store_herm_row(float2* __restrict__ Gp, int i, const float2 (&r)[UP]) {
+    const int base = (i * (i + 1)) / 2;
+#pragma unroll
+    for (int j = 0; j < UP; ++j)
+        if (j <= i) Gp[base + j] = r[j];
+}
+
+// Broadcast-read a UP-vector written by the pair's lanes into registers.
+template <int UP>
+__device__ __forceinline__ void read_vec(const float2* buf, float2 (&v)[UP]) {
+    const float4* p = reinterpret_cast<const float4*>(buf);
+#pragma unroll
+    for (int k = 0; k < UP / 2; ++k) {
+        const float4 q = p[k];
+        v[2 * k] = make_float2(q.x, q.y);
+        v[2 * k + 1] = make_float2(q.z, q.w);
+    }
+}
+
+// In-place Gauss-Jordan inverse, lane i holds row i; prow = per-pair UP-line.
+template <int UP>
+__device__ __forceinline__ bool gj_invert(float2 (&r)[UP], float2* prow, int i) {
+    bool ok = true;
+#pragma unroll (UP <= 16 ? UP : 1)
+    for (int k = 0; k < UP; ++k) {
+        // lane k publishes its row (pivot row)
+        if (i == k) {
+            float4* p = reinterpret_cast<float4*>(prow);
+#pragma unroll
+            for (int q = 0; q < UP / 2; ++q) p[q] = make_float4(r[2 * q].x, r[2 * q].y, r[2 * q + 1].x, r[2 * q + 1].y);
+        }
+        __syncwarp();
+        float2 pr[UP];
+        read_vec<UP>(prow, pr);
+        // pivot = pr[k] (real part; HPD => real, positive)
+        float piv = 0.f;
+        float2 fk = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < UP; ++j) {
+            if (j == k) { piv = pr[j].x; fk = r[j]; }
+        }
+        const bool good = (piv > 0.f) && (piv < INFINITY);
+        ok = ok && good;
+        const float ip = good ? 1.0f / piv : 0.f;
+        if (i == k) {
+#pragma unroll
+            for (int j = 0; j < UP; ++j) r[j] = (j == k) ? make_float2(ip, 0.f) : c_scale(pr[j], ip);
+        } else {
+            // r_j -= f * pr_j * ip  (j != k);  r_k = -f * ip
+            const float2 f = c_scale(fk, ip);
+#pragma unroll
+            for (int j = 0; j < UP; ++j) {
+                if (j == k) r[j] = make_float2(-f.x, -f.y);
+                else {
+                    r[j].x -= f.x * pr[j].x - f.y * pr[j].y;
+                    r[j].y -= f.x * pr[j].y + f.y * pr[j].x;
+                }
+            }
+        }
+        __syncwarp();
+    }
+    return ok;
+}
+
+// y = sum_j R[j] v_j with v published by the pair's lanes in buf (v_i from lane i).
+template <int UP>
+__device__ __forceinline__ float2 row_apply(const float2 (&R)[UP], float2* buf, int i, float2 vi) {
+    buf[i] = vi;
+    __syncwarp();
+    float2 v[UP];
+    read_vec<UP>(buf, v);
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < UP; ++j) c_fma(acc, R[j], v[j]);
+    __syncwarp();
+    return acc;
+}
+
+// Fixed-order sum over the CTA's clusters for each (subcarrier, user):
+// W[nl][c][u] -> out[nl][u] (threads (nl, u) sum c = 0..C-1 in order).
+__device__ __forceinline__ float2 cluster_sum(const float2* W, int C, int UP, int nl, int u) {
+    float2 acc = make_float2(0.f, 0.f);
+    const float2* p = W + (size_t)nl * C * UP + u;
+    int c = 0;
+    for (; c + 4 <= C; c += 4) {
+        const float2 a0 = p[(c + 0) * UP], a1 = p[(c + 1) * UP], a2 = p[(c + 2) * UP], a3 = p[(c + 3) * UP];
+        acc = c_add(c_add(c_add(c_add(acc, a0), a1), a2), a3);
+    }
+    for (; c < C; ++c) acc = c_add(acc, p[c * UP]);
+    return acc;
+}
+
+// ============================================================ ADMM-UL
+
+
+// Split path, preprocessing: G^{-1} and yreg = G^{-1} mf per pair (lane = row).
+template <int UP>
+__global__ void __launch_bounds__(256, UP == 32 ? 1 : 3) k_inv_ul(UlArgs a, long npairs) {
+    __shared__ __align__(16) float2 sbuf[256 / UP][UP];
+    const int q = threadIdx.x / UP, i = threadIdx.x % UP;
+    const long p = (long)blockIdx.x * (256 / UP) + q;
+    const bool valid = p < npairs;
+    const long pp = valid ? p : npairs - 1;
+    float2 R[UP];
+    load_herm_row<UP>(a.G + (size_t)pp * tri(UP), i, R);
+    const bool ok = gj_invert<UP>(R, sbuf[q], i);
+    if (!ok && valid) atomicOr(a.flag, 1);
+    if (valid) store_herm_row<UP>(a.Ginv + (size_t)p * tri(UP), i, R);
+    for (int j = 0; j < a.J; ++j) {
+        const float2 m = a.mf[((size_t)pp * a.J + j) * UP + i];
+        const float2 yr = row_apply<UP>(R, sbuf[q], i, m);
+        if (valid) a.yreg[((size_t)p * a.J + j) * UP + i] = yr;
+    }
+}
+
+// Fused (world == 1): G^{-1} in registers, all T iterations of Alg. 1 on chip.
+// CTA = NT subcarriers x C clusters x UP lanes.
+template <int UP>
+__global__ void __launch_bounds__(512) k_admm_gj(UlArgs a) {
+    extern __shared__ __align__(16) float2 sm[];
+    const int C = a.C_loc, NT = a.NT;
+    float2* pbuf = sm;                                  // [NT*C][UP] per-pair line
+    float2* W = pbuf + (size_t)NT * C * UP;             // [NT][C][UP]
+    float2* Sv = W + (size_t)NT * C * UP;               // [NT][UP]
+    const int tid = threadIdx.x;
+    const int q = tid / UP, i = tid % UP;
+    const int nl = q / C, c = q % C;
+    const int n0 = blockIdx.x * NT;
+    const int n = n0 + nl;
+    const bool valid = n < a.N;
+    const size_t pair = (size_t)c * a.N + (valid ? n : a.N - 1);
+    float2* buf = pbuf + (size_t)q * UP;
+
+    float2 R[UP];
+    load_herm_row<UP>(a.Ginv + pair * tri(UP), i, R); // row i of B_c^{-1} (k_inv_ul)
+#pragma unroll
+    for (int j = 0; j < UP; ++j) R[j] = c_scale(R[j], a.rho);   // rho B_c^{-1} (eq. (3))
+
+    for (int jj = 0; jj < a.J; ++jj) {
+        const float2 yreg = a.yreg[(pair * a.J + jj) * UP + i];  // B^{-1} H^H y (Alg. 1 line 8)
+        float2 lam = make_float2(0.f, 0.f), z = yreg, w = yreg;   // line 10
+        for (int t = 1; t <= a.T; ++t) {
+            if (t > 1) {
+                const float2 s = Sv[nl * UP + i];
+                lam = c_add(lam, c_scale(c_sub(z, s), a.gamma));     // line 12
+                const float2 v = c_sub(s, lam);
+                z = c_add(yreg, row_apply<UP>(R, buf, i, v));       // line 15, eq. (3)
+                w = c_add(z, lam);                                   // line 17
+            }
+            W[((size_t)nl * C + c) * UP + i] = valid ? w : make_float2(0.f, 0.f);
+            __syncthreads();
+            if (tid < NT * UP) {                                     // line 18 (consensus) + 19 (prox)
+                const int el = tid / UP, uu = tid % UP;
+                Sv[el * UP + uu] = prox(cluster_sum(W, C, UP, el, uu), a.px);
+            }
+            __syncthreads();
+        }
+        if (tid < NT * UP) {
+            const int el = tid / UP, uu = tid % UP;
+            const int nn = n0 + el;
+            if (nn < a.N && uu < a.U) {
+                const float2 s = Sv[el * UP + uu];
+                a.s_hat[((size_t)nn * a.J + jj) * a.U + uu] = s;
+                if (a.hard) a.hard[((size_t)nn * a.J + jj) * a.U + uu] = slice_bits(s, a.md);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Split path: one iteration (or the init t = 1) for all local clusters of NT
+// subcarriers, clusters visited in chunks of CCH (any C_loc); writes the
+// local partial consensus sum (fixed cluster order) into wbuf.
+template <int UP>
+__global__ void __launch_bounds__(512) k_admm_it(UlArgs a, int CCH) {
+    extern __shared__ __align__(16) float2 sm[];
+    const int C = a.C_loc, NT = a.NT, J = a.J;
+    float2* pbuf = sm;                                  // [NT*CCH][UP]
+    float2* W = pbuf + (size_t)NT * CCH * UP;           // [NT][CCH][UP]
+    float2* Sv = W + (size_t)NT * CCH * UP;             // [NT][J][UP]
+    float2* Acc = Sv + (size_t)NT * J * UP;             // [NT][J][UP]
+    const int tid = threadIdx.x;
+    const int q = tid / UP, i = tid % UP;
+    const int nl = q / CCH, cl = q % CCH;
+    const int n0 = blockIdx.x * NT;
+    const int n = n0 + nl;
+    const int nn = n < a.N ? n : a.N - 1;
+    float2* buf = pbuf + (size_t)q * UP;
+    for (int e = tid; e < NT * J * UP; e += blockDim.x) {
+        const int el = e / (J * UP);
+        const bool ok = n0 + el < a.N && !a.init;
+        Sv[e] = prox(ok ? a.wbuf[(size_t)n0 * J * UP + e] : make_float2(0.f, 0.f), a.px);
+        Acc[e] = make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    for (int c0 = 0; c0 < C; c0 += CCH) {
+        const int c = c0 + cl;
+        const bool valid = n < a.N && c < C;
+        const size_t pair = (size_t)(c < C ? c : C - 1) * a.N + nn;
+        float2 R[UP];
+        if (!a.init) {
+            load_herm_row<UP>(a.Ginv + pair * tri(UP), i, R);
+#pragma unroll
+            for (int j = 0; j < UP; ++j) R[j] = c_scale(R[j], a.rho);
+        }
+        for (int jj = 0; jj < J; ++jj) {
+            const size_t o = (pair * J + jj) * UP + i;
+            const float2 yreg = a.yreg[o];
+            float2 lam, z, w;
+            if (a.init) {                                                // line 10
+                lam = make_float2(0.f, 0.f);
+                z = yreg;
+                w = yreg;
+            } else {
+                const float2 s = Sv[((size_t)nl * J + jj) * UP + i];
+                lam = c_add(a.lam[o], c_scale(c_sub(a.z[o], s), a.gamma));   // line 12
+                z = c_add(yreg, row_apply<UP>(R, buf, i, c_sub(s, lam)));    // line 15
+                w = c_add(z, lam);                                           // line 17
+            }
+            if (valid) { a.lam[o] = lam; a.z[o] = z; }
+            W[((size_t)nl * CCH + cl) * UP + i] = valid ? w : make_float2(0.f, 0.f);
+            __syncthreads();
+            if (tid < NT * UP) {
+                const int el = tid / UP, uu = tid % UP;
+                float2* ac = Acc + ((size_t)el * J + jj) * UP + uu;
+                *ac = c_add(*ac, cluster_sum(W, CCH, UP, el, uu));
+            }
+            __syncthreads();
+        }
+    }
+    for (int e = tid; e < NT * J * UP; e += blockDim.x)
+        if (n0 + e / (J * UP) < a.N) a.wbuf[(size_t)n0 * J * UP + e] = Acc[e];
+}
+
+// ============================================================ ADMM-DL
+
+
+// x_c = H_c^H r (r = B^{-1} q published in buf): lanes own antennas s = i, i+UP, ...
+template <int UP>
+__device__ __forceinline__ void bf_output(const float2* __restrict__ Hd, float2* buf, int i, float2 ri, int U, int S,
+                                          float2* __restrict__ xo, bool valid) {
+    buf[i] = ri;
+    __syncwarp();
+    float2 r[UP];
+    read_vec<UP>(buf, r);
+    for (int s = i; s < S; s += UP) {
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < UP; ++u)
+            if (u < U) c_fmac(acc, __ldg(Hd + (size_t)u * S + s), r[u]);
+        if (valid) xo[s] = acc;
+    }
+    __syncwarp();
+}
+
+// Split path: B^{-1} per pair.
+template <int UP>
+__global__ void __launch_bounds__(256, UP == 32 ? 1 : 3) k_inv_dl(DlArgs a, long npairs) {
+    __shared__ __align__(16) float2 sbuf[256 / UP][UP];
+    const int q = threadIdx.x / UP, i = threadIdx.x % UP;
+    const long p = (long)blockIdx.x * (256 / UP) + q;
+    const bool valid = p < npairs;
+    const long pp = valid ? p : npairs - 1;
+    float2 R[UP];
+    load_herm_row<UP>(a.G + (size_t)pp * tri(UP), i, R);
+    const bool ok = gj_invert<UP>(R, sbuf[q], i);
+    if (!ok && valid) atomicOr(a.flag, 1);
+    if (valid) store_herm_row<UP>(a.Binv + (size_t)p * tri(UP), i, R);
+}
+
+// Fused (world == 1): B^{-1} in registers; init, T-1 consensus iterations of
+// Alg. 3 in the exact m-form (m_c = q - rho^{-1} B^{-1} q, q = z + lambda;
+// DESIGN.md section 5) and the output pass x_c = H_c^H B^{-1} q.
+template <int UP>
+__global__ void __launch_bounds__(512) k_bf_gj(DlArgs a) {
+    extern __shared__ __align__(16) float2 sm[];
+    const int C = a.C_loc, NT = a.NT;
+    float2* pbuf = sm;
+    float2* W = pbuf + (size_t)NT * C * UP;
+    float2* Ws = W + (size_t)NT * C * UP;
+    const int tid = threadIdx.x;
+    const int q = tid / UP, i = tid % UP;
+    const int nl = q / C, c = q % C;
+    const int n0 = blockIdx.x * NT;
+    const int n = n0 + nl;
+    const bool valid = n < a.N;
+    const int nn = valid ? n : a.N - 1;
+    const size_t pair = (size_t)c * a.N + nn;
+    float2* buf = pbuf + (size_t)q * UP;
+
+    // the output pass re-reads H_c: start pulling this pair's tile into L2 now
+    if (i == 0) {
+        const size_t bytes = (size_t)a.U * a.S * 8;
+        if ((bytes & 15) == 0 && bytes < (1u << 20))
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.Hd + pair * (size_t)a.U * a.S),
+                         "r"((uint32_t)bytes) : "memory");
+    }
+    float2 R[UP];
+    load_herm_row<UP>(a.Binv + pair * tri(UP), i, R);  // row i of B_c^{-1} (k_inv_dl)
+
+    for (int jj = 0; jj < a.J; ++jj) {
+        const float2 sv = i < a.U ? a.s[((size_t)nn * a.J + jj) * a.U + i] : make_float2(0.f, 0.f);
+        float2 lam = make_float2(0.f, 0.f);
+        float2 qv = c_scale(sv, a.a0);                                   // line 8: z = a0 s
+        for (int t = 2; t <= a.T; ++t) {
+            const float2 bq = row_apply<UP>(R, buf, i, qv);
+            const float2 m = c_sub(qv, c_scale(bq, a.rho_inv));          // line 11 (m-form)
+            const float2 w = c_sub(m, lam);                              // line 12
+            W[((size_t)nl * C + c) * UP + i] = valid ? w : make_float2(0.f, 0.f);
+            __syncthreads();
+            if (tid < NT * UP) Ws[tid] = cluster_sum(W, C, UP, tid / UP, tid % UP);   // line 13
+            __syncthreads();
+            const float2 z = c_add(w, c_scale(c_sub(sv, Ws[nl * UP + i]), a.inv_c));  // line 14
+            lam = c_sub(lam, c_scale(c_sub(m, z), a.gamma));                         // line 15
+            qv = c_add(z, lam);
+            __syncthreads();
+        }
+        const float2 r = row_apply<UP>(R, buf, i, qv);                  // B^{-1} q
+        bf_output<UP>(a.Hd + pair * (size_t)a.U * a.S, buf, i, r, a.U, a.S,
+                      a.x + (pair * a.J + jj) * a.S, valid);            // line 20 / output
+    }
+}
+
+// Split path step t (2..T): complete iteration t-1 (or the init when t == 2),
+// then m, w_c and the local partial sum.  step == T+1: complete, write x_c.
+// Clusters in chunks of CCH.
+template <int UP>
+__global__ void __launch_bounds__(512) k_bf_it(DlArgs a, int CCH) {
+    extern __shared__ __align__(16) float2 sm[];
+    const int C = a.C_loc, NT = a.NT, J = a.J;
+    float2* pbuf = sm;                                  // [NT*CCH][UP]
+    float2* W = pbuf + (size_t)NT * CCH * UP;           // [NT][CCH][UP]
+    float2* Wv = W + (size_t)NT * CCH * UP;             // [NT][J][UP]  allreduced w^(t-1)
+    float2* Acc = Wv + (size_t)NT * J * UP;             // [NT][J][UP]
+    const int tid = threadIdx.x;
+    const int q = tid / UP, i = tid % UP;
+    const int nl = q / CCH, cl = q % CCH;
+    const int n0 = blockIdx.x * NT;
+    const int n = n0 + nl;
+    const int nn = n < a.N ? n : a.N - 1;
+    float2* buf = pbuf + (size_t)q * UP;
+    const bool fin = a.step > a.T;
+    const bool first = a.step == 2;
+    for (int e = tid; e < NT * J * UP; e += blockDim.x) {
+        const int el = e / (J * UP);
+        Wv[e] = (n0 + el < a.N && !first) ? a.wbuf[(size_t)n0 * J * UP + e] : make_float2(0.f, 0.f);
+        Acc[e] = make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    for (int c0 = 0; c0 < C; c0 += CCH) {
+        const int c = c0 + cl;
+        const bool valid = n < a.N && c < C;
+        const size_t pair = (size_t)(c < C ? c : C - 1) * a.N + nn;
+        float2 R[UP];
+        load_herm_row<UP>(a.Binv + pair * tri(UP), i, R);
+        for (int jj = 0; jj < J; ++jj) {
+            const size_t o = (pair * J + jj) * UP + i;
+            const float2 sv = i < a.U ? a.s[((size_t)nn * J + jj) * a.U + i] : make_float2(0.f, 0.f);
+            float2 lam, qv;
+            if (first) {                                                 // line 8
+                lam = make_float2(0.f, 0.f);
+                qv = c_scale(sv, a.a0);
+            } else {                                                     // lines 14-15 of t-1
+                const float2 mo = a.m[o], lo = a.lam[o];
+                const float2 w = c_sub(mo, lo);
+                const float2 z = c_add(w, c_scale(c_sub(sv, Wv[((size_t)nl * J + jj) * UP + i]), a.inv_c));
+                lam = c_sub(lo, c_scale(c_sub(mo, z), a.gamma));
+                qv = c_add(z, lam);
+            }
+            const float2 bq = row_apply<UP>(R, buf, i, qv);
+            if (fin) {
+                bf_output<UP>(a.Hd + pair * (size_t)a.U * a.S, buf, i, bq, a.U, a.S, a.x + (pair * J + jj) * a.S, valid);
+                continue;
+            }
+            const float2 m = c_sub(qv, c_scale(bq, a.rho_inv));          // line 11
+            if (valid) { a.m[o] = m; a.lam[o] = lam; }
+            W[((size_t)nl * CCH + cl) * UP + i] = valid ? c_sub(m, lam) : make_float2(0.f, 0.f);   // line 12
+            __syncthreads();
+            if (tid < NT * UP) {
+                const int el = tid / UP, uu = tid % UP;
+                float2* ac = Acc + ((size_t)el * J + jj) * UP + uu;
+                *ac = c_add(*ac, cluster_sum(W, CCH, UP, el, uu));
+            }
+            __syncthreads();
+        }
+    }
+    if (fin) return;
+    for (int e = tid; e < NT * J * UP; e += blockDim.x)
+        if (n0 + e / (J * UP) < a.N) a.wbuf[(size_t)n0 * J * UP + e] = Acc[e];
+}
+
+// ============================================================ launchers
+static int cdiv_i(long x, long y) { return (int)((x + y - 1) / y); }
+
+size_t iter_smem(int UP, int NT, int C) { return ((size_t)2 * NT * C * UP + (size_t)NT * UP) * 8; }
+
+// CTA shape: NT subcarriers x C_loc clusters x UP lanes (<= 1024 threads).
+bool iter_cfg(int UP, int C_loc, int N, int max_smem, int* NT) {
+    const int per_n = C_loc * UP;
+    if (per_n > 512) return false;
+    int nt = std::max(1, 512 / per_n);
+    nt = std::min(nt, N);
+    while (nt > 1 && iter_smem(UP, nt, C_loc) > (size_t)max_smem) --nt;
+    if (iter_smem(UP, nt, C_loc) > (size_t)max_smem) return false;
+    *NT = nt;
+    return true;
+}
+
+template <typename K>
+static void big_smem(K k, size_t smem) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+cudaError_t launch_inv_ul(const LaunchCtx& L, int UP, UlArgs a, long npairs) {
+    DBP_DISPATCH_UP(UP, k_inv_ul<UPc><<<cdiv_i(npairs, 256 / UPc), 256, 0, L.stream>>>(a, npairs));
+    L.count(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_admm_gj(const LaunchCtx& L, int UP, UlArgs a) {
+    const size_t smem = iter_smem(UP, a.NT, a.C_loc);
+    DBP_DISPATCH_UP(UP, big_smem(k_admm_gj<UPc>, smem);
+                    k_admm_gj<UPc><<<cdiv_i(a.N, a.NT), a.NT * a.C_loc * UPc, smem, L.stream>>>(a));
+    L.count(1);
+    return cudaGetLastError();
+}
+
+size_t split_smem(int UP, int NT, int CCH, int J) { return ((size_t)2 * NT * CCH * UP + (size_t)2 * NT * J * UP) * 8; }
+
+// Split CTA shape: CCH clusters per chunk, NT subcarriers, ~512 threads.
+void split_cfg(int UP, int C_loc, int N, int J, int* NT, int* CCH) {
+    int cch = std::max(1, std::min(C_loc, 512 / UP));
+    int nt = std::max(1, std::min(N, 512 / (cch * UP)));
+    *NT = nt;
+    *CCH = cch;
+}
+
+cudaError_t launch_admm_it(const LaunchCtx& L, int UP, UlArgs a, int CCH) {
+    const size_t smem = split_smem(UP, a.NT, CCH, a.J);
+    DBP_DISPATCH_UP(UP, big_smem(k_admm_it<UPc>, smem);
+                    k_admm_it<UPc><<<cdiv_i(a.N, a.NT), a.NT * CCH * UPc, smem, L.stream>>>(a, CCH));
+    L.count(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_inv_dl(const LaunchCtx& L, int UP, DlArgs a, long npairs) {
+    DBP_DISPATCH_UP(UP, k_inv_dl<UPc><<<cdiv_i(npairs, 256 / UPc), 256, 0, L.stream>>>(a, npairs));
+    L.count(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bf_gj(const LaunchCtx& L, int UP, DlArgs a) {
+    const size_t smem = iter_smem(UP, a.NT, a.C_loc);
+    DBP_DISPATCH_UP(UP, big_smem(k_bf_gj<UPc>, smem);
+                    k_bf_gj<UPc><<<cdiv_i(a.N, a.NT), a.NT * a.C_loc * UPc, smem, L.stream>>>(a));
+    L.count(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bf_it(const LaunchCtx& L, int UP, DlArgs a, int CCH) {
+    const size_t smem = split_smem(UP, a.NT, CCH, a.J);
+    DBP_DISPATCH_UP(UP, big_smem(k_bf_it<UPc>, smem);
+                    k_bf_it<UPc><<<cdiv_i(a.N, a.NT), a.NT * CCH * UPc, smem, L.stream>>>(a, CCH));
+    L.count(1);
+    return cudaGetLastError();
+}
+
+}  // namespace dbp

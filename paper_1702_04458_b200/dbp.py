@@ -22,10 +22,11 @@ REG = {"mmse": 0, "zf": 1, "box": 2}
 MOD = {"bpsk": 1, "qpsk": 2, "qam16": 4, "qam64": 6}
 ALGO = {"admm_ul": 0, "cg_ul": 1, "admm_dl": 2}
 OPT_FORCE_SPLIT = 1
+OPT_KERNEL_TIMING = 2
 
 EXPORTS = ["dbp_get_unique_id", "dbp_ctx_create", "dbp_ctx_destroy", "dbp_set_option", "dbp_get_stats",
            "dbp_last_error", "dbp_workspace_bytes", "dbp_detect_admm", "dbp_detect_cg",
-           "dbp_beamform_admm", "dbp_slice", "dbp_sync"]
+           "dbp_beamform_admm", "dbp_slice", "dbp_sync", "dbp_get_kernel_times"]
 
 
 class DbpError(RuntimeError):
@@ -42,6 +43,10 @@ class Dims(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [("allreduce_calls", ctypes.c_int64), ("allreduce_bytes", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("consensus_rounds", ctypes.c_int64)]
+
+
+class KernelTime(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 40), ("launches", ctypes.c_int64), ("total_ms", ctypes.c_double)]
 
 
 _lib = None
@@ -69,6 +74,7 @@ def load() -> ctypes.CDLL:
         "dbp_beamform_admm": [P, P, P, P, F, F, F, ctypes.c_int32, P, P, S, P],
         "dbp_slice": [P, I, I64, P, P, P],
         "dbp_sync": [P, P],
+        "dbp_get_kernel_times": [P, P, I, P, I],
     }
     for name, args in sigs.items():
         fn = getattr(lib, name)
@@ -169,6 +175,13 @@ class Context:
         out = ctypes.c_size_t()
         _check(load().dbp_workspace_bytes(self._h, ctypes.byref(d), ALGO[algo], ctypes.byref(out)))
         return out.value
+
+    def kernel_times(self, reset: bool = False) -> dict:
+        """{name: (launches, total_ms)} recorded under OPT_KERNEL_TIMING (blocks on the events)."""
+        arr = (KernelTime * 64)()
+        n = ctypes.c_int()
+        _check(load().dbp_get_kernel_times(self._h, arr, 64, ctypes.byref(n), int(reset)))
+        return {arr[i].name.decode(): (arr[i].launches, arr[i].total_ms) for i in range(n.value)}
 
     def sync(self, stream=None):
         _check(load().dbp_sync(self._h, _stream(stream, None) if stream is not None else _cur_stream()))
