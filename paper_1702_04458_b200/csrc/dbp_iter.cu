@@ -65,7 +65,7 @@ __device__ __forceinline__ void read_vec(const float2* buf, float2 (&v)[UP]) {
 template <int UP>
 __device__ __forceinline__ bool gj_invert(float2 (&r)[UP], float2* prow, int i) {
     bool ok = true;
-#pragma unroll (UP <= 16 ? UP : 1)
+#pragma unroll
     for (int k = 0; k < UP; ++k) {
         // lane k publishes its row (pivot row)
         if (i == k) {
@@ -76,31 +76,24 @@ __device__ __forceinline__ bool gj_invert(float2 (&r)[UP], float2* prow, int i) 
         __syncwarp();
         float2 pr[UP];
         read_vec<UP>(prow, pr);
-        // pivot = pr[k] (real part; HPD => real, positive)
-        float piv = 0.f;
-        float2 fk = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int j = 0; j < UP; ++j) {
-            if (j == k) { piv = pr[j].x; fk = r[j]; }
-        }
+        // pivot (real and positive for HPD input), then one divergence-free
+        // update for every lane:  r_j <- m r_j - fs pr_j (j != k),  r_k <- -fs,
+        // with m = 0, fs = -1/piv on the pivot lane (row k <- row k / piv,
+        // (k,k) <- 1/piv) and m = 1, fs = r_k/piv elsewhere (Jordan step).
+        const float piv = pr[k].x;
         const bool good = (piv > 0.f) && (piv < INFINITY);
         ok = ok && good;
-        const float ip = good ? 1.0f / piv : 0.f;
-        if (i == k) {
+        const float ip = good ? __frcp_rn(piv) : 0.f;
+        const bool me = (i == k);
+        const float m = me ? 0.f : 1.f;
+        const float2 fs = me ? make_float2(-ip, 0.f) : c_scale(r[k], ip);
 #pragma unroll
-            for (int j = 0; j < UP; ++j) r[j] = (j == k) ? make_float2(ip, 0.f) : c_scale(pr[j], ip);
-        } else {
-            // r_j -= f * pr_j * ip  (j != k);  r_k = -f * ip
-            const float2 f = c_scale(fk, ip);
-#pragma unroll
-            for (int j = 0; j < UP; ++j) {
-                if (j == k) r[j] = make_float2(-f.x, -f.y);
-                else {
-                    r[j].x -= f.x * pr[j].x - f.y * pr[j].y;
-                    r[j].y -= f.x * pr[j].y + f.y * pr[j].x;
-                }
-            }
+        for (int j = 0; j < UP; ++j) {
+            if (j == k) continue;
+            r[j].x = fmaf(-fs.x, pr[j].x, fmaf(fs.y, pr[j].y, m * r[j].x));
+            r[j].y = fmaf(-fs.x, pr[j].y, fmaf(-fs.y, pr[j].x, m * r[j].y));
         }
+        r[k] = make_float2(-fs.x, -fs.y);
         __syncwarp();
     }
     return ok;
