@@ -126,11 +126,11 @@ def host_cores() -> int:
         return os.cpu_count() or 1
 
 
-def cpu_baseline(budget_s: float = 12.0, n_sub: int = 240) -> dict:
+def cpu_baseline(budget_s: float = 10.0, n_sub: int = 240) -> dict:
     import oracle
     oracle.build()
     tot_t, tot_b, reps = 0.0, 0, 0
-    while tot_t < budget_s and reps < 50:
+    while tot_t < budget_s and reps < 1000:
         dt, b = _oracle_sample(n_sub)
         tot_t += dt
         tot_b += b
