@@ -374,7 +374,7 @@ extern "C" dbp_status dbp_detect_admm(dbp_ctx* c, const dbp_dims* d, const dbp_c
     if (reg < 0 || reg > 2) return fail(DBP_ERR_INVALID_ARG, "reg %d", reg);
     if (!mod_ok(mod)) return fail(DBP_ERR_INVALID_ARG, "mod %d", mod);
     if (T < 1) return fail(DBP_ERR_INVALID_ARG, "T must be >= 1");
-    if (pre_smem(sh.UP, sh.S, sh.U, sh.J, PRE_ADMM_) > (size_t)c->max_smem) return fail(DBP_ERR_UNSUPPORTED, "S too large for the preprocessing tile");
+    if (prelr_smem(sh.UP, sh.S, sh.U, sh.J, true) > (size_t)c->max_smem) return fail(DBP_ERR_UNSUPPORTED, "S too large for the preprocessing tile");
     CU(cudaSetDevice(c->device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const Layout Lw = layout(sh, DBP_ALGO_ADMM_UL);
@@ -391,12 +391,13 @@ extern "C" dbp_status dbp_detect_admm(dbp_ctx* c, const dbp_dims* d, const dbp_c
     float2* mf = reinterpret_cast<float2*>(k.ws + Lw.off[1]);
     LaunchCtx L{s, c->d_flag, &c->launches};
 
-    // a1, a3: G_c = H_c^H H_c + rho I and H_c^H y_c (Alg. 1 lines 7-8)
-    KT("gram_ul", launch_gram(L, sh.UP, PRE_ADMM_, dH, dy, sh.S, sh.U, sh.J, sh.pairs(), rho, G, mf));
+    float2* yreg = reinterpret_cast<float2*>(k.ws + Lw.off[2]);
+    // a1-a3: G_c = H_c^H H_c + rho I, B_c^{-1} and y^reg = B_c^{-1} H_c^H y_c (Alg. 1 lines 7-8)
+    KT("pre_ul", launch_prelr(L, sh.UP, 1, dH, dy, sh.S, sh.U, sh.J, sh.pairs(), rho, G, yreg));
 
     UlArgs a{};
     a.G = G; a.mf = mf; a.Ginv = G;
-    a.yreg = reinterpret_cast<float2*>(k.ws + Lw.off[2]);
+    a.yreg = yreg;
     a.lam = reinterpret_cast<float2*>(k.ws + Lw.off[3]);
     a.z = reinterpret_cast<float2*>(k.ws + Lw.off[4]);
     a.wbuf = reinterpret_cast<float2*>(k.ws + Lw.off[5]);
@@ -409,13 +410,11 @@ extern "C" dbp_status dbp_detect_admm(dbp_ctx* c, const dbp_dims* d, const dbp_c
     a.md = modem_of(mod);
     int NT, CCH;
     if (c->world == 1 && !c->force_split && iter_cfg(sh.UP, sh.C_loc, sh.N, c->max_smem, &NT)) {
-        // a2: B_c^{-1} and y^reg; a4-a8 fused: all T iterations on chip (world == 1)
-        KT("inv_ul", launch_inv_ul(L, sh.UP, a, sh.pairs()));
+        // a4-a8 fused: all T iterations on chip (world == 1)
         a.NT = NT;
         KT("admm_fused", launch_admm_gj(L, sh.UP, a));
         c->consensus_rounds += T;
     } else {
-        KT("inv_ul", launch_inv_ul(L, sh.UP, a, sh.pairs()));              // a2 + yreg
         split_cfg(sh.UP, sh.C_loc, sh.N, sh.J, &NT, &CCH);
         a.NT = NT;
         const size_t nw = (size_t)sh.N * sh.J * sh.UP;
@@ -440,7 +439,7 @@ extern "C" dbp_status dbp_detect_cg(dbp_ctx* c, const dbp_dims* d, const dbp_cf3
     if (!(rho >= 0.f) || !std::isfinite(rho)) return fail(DBP_ERR_INVALID_ARG, "rho must be >= 0 (P376)");
     if (!mod_ok(mod)) return fail(DBP_ERR_INVALID_ARG, "mod %d", mod);
     if (T < 1) return fail(DBP_ERR_INVALID_ARG, "T must be >= 1");
-    if (pre_smem(sh.UP, sh.S, sh.U, sh.J, PRE_CG_) > (size_t)c->max_smem) return fail(DBP_ERR_UNSUPPORTED, "S too large for the preprocessing tile");
+    if (prelr_smem(sh.UP, sh.S, sh.U, sh.J, true) > (size_t)c->max_smem) return fail(DBP_ERR_UNSUPPORTED, "S too large for the preprocessing tile");
     CU(cudaSetDevice(c->device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const Layout Lw = layout(sh, DBP_ALGO_CG_UL);
@@ -468,8 +467,8 @@ extern "C" dbp_status dbp_detect_cg(dbp_ctx* c, const dbp_dims* d, const dbp_cf3
 
     // b1: per-pair Gram H_c^H H_c and matched filter H_c^H y_c, then the
     // per-GPU sums (G_loc, local y^MRC) in fixed cluster order.
-    KT("gram_cg", launch_gram(L, sh.UP, PRE_CG_, static_cast<const float2*>(k.io[0].dev),
-                               static_cast<const float2*>(k.io[1].dev), sh.S, sh.U, sh.J, sh.pairs(), 0.f, Gp, mf));
+    KT("pre_cg", launch_prelr(L, sh.UP, 0, static_cast<const float2*>(k.io[0].dev),
+                              static_cast<const float2*>(k.io[1].dev), sh.S, sh.U, sh.J, sh.pairs(), 0.f, Gp, mf));
     KT("cg_gsum", launch_cg_gsum(L, sh.UP, Gp, mf, sh.C_loc, sh.N, sh.J, const_cast<float2*>(a.Gloc), a.wbuf));
     const size_t nw = (size_t)sh.N * sh.J * sh.UP;
     if ((st = allreduce(c, a.wbuf, nw, s))) return st;              // line 4: y^MRC consensus
@@ -499,7 +498,7 @@ extern "C" dbp_status dbp_beamform_admm(dbp_ctx* c, const dbp_dims* d, const dbp
     if (!(eps >= 0.f)) return fail(DBP_ERR_INVALID_ARG, "eps must be >= 0");
     if (eps > 0.f) return fail(DBP_ERR_UNSUPPORTED, "eps > 0 (Lemma 2 shrink) is not in v1");
     if (T < 1) return fail(DBP_ERR_INVALID_ARG, "T must be >= 1");
-    if (pre_smem(sh.UP, sh.S, sh.U, sh.J, PRE_BF_) > (size_t)c->max_smem) return fail(DBP_ERR_UNSUPPORTED, "S too large for the preprocessing tile");
+    if (prelr_smem(sh.UP, sh.S, sh.U, sh.J, false) > (size_t)c->max_smem) return fail(DBP_ERR_UNSUPPORTED, "S too large for the preprocessing tile");
     CU(cudaSetDevice(c->device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const Layout Lw = layout(sh, DBP_ALGO_ADMM_DL);
@@ -526,16 +525,14 @@ extern "C" dbp_status dbp_beamform_admm(dbp_ctx* c, const dbp_dims* d, const dbp
     a.a0 = (float)std::max((double)sh.U / ((double)sh.C * sh.S), 1.0 / sh.C);   // Alg. 3 line 8 (P507)
     a.inv_c = (float)(1.0 / sh.C);
 
-    // c1: B_c = H_c H_c^H + rho^{-1} I_U (Alg. 3 line 5)
-    KT("gram_dl", launch_gram(L, sh.UP, PRE_BF_, a.Hd, nullptr, sh.S, sh.U, sh.J, sh.pairs(), a.rho_inv, G, nullptr));
+    // c1: B_c = H_c H_c^H + rho^{-1} I_U and its inverse (Alg. 3 lines 5-6)
+    KT("pre_dl", launch_prelr(L, sh.UP, 2, a.Hd, nullptr, sh.S, sh.U, sh.J, sh.pairs(), a.rho_inv, G, nullptr));
     int NT, CCH;
     if (c->world == 1 && !c->force_split && iter_cfg(sh.UP, sh.C_loc, sh.N, c->max_smem, &NT)) {
-        KT("inv_dl", launch_inv_dl(L, sh.UP, a, sh.pairs()));              // c1 inverse
         a.NT = NT;
         KT("bf_fused", launch_bf_gj(L, sh.UP, a));                         // c2-c4
         c->consensus_rounds += T - 1;
     } else {
-        KT("inv_dl", launch_inv_dl(L, sh.UP, a, sh.pairs()));              // c1 inverse
         split_cfg(sh.UP, sh.C_loc, sh.N, sh.J, &NT, &CCH);
         a.NT = NT;
         const size_t nw = (size_t)sh.N * sh.J * sh.UP;

@@ -2,6 +2,7 @@
 // kernels (dbp_kernels.cu).  Not installed; not part of the public ABI.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -43,7 +44,17 @@ struct CgArgs {
 
 
 
+// 3-D TMA tensor map over 8-byte elements (dims innermost first, box may exceed
+// the tensor: out-of-bounds elements are zero-filled).  false if unsupported.
+bool make_map3(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1,
+               uint32_t b2);
 size_t pre_smem(int UP, int S, int U, int J, int mode);
+size_t prelr_smem(int UP, int S, int U, int J, bool ul);
+bool launch_prefold(const LaunchCtx& L, int UP, int mode, const float2* H, const float2* y, int S, int U, int J,
+                    long npairs, float delta, float2* Gout, float2* vout);
+// Lane-row preprocessing: mode 0 = Gram + H^H y (CG), 1 = G^{-1} + y^reg (ADMM-UL), 2 = B^{-1} (ADMM-DL)
+cudaError_t launch_prelr(const LaunchCtx& L, int UP, int mode, const float2* H, const float2* y, int S, int U, int J,
+                         long npairs, float delta, float2* Gout, float2* vout);
 // Gram (+ delta I) per pair -> Gout [pairs][tri(UP)]; matched filter -> mfout [pairs][J][UP] (not for BF)
 cudaError_t launch_gram(const LaunchCtx& L, int UP, int mode, const float2* H, const float2* y, int S, int U,
                         int J, long npairs, float delta, float2* Gout, float2* mfout);
