@@ -44,25 +44,30 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Build libdbp.so in-tree (or `out`, with extra -D`defines`, for tuning variants)."""
+    if out is None and not force and not stale():
         return LIB
+    dest = out or LIB
     inc, lib = nccl_dirs()
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = dest + f".tmp{os.getpid()}"
     cmd = ["nvcc", ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",
            "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
-           "-o", tmp] + sources() + ["-L", lib, "-l:libnccl.so.2", f"-Xlinker=-rpath={lib}"]
+           *[f"-D{d}" for d in defines], "-o", tmp] + sources() + ["-L", lib, "-l:libnccl.so.2", f"-Xlinker=-rpath={lib}"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libdbp.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, dest)
+    return dest
 
 
 if __name__ == "__main__":
-    build(force=True, verbose="-v" in sys.argv)
-    print(LIB)
+    # python build.py [-v] [--out PATH] [-DNAME=VAL ...]
+    args = sys.argv[1:]
+    out = args[args.index("--out") + 1] if "--out" in args else None
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    print(build(force=True, verbose="-v" in args, out=out, defines=defs))

@@ -41,6 +41,12 @@ __device__ __forceinline__ void c_fmacb(float2& acc, float2 a, float2 b) {
 }
 __device__ __forceinline__ float c_norm2(float2 a) { return fmaf(a.x, a.x, a.y * a.y); }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // Packed lower-triangular storage, row-major: (i, j), j <= i.
 __host__ __device__ constexpr int tri(int n) { return n * (n + 1) / 2; }
 __host__ __device__ __forceinline__ int pidx(int i, int j) { return (i * (i + 1)) / 2 + j; }

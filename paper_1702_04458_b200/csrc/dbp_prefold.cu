@@ -27,12 +27,14 @@
 //    R complex FMAs per pivot.  The matrix is Jacobi-scaled to unit diagonal
 //    first: pivots are then Schur complements <= 1, which lets the pivot row
 //    use the same update a - f conj(c_t) (f = 1 - 1/a_kk) without cancellation.
-//  * Every warp is an independent persistent worker with its own 2-stage
-//    mbarrier ring of 3-D TMA boxes (8 antennas x PW pairs per stage); there
-//    is no CTA-level barrier.  Bank conflicts: UL rows are padded to UP+2
-//    users (zero-filled out-of-bounds box) and pair q reads antenna
-//    (s + q) mod 8, which puts the PW pairs of a warp on distinct bank groups;
-//    DL boxes are {10 antennas, UP+1 users} (pair pitch = 5 mod 8 units).
+//  * Every warp is an independent persistent worker with its own 3-stage
+//    mbarrier ring of 3-D TMA boxes (4 antennas x PW pairs per stage); there
+//    is no CTA-level barrier.  Bank conflicts (UP = 16, 8 pairs per warp):
+//    UL rows are padded to UP+2 users (zero-filled out-of-bounds box elements,
+//    line pitch = 1 mod 8 16-B units) and pair q reads antenna (s + q/2) mod 4;
+//    DL boxes are {4 antennas, UP+1 users} (pair pitch = 2 mod 8 units) and
+//    pair q reads antenna pair (s/2 + q/4) mod 2.  Either way the 8 pairs'
+//    LDS.128 addresses fall on 8 distinct bank groups.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -43,16 +45,33 @@
 #include "dbp_internal.h"
 #include "dbp_lanerow.cuh"
 
+// tuning knobs (build.py -D...): TMA ring depth, UL antenna-loop unroll
+#ifndef DBP_PF_NST
+#define DBP_PF_NST 3
+#endif
+#ifndef DBP_PF_UNROLL
+#define DBP_PF_UNROLL 2
+#endif
+#ifndef DBP_PF_RCPRN
+#define DBP_PF_RCPRN 1
+#endif
+#ifndef DBP_PF_PUB_BRANCH
+#define DBP_PF_PUB_BRANCH 1
+#endif
+#pragma nv_diag_suppress 128   // MODE 0 returns before the inverse: "loop is not reachable"
+
 namespace dbp {
+
+constexpr int PF_UNROLL = DBP_PF_UNROLL;
 
 template <int UP>
 struct PF {
     static constexpr int R = 4;
     static constexpr int L = UP / R;                 // lanes per pair: 1, 2, 4
     static constexpr int PW = 32 / L;                // pairs per warp: 32, 16, 8
-    static constexpr int SC = 8;                     // antennas per stage
+    static constexpr int SC = 4;                     // antennas per stage
     static constexpr int WARPS = 4;
-    static constexpr int NST = 2;
+    static constexpr int NST = DBP_PF_NST;
     static constexpr int NSLOT = 10 * L;             // L * R(R+1)/2
 };
 
@@ -62,13 +81,13 @@ template <int UP, bool DL, int MODE>
 struct PFL {
     using P = PF<UP>;
     static constexpr bool MF = !DL && MODE != 2;
-    static constexpr int HL = DL ? P::SC + 2 : UP + 2;          // smem line (float2)
+    static constexpr int HL = DL ? P::SC : UP + 2;              // smem line (float2)
     static constexpr int NL = DL ? UP + 1 : P::SC;              // lines per pair
     static constexpr int HSZ = P::PW * NL * HL;                 // float2
     static constexpr int YSZ = MF ? P::PW * P::SC : 0;
     static constexpr int STG = ((HSZ + YSZ) * 8 + 127) / 128 * 128;   // bytes
     static constexpr int PLN = P::PW * (UP + 2);                // pivot lines (float2)
-    static constexpr int WREG = (P::NST * STG + PLN * 8 + 127) / 128 * 128;
+    static constexpr int WREG = (P::NST * STG + PLN * 8 + P::PW * UP * 4 + 127) / 128 * 128;
     static constexpr size_t SMEM = 128 + (size_t)P::WARPS * WREG;
 };
 
@@ -82,7 +101,7 @@ struct PfArgs {
 };
 
 template <int UP, bool DL, int MODE>
-__global__ void __launch_bounds__(128, 2)
+__global__ void __launch_bounds__(128, 3)
 k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmY, PfArgs a) {
     using P = PF<UP>;
     using Q = PFL<UP, DL, MODE>;
@@ -94,22 +113,24 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw) + warp * NST;
     unsigned char* wbase = smem_raw + 128 + (size_t)warp * Q::WREG;
     const int q = lane / L, l = lane % L;
-    float2* pl = reinterpret_cast<float2*>(wbase + NST * Q::STG) + q * (UP + 2);
+    float2* pl = reinterpret_cast<float2*>(wbase + NST * Q::STG) + q * (UP + 2);    // pivot column + E_k
+    float* dline = reinterpret_cast<float*>(wbase + NST * Q::STG + Q::PLN * 8) + q * UP;   // Jacobi scales
 
     int row[R];
 #pragma unroll
     for (int m = 0; m < R; ++m) row[m] = (m & 1) ? (m + 1) * L - 1 - l : m * L + l;
 
-    const long ngroups = (a.npairs + PW - 1) / PW;
-    const long gw = (long)blockIdx.x * P::WARPS + warp, W = (long)gridDim.x * P::WARPS;
-    const long nitems = gw < ngroups ? (ngroups - 1 - gw) / W + 1 : 0;
+    // (pair counts fit in int: launch_prefold takes npairs <= 2^30)
+    const int ngroups = (int)((a.npairs + PW - 1) / PW);
+    const int gw = blockIdx.x * P::WARPS + warp, W = gridDim.x * P::WARPS;
+    const int nitems = gw < ngroups ? (ngroups - 1 - gw) / W + 1 : 0;
     const int nch = (a.S + SC - 1) / SC;
-    const long nseq = nitems * nch;
+    const int nseq = nitems * nch;
 
-    auto issue = [&](long sq) {
-        const long item = sq / nch;
-        const int ch = (int)(sq % nch), st = (int)(sq % NST);
-        const int p0 = (int)((gw + item * W) * PW);
+    // sequence number sq -> (item, chunk, stage); issued NST ahead of consumption
+    auto issue = [&](int sq, int st) {
+        const int item = sq / nch, ch = sq - item * nch;
+        const int p0 = (gw + item * W) * PW;
         unsigned char* dst = wbase + st * Q::STG;
         mbar_arrive_expect_tx(&bar[st], (uint32_t)((Q::HSZ + Q::YSZ) * 8));
         if (DL) {
@@ -125,11 +146,12 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
     }
     __syncwarp();
     if (lane == 0)
-        for (long s = 0; s < NST && s < nseq; ++s) issue(s);
+        for (int s = 0; s < NST && s < nseq; ++s) issue(s, s);
 
-    long sq = 0;
-    for (long it = 0; it < nitems; ++it) {
-        const long p = (gw + it * W) * PW + q;
+    int sq = 0, st = 0;
+    uint32_t phase = 0;
+    for (int it = 0; it < nitems; ++it) {
+        const long p = (long)(gw + it * W) * PW + q;
         const bool valid = p < a.npairs;
 
         // ------------------------------------------------ Gram slots (+ matched filter)
@@ -140,16 +162,15 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
 #pragma unroll
         for (int m = 0; m < R; ++m) E[m] = make_float2(0.f, 0.f);
 
-        for (int ch = 0; ch < nch; ++ch, ++sq) {
-            const int st = (int)(sq % NST);
-            mbar_wait(&bar[st], (uint32_t)((sq / NST) & 1));
+        for (int ch = 0; ch < nch; ++ch) {
+            mbar_wait(&bar[st], phase);
             const float2* hs = reinterpret_cast<const float2*>(wbase + st * Q::STG);
             if (!DL) {
                 const float2* hq = hs + q * NL * HL;
                 const float2* yq = hs + Q::HSZ + q * SC;
-#pragma unroll
+#pragma unroll PF_UNROLL
                 for (int s = 0; s < SC; ++s) {
-                    const int sr = (s + q) & (SC - 1);
+                    const int sr = (s + (q >> 1)) & (SC - 1);     // pair-rotated antenna: conflict-free LDS.128
                     const float2* hrow = hq + sr * HL;
                     float2 h[UP];
                     read_vec<UP>(hrow, h);
@@ -168,8 +189,9 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
                 }
             } else {
                 const float2* hq = hs + q * NL * HL;
-#pragma unroll
-                for (int s = 0; s < SC; s += 2) {
+#pragma unroll 1
+                for (int s0 = 0; s0 < SC; s0 += 2) {
+                    const int s = (s0 + 2 * (q >> 2)) & (SC - 1);       // pair-rotated antenna pair
                     float4 o[R];
 #pragma unroll
                     for (int m = 0; m < R; ++m) o[m] = *reinterpret_cast<const float4*>(hq + row[m] * HL + s);
@@ -189,8 +211,10 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
             __syncwarp();
             if (lane == 0 && sq + NST < nseq) {
                 fence_proxy_async();
-                issue(sq + NST);
+                issue(sq + NST, st);
             }
+            ++sq;
+            if (++st == NST) { st = 0; phase ^= 1u; }
         }
 
         // diagonal: real, + delta
@@ -231,19 +255,13 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
         for (int m = 0; m < R; ++m) dr[m] = dg[m] > 0.f ? rsqrtf(dg[m]) : 1.f;
         __syncwarp();
 #pragma unroll
-        for (int m = 0; m < R; ++m) pl[row[m]] = make_float2(dr[m], 0.f);
+        for (int m = 0; m < R; ++m) dline[row[m]] = dr[m];
         __syncwarp();
-        float dv[UP];
-        {
-            float2 t2[UP];
-            read_vec<UP>(pl, t2);
-#pragma unroll
-            for (int t = 0; t < UP; ++t) dv[t] = t2[t].x;
-        }
 #pragma unroll
         for (int m = 0; m < R; ++m) {
 #pragma unroll
-            for (int t = 0; t < (m + 1) * L; ++t) A[pf_off(m, L) + t] = c_scale(A[pf_off(m, L) + t], dr[m] * dv[t]);
+            for (int t = 0; t < (m + 1) * L; ++t)
+                A[pf_off(m, L) + t] = c_scale(A[pf_off(m, L) + t], dr[m] * dline[t]);
             E[m] = c_scale(E[m], dr[m]);
         }
 
@@ -254,47 +272,67 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
             const int mk = k / L;
             const int lk = (mk & 1) ? (mk + 1) * L - 1 - k : k - mk * L;   // owner lane of row k
             __syncwarp();
-            // publish column k of the current matrix: c_j = a_jk
+            // publish column k of the current matrix: c_j = a_jk.  Stores are
+            // unconditional with the address selected (pl[UP+1] is a dump slot),
+            // so the sweep has no divergent branch and ptxas emits no
+            // divergent-path copy of it around __syncwarp.
+            float2* const dump = pl + UP + 1;
 #pragma unroll
             for (int m = 0; m < R; ++m)
-                if (k < (m + 1) * L && row[m] >= k) pl[row[m]] = A[pf_off(m, L) + k];
+                if (k < (m + 1) * L) *(row[m] >= k ? pl + row[m] : dump) = A[pf_off(m, L) + k];
+#if DBP_PF_PUB_BRANCH
             if (l == lk) {
 #pragma unroll
-                for (int m = 0; m < R; ++m) {
-                    if (m != mk) continue;
-#pragma unroll
-                    for (int t = 0; t < k && t < (m + 1) * L; ++t) pl[t] = c_conj(A[pf_off(m, L) + t]);
-                    if (MODE == 1) pl[UP] = E[m];
-                }
+                for (int t = 0; t < k && t < (mk + 1) * L; ++t) pl[t] = c_conj(A[pf_off(mk, L) + t]);
+                if (MODE == 1) pl[UP] = E[mk];
             }
+#else
+            {
+                const bool own = l == lk;
+#pragma unroll
+                for (int t = 0; t < k && t < (mk + 1) * L; ++t) *(own ? pl + t : dump) = c_conj(A[pf_off(mk, L) + t]);
+                if (MODE == 1) *(own ? pl + UP : dump) = E[mk];
+            }
+#endif
             __syncwarp();
-            float2 c[UP];
-            read_vec<UP>(pl, c);
             float2 cr[R];
 #pragma unroll
             for (int m = 0; m < R; ++m) cr[m] = pl[row[m]];
             const float2 Ek = MODE == 1 ? pl[UP] : make_float2(0.f, 0.f);
-            const float piv = c[k].x;
+            const float piv = pl[k].x;
             const bool good = (piv > 0.f) && (piv < INFINITY);
             ok = ok && good;
-            const float ip = good ? __frcp_rn(piv) : 0.f;
+            const float ip = good ? (DBP_PF_RCPRN ? __frcp_rn(piv) : rcp_approx(piv)) : 0.f;
+            float2 f[R];
+            bool me[R];
 #pragma unroll
             for (int m = 0; m < R; ++m) {
-                const bool me = row[m] == k;
-                const float2 f = me ? make_float2(1.f - ip, 0.f) : c_scale(cr[m], ip);
-#pragma unroll
-                for (int t = 0; t < (m + 1) * L; ++t) {
-                    float2& x = A[pf_off(m, L) + t];
-                    if (t == k) {
-                        x = me ? make_float2(-ip, 0.f) : c_scale(x, ip);
-                    } else {        // x -= f conj(c_t)
-                        x.x = fmaf(-f.x, c[t].x, fmaf(-f.y, c[t].y, x.x));
-                        x.y = fmaf(-f.y, c[t].x, fmaf(f.x, c[t].y, x.y));
-                    }
-                }
+                me[m] = row[m] == k;
+                f[m] = me[m] ? make_float2(1.f - ip, 0.f) : c_scale(cr[m], ip);
                 if (MODE == 1) {    // border: E -= f E_k
-                    E[m].x = fmaf(-f.x, Ek.x, fmaf(f.y, Ek.y, E[m].x));
-                    E[m].y = fmaf(-f.x, Ek.y, fmaf(-f.y, Ek.x, E[m].y));
+                    E[m].x = fmaf(-f[m].x, Ek.x, fmaf(f[m].y, Ek.y, E[m].x));
+                    E[m].y = fmaf(-f[m].x, Ek.y, fmaf(-f[m].y, Ek.x, E[m].y));
+                }
+            }
+            // t-outer so each broadcast c_t (two per LDS.128) is live only across its R slots
+#pragma unroll
+            for (int t2 = 0; t2 < UP; t2 += 2) {
+                const float4 cc = *reinterpret_cast<const float4*>(pl + t2);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int t = t2 + h;
+                    const float2 ct = h ? make_float2(cc.z, cc.w) : make_float2(cc.x, cc.y);
+#pragma unroll
+                    for (int m = 0; m < R; ++m) {
+                        if (t >= (m + 1) * L) continue;
+                        float2& x = A[pf_off(m, L) + t];
+                        if (t == k) {
+                            x = me[m] ? make_float2(-ip, 0.f) : c_scale(x, ip);
+                        } else {    // x -= f conj(c_t)
+                            x.x = fmaf(-f[m].x, ct.x, fmaf(-f[m].y, ct.y, x.x));
+                            x.y = fmaf(-f[m].y, ct.x, fmaf(f[m].x, ct.y, x.y));
+                        }
+                    }
                 }
             }
         }
@@ -308,7 +346,7 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
                 float2* Gr = G + (row[m] * (row[m] + 1)) / 2;
 #pragma unroll
                 for (int t = 0; t < (m + 1) * L; ++t)
-                    if (t <= row[m]) Gr[t] = c_scale(A[pf_off(m, L) + t], -dr[m] * dv[t]);
+                    if (t <= row[m]) Gr[t] = c_scale(A[pf_off(m, L) + t], -dr[m] * dline[t]);
                 if (MODE == 1) a.vout[(size_t)p * UP + row[m]] = c_scale(E[m], dr[m]);
             }
         }
@@ -326,7 +364,7 @@ static bool launch_pf_t(const LaunchCtx& L, const float2* H, const float2* y, Pf
         if (!make_map3(&tmH, H, a.U, a.S, a.npairs, UP + 2, P::SC, P::PW)) return false;
         if (Q::MF && !make_map3(&tmY, y, a.S, 1, a.npairs, P::SC, 1, P::PW)) return false;
     } else {
-        if (!make_map3(&tmH, H, a.S, a.U, a.npairs, P::SC + 2, UP + 1, P::PW)) return false;
+        if (!make_map3(&tmH, H, a.S, a.U, a.npairs, P::SC, UP + 1, P::PW)) return false;
     }
     if (!g_sms_pf) {
         int dev = 0;
@@ -362,7 +400,7 @@ size_t prefold_smem(int UP, bool dl, int mode) {
 // uses the lane-row kernel (dbp_prelr.cu).
 bool launch_prefold(const LaunchCtx& L, int UP, int mode, const float2* H, const float2* y, int S, int U, int J,
                     long npairs, float delta, float2* Gout, float2* vout) {
-    if (UP > 16 || (mode != 2 && J != 1) || npairs <= 0) return false;
+    if (UP > 16 || (mode != 2 && J != 1) || npairs <= 0 || npairs > (1L << 30)) return false;
     PfArgs a{S, U, npairs, delta, Gout, vout, L.flag};
     switch (UP) {
 #define DBP_PF_CASE(UPc)                                                  \

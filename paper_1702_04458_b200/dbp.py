@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdbp.so")
+LIB_PATH = os.environ.get("DBP_LIB") or os.path.join(_HERE, "libdbp.so")   # DBP_LIB: tuning variants
 
 STATUS = {0: "DBP_OK", 1: "DBP_ERR_INVALID_ARG", 2: "DBP_ERR_UNSUPPORTED", 3: "DBP_ERR_NOT_HPD",
           4: "DBP_ERR_CUDA", 5: "DBP_ERR_NCCL", 6: "DBP_ERR_WORKSPACE"}
