@@ -168,27 +168,38 @@ def run_reference(args, rank: int, world: int):
 
 
 # ------------------------------------------------------------------ roofline model
-def algorithmic_bytes(kernel: str, C_loc: int) -> float:
-    """Algorithmic HBM bytes per launch (DESIGN.md section 5 table)."""
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # SMs x FP32 lanes x 2 flop/FMA x max SM clock
+
+
+def algorithmic(kernel: str, C_loc: int):
+    """(bound, amount) per launch of a libdbp kernel (DESIGN.md section 5 table).
+
+    HBM-bound kernels: algorithmic bytes (each operand read once, each result
+    written once).  FP32-bound preprocessing: algorithmic flops, 8 per complex
+    MAC, counting the Hermitian Gram (S*tri(U) MACs), the matched filter
+    (S*U*J), the Hermitian inverse (U*tri(U): one rank-1 update of the lower
+    triangle per pivot) and y^reg (U*U*J).
+    """
     S, U, N, J = UL.S, UL.U, UL.N, UL.N_sym
     tri = U * (U + 1) // 2
     P = C_loc * N
     c8 = 8
+    gram, mf, inv, yreg = S * tri, S * U * J, U * tri, U * U * J
+    flops = {
+        "pre_cg": P * (gram + mf) * 8,
+        "pre_ul": P * (gram + mf + inv + yreg) * 8,
+        "pre_dl": P * (gram + inv) * 8,
+    }
+    if kernel in flops:
+        return "alu", float(flops[kernel])
     table = {
-        # k_gram: read H_c (+ y_c), write packed Gram (+ matched filter)
-        "gram_ul": P * (S * U + J * S + tri + J * U) * c8,
-        "gram_cg": P * (S * U + J * S + tri + J * U) * c8,
-        "gram_dl": P * (S * U + tri) * c8,
-        # k_inv: read packed G (+ mf), write packed G^{-1} (+ yreg)
-        "inv_ul": P * (2 * tri + 2 * J * U) * c8,
-        "inv_dl": P * (2 * tri) * c8,
-        # fused iterations: read G^{-1} rows (+ yreg / s, H_c for the DL output), write outputs
+        # fused iterations: read G^{-1} (+ y^reg / s, H_c for the DL output), write outputs
         "admm_fused": P * (tri + J * U) * c8 + N * J * U * (c8 + 1),
         "bf_fused": P * (tri + S * U + J * S) * c8 + N * J * U * c8,
         "cg_gsum": P * (tri + J * U) * c8 + N * (tri + J * U) * c8,
         "cg_fused": N * (tri + J * U) * c8 + N * J * U * (c8 + 1),
     }
-    return float(table.get(kernel, 0.0))
+    return "hbm", float(table.get(kernel, 0.0))
 
 
 def load_traffic() -> dict:
@@ -347,11 +358,17 @@ def main():
     roof = None
     if dom:
         avg_s = ktimes[dom][1] / ktimes[dom][0] * 1e-3
-        ab = algorithmic_bytes(dom, C_loc)
+        bound, amt = algorithmic(dom, C_loc)
         traffic = load_traffic().get(dom)
-        roof = {"kernel": dom, "bound": "hbm", "achieved": ab / avg_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                "frac": ab / avg_s / 1e9 / hbm_peak, "traffic": traffic, "algorithmic_bytes": ab,
-                "avg_launch_us": avg_s * 1e6, "peak_source": peak_src}
+        if bound == "hbm":
+            roof = {"kernel": dom, "bound": "hbm", "achieved": amt / avg_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": amt / avg_s / 1e9 / hbm_peak, "traffic": traffic, "algorithmic_bytes": amt,
+                    "avg_launch_us": avg_s * 1e6, "peak_source": peak_src}
+        else:
+            roof = {"kernel": dom, "bound": "alu", "achieved": amt / avg_s / 1e12, "peak": FP32_PEAK_TFLOPS,
+                    "unit": "TFLOP/s", "frac": amt / avg_s / 1e12 / FP32_PEAK_TFLOPS, "traffic": traffic,
+                    "algorithmic_flops": amt, "avg_launch_us": avg_s * 1e6,
+                    "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md)"}
 
     # end to end through the C ABI with pinned host buffers
     e2e = None
