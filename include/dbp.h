@@ -93,7 +93,12 @@ typedef enum {
     DBP_OPT_FORCE_SPLIT = 1,
     /* 1: bracket every libdbp kernel launch with CUDA events on its stream and
      * accumulate per-kernel device time (read with dbp_get_kernel_times). */
-    DBP_OPT_KERNEL_TIMING = 2
+    DBP_OPT_KERNEL_TIMING = 2,
+    /* 0 (default): at world == 1, when UP <= 16, N_sym == 1, C <= 128/UP*4 and
+     * U, S are even, each solver is ONE per-subcarrier kernel (local Gram,
+     * inverse, every consensus round and the output on chip); 1: use the
+     * preprocessing + iteration kernels instead (same results up to rounding). */
+    DBP_OPT_NO_FUSED = 3
 } dbp_option;
 
 /* Per-kernel device time accumulated under DBP_OPT_KERNEL_TIMING. */

@@ -25,6 +25,7 @@ struct dbp_ctx {
     int64_t launches = 0;
     int64_t allreduce_calls = 0, allreduce_bytes = 0, consensus_rounds = 0;
     int force_split = 0;
+    int no_fused = 0;
     void* stage = nullptr;       // host-I/O staging (device)
     size_t stage_bytes = 0;
     void* iws = nullptr;         // internal workspace when ws == NULL
@@ -146,6 +147,7 @@ extern "C" dbp_status dbp_set_option(dbp_ctx* c, int option, int64_t value) {
     if (!c) return fail(DBP_ERR_INVALID_ARG, "ctx is NULL");
     if (option == DBP_OPT_FORCE_SPLIT) { c->force_split = value ? 1 : 0; return DBP_OK; }
     if (option == DBP_OPT_KERNEL_TIMING) { c->timing = value ? 1 : 0; return DBP_OK; }
+    if (option == DBP_OPT_NO_FUSED) { c->no_fused = value ? 1 : 0; return DBP_OK; }
     return fail(DBP_ERR_INVALID_ARG, "unknown option %d", option);
 }
 
@@ -391,6 +393,18 @@ extern "C" dbp_status dbp_detect_admm(dbp_ctx* c, const dbp_dims* d, const dbp_c
     float2* mf = reinterpret_cast<float2*>(k.ws + Lw.off[1]);
     LaunchCtx L{s, c->d_flag, &c->launches};
 
+    if (c->world == 1 && !c->force_split && !c->no_fused && fused_ok(sh.UP, sh.C, sh.N, sh.J, sh.S, sh.U)) {
+        // a1-a8 in one per-subcarrier kernel (world == 1, supported shape)
+        bool launched = false;
+        KT("fused_ul", (launched = launch_fused_ul(L, sh.UP, false, dH, dy, sh.C, sh.N, sh.S, sh.U, T, rho, gamma,
+                                                   N0, Es, make_prox(reg, mod, sh.C, rho, N0, Es), modem_of(mod),
+                                                   static_cast<float2*>(k.io[2].dev),
+                                                   static_cast<uint8_t*>(k.io[3].dev)), cudaGetLastError()));
+        if (launched) {
+            c->consensus_rounds += T;
+            return end_call(c, k, s);
+        }
+    }
     float2* yreg = reinterpret_cast<float2*>(k.ws + Lw.off[2]);
     // a1-a3: G_c = H_c^H H_c + rho I, B_c^{-1} and y^reg = B_c^{-1} H_c^H y_c (Alg. 1 lines 7-8)
     KT("pre_ul", launch_prelr(L, sh.UP, 1, dH, dy, sh.S, sh.U, sh.J, sh.pairs(), rho, G, yreg));
@@ -465,6 +479,18 @@ extern "C" dbp_status dbp_detect_cg(dbp_ctx* c, const dbp_dims* d, const dbp_cf3
     a.N = sh.N; a.J = sh.J; a.U = sh.U; a.T = T; a.rho = rho;
     a.md = modem_of(mod);
 
+    if (c->world == 1 && !c->force_split && !c->no_fused && fused_ok(sh.UP, sh.C, sh.N, sh.J, sh.S, sh.U)) {
+        // b1-b5 in one per-subcarrier kernel (world == 1, supported shape)
+        bool launched = false;
+        KT("fused_cg", (launched = launch_fused_ul(L, sh.UP, true, static_cast<const float2*>(k.io[0].dev),
+                                                   static_cast<const float2*>(k.io[1].dev), sh.C, sh.N, sh.S, sh.U,
+                                                   T, rho, 1.f, 0.f, 1.f, Prox{}, modem_of(mod), a.x_hat, a.hard),
+                        cudaGetLastError()));
+        if (launched) {
+            c->consensus_rounds += T + 1;
+            return end_call(c, k, s);
+        }
+    }
     // b1: per-pair Gram H_c^H H_c and matched filter H_c^H y_c, then the
     // per-GPU sums (G_loc, local y^MRC) in fixed cluster order.
     KT("pre_cg", launch_prelr(L, sh.UP, 0, static_cast<const float2*>(k.io[0].dev),
@@ -525,6 +551,16 @@ extern "C" dbp_status dbp_beamform_admm(dbp_ctx* c, const dbp_dims* d, const dbp
     a.a0 = (float)std::max((double)sh.U / ((double)sh.C * sh.S), 1.0 / sh.C);   // Alg. 3 line 8 (P507)
     a.inv_c = (float)(1.0 / sh.C);
 
+    if (c->world == 1 && !c->force_split && !c->no_fused && fused_ok(sh.UP, sh.C, sh.N, sh.J, sh.S, sh.U)) {
+        // c1-c4 in one per-subcarrier kernel (world == 1, supported shape)
+        bool launched = false;
+        KT("fused_dl", (launched = launch_fused_dl(L, sh.UP, a.Hd, a.s, sh.C, sh.N, sh.S, sh.U, T, rho, gamma,
+                                                   a.a0, a.x), cudaGetLastError()));
+        if (launched) {
+            c->consensus_rounds += T - 1;
+            return end_call(c, k, s);
+        }
+    }
     // c1: B_c = H_c H_c^H + rho^{-1} I_U and its inverse (Alg. 3 lines 5-6)
     KT("pre_dl", launch_prelr(L, sh.UP, 2, a.Hd, nullptr, sh.S, sh.U, sh.J, sh.pairs(), a.rho_inv, G, nullptr));
     int NT, CCH;

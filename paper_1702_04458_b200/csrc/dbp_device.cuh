@@ -88,6 +88,13 @@ __device__ __forceinline__ void tma_load3(void* dst, const void* map, int c0, in
         ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ void tma_load4(void* dst, const void* map, int c0, int c1, int c2, int c3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+        ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+          "r"(smem_u32(bar))
+        : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // ------------------------------------------------------------ constellation
@@ -242,6 +249,34 @@ __device__ __forceinline__ float2 herm_mv_row(const float2* G, const float2* v, 
     for (int j = 0; j <= r; ++j) c_fma(acc, G[pidx(r, j)], v[j]);
     for (int j = r + 1; j < UP; ++j) c_fmac(acc, G[pidx(j, r)], v[j]);
     return acc;
+}
+
+// ---------------------------------------------------------------- CG (Alg. 2)
+// sum over the UP-lane group (xor butterfly, the paper's shuffle allreduce P715)
+template <int UP>
+__device__ __forceinline__ float group_sum(float v) {
+#pragma unroll
+    for (int o = UP / 2; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// One replicated CG update (Alg. 2 lines 13-18) for lane u given w = sum_c w_c.
+template <int UP>
+__device__ __forceinline__ void cg_update(float2& x, float2& r, float2& p, float& rr, float2 w, float rho) {
+    float2 e = c_add(c_scale(p, rho), w);                                   // line 13
+    float phe = group_sum<UP>(fmaf(p.x, e.x, p.y * e.y));                   // Re(p^H e)
+    const bool live = rr > 0.f;                                             // reading 4
+    float alpha = live ? rr / phe : 0.f;                                    // line 14
+    float2 xn = c_add(x, c_scale(p, alpha));                                // line 15
+    float2 rn = c_sub(r, c_scale(e, alpha));                                // line 16 (e^(t))
+    float rr1 = group_sum<UP>(c_norm2(rn));
+    float beta = live ? rr1 / rr : 0.f;                                     // line 17
+    if (live) {
+        x = xn;
+        r = rn;
+        p = c_add(rn, c_scale(p, beta));                                    // line 18
+        rr = rr1;
+    }
 }
 
 }  // namespace dbp

@@ -1,0 +1,312 @@
+// dbp_fold.cuh -- the "folded rows" per-pair layout shared by the
+// preprocessing kernel k_prefold (dbp_prefold.cu) and the fused
+// per-subcarrier solvers (dbp_fused.cu).  See dbp_prefold.cu for the design
+// (DESIGN.md section 5.1).
+//
+// L = UP/4 lanes own one (cluster, subcarrier) pair; lane l holds R = 4 rows
+// of the pair's Hermitian U x U matrix, r_m = l, 2L-1-l, 2L+l, 4L-1-l, and
+// for row r_m the compile-time columns t < (m+1)L ("slots"; slot (m, t) is
+// valid iff t <= r_m, the others are junk and never read).  A warp holds
+// PW = 32/L pairs.
+#pragma once
+
+#include "dbp_device.cuh"
+#include "dbp_lanerow.cuh"
+
+// tuning knobs (build.py -D...): TMA ring depth, UL antenna-loop unroll,
+// IEEE vs approximate pivot reciprocal, branch vs select pivot publication
+#ifndef DBP_PF_NST
+#define DBP_PF_NST 3
+#endif
+#ifndef DBP_PF_UNROLL
+#define DBP_PF_UNROLL 2
+#endif
+#ifndef DBP_PF_RCPRN
+#define DBP_PF_RCPRN 1
+#endif
+
+namespace dbp {
+
+constexpr int PF_UNROLL = DBP_PF_UNROLL;
+
+template <int UP>
+struct Fold {
+    static constexpr int R = 4;
+    static constexpr int L = UP / R;                 // lanes per pair: 1, 2, 4
+    static constexpr int PW = 32 / L;                // pairs per warp: 32, 16, 8
+    static constexpr int SC = 4;                     // antennas per TMA stage
+    static constexpr int NST = DBP_PF_NST;           // per-warp ring depth
+    static constexpr int NSLOT = 10 * L;             // L * R(R+1)/2
+    static constexpr int TRI = UP * (UP + 1) / 2;
+    __host__ __device__ static constexpr int off(int m) { return L * m * (m + 1) / 2; }
+    __device__ static __forceinline__ int row(int m, int l) { return (m & 1) ? (m + 1) * L - 1 - l : m * L + l; }
+};
+
+// One warp's TMA box: UL {UP+2 users (2 out-of-bounds, zero-filled), SC
+// antennas, PW pairs} + y {SC, PW}; DL {SC antennas, UP+1 users, PW pairs}.
+template <int UP, bool DL, bool MF>
+struct FoldStage {
+    using F = Fold<UP>;
+    static constexpr int HL = DL ? F::SC : UP + 2;              // smem line (float2)
+    static constexpr int NL = DL ? UP + 1 : F::SC;              // lines per pair
+    static constexpr int HSZ = F::PW * NL * HL;                 // float2
+    static constexpr int YSZ = MF ? F::PW * F::SC : 0;
+    static constexpr int BYTES = (HSZ + YSZ) * 8;               // complete_tx bytes
+    static constexpr int STG = (BYTES + 127) / 128 * 128;       // stage pitch
+};
+
+// ---------------------------------------------------------------- Gram
+// UL: G_rt += conj(h_sr) h_st (and b_r += conj(h_sr) y_s) over one stage.
+// Pair q reads antenna (s + q/2) mod 4: the 8 pairs' LDS.128 hit distinct bank groups.
+template <int UP, bool MF>
+__device__ __forceinline__ void fold_gram_ul(float2 (&A)[Fold<UP>::NSLOT], float2 (&E)[4], const float2* stage, int q,
+                                             const int (&row)[4]) {
+    using F = Fold<UP>;
+    using G = FoldStage<UP, false, MF>;
+    const float2* hq = stage + q * G::NL * G::HL;
+    const float2* yq = stage + G::HSZ + q * F::SC;
+#pragma unroll PF_UNROLL
+    for (int s = 0; s < F::SC; ++s) {
+        const int sr = (s + (q >> 1)) & (F::SC - 1);
+        const float2* hrow = hq + sr * G::HL;
+        float2 h[UP];
+        read_vec<UP>(hrow, h);
+        float2 o[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) o[m] = hrow[row[m]];
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int t = 0; t < (m + 1) * F::L; ++t) c_fmac(A[F::off(m) + t], o[m], h[t]);
+        if (MF) {
+            const float2 yv = yq[sr];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) c_fmac(E[m], o[m], yv);
+        }
+    }
+}
+
+// DL: B_rt += H_rs conj(H_ts); pair q reads antenna pair (s/2 + q/4) mod 2.
+template <int UP>
+__device__ __forceinline__ void fold_gram_dl(float2 (&A)[Fold<UP>::NSLOT], const float2* stage, int q, const int (&row)[4]) {
+    using F = Fold<UP>;
+    using G = FoldStage<UP, true, false>;
+    const float2* hq = stage + q * G::NL * G::HL;
+#pragma unroll 1
+    for (int s0 = 0; s0 < F::SC; s0 += 2) {
+        const int s = (s0 + 2 * (q >> 2)) & (F::SC - 1);
+        float4 o[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) o[m] = *reinterpret_cast<const float4*>(hq + row[m] * G::HL + s);
+#pragma unroll
+        for (int t = 0; t < UP; ++t) {
+            const float4 v = *reinterpret_cast<const float4*>(hq + t * G::HL + s);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                if (t < (m + 1) * F::L) {
+                    c_fmacb(A[F::off(m) + t], make_float2(o[m].x, o[m].y), make_float2(v.x, v.y));
+                    c_fmacb(A[F::off(m) + t], make_float2(o[m].z, o[m].w), make_float2(v.z, v.w));
+                }
+            }
+        }
+    }
+}
+
+// Real diagonal + delta; dg[m] = diagonal of row r_m.  (Bit-mask predicates:
+// a "t == row" compare chain gets folded into a dynamically indexed
+// local-memory access by the compiler.)
+template <int UP>
+__device__ __forceinline__ void fold_diag(float2 (&A)[Fold<UP>::NSLOT], const int (&row)[4], float delta, float (&dg)[4]) {
+    using F = Fold<UP>;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        dg[m] = 0.f;
+        const unsigned dmask = 1u << row[m];
+#pragma unroll
+        for (int t = 0; t < (m + 1) * F::L; ++t) {
+            const bool d = (dmask >> t) & 1u;
+            float2& x = A[F::off(m) + t];
+            x.x = d ? x.x + delta : x.x;
+            x.y = d ? 0.f : x.y;
+            dg[m] += d ? x.x : 0.f;
+        }
+    }
+}
+
+// Jacobi scaling to unit diagonal: A_rt *= d_r d_t, E_r *= d_r (d = dg^-1/2,
+// published to the pair's dline for the column factors).
+template <int UP, bool BORDER>
+__device__ __forceinline__ void fold_jacobi(float2 (&A)[Fold<UP>::NSLOT], float2 (&E)[4], const float (&dg)[4],
+                                            float (&dr)[4], float* dline, const int (&row)[4]) {
+    using F = Fold<UP>;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) dr[m] = dg[m] > 0.f ? rsqrtf(dg[m]) : 1.f;
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < 4; ++m) dline[row[m]] = dr[m];
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+#pragma unroll
+        for (int t = 0; t < (m + 1) * F::L; ++t) A[F::off(m) + t] = c_scale(A[F::off(m) + t], dr[m] * dline[t]);
+        if (BORDER) E[m] = c_scale(E[m], dr[m]);
+    }
+}
+
+// Hermitian sweep over pivots k = 0..UP-1 (Goodnight form): afterwards the
+// valid slots hold -M^{-1} of the (scaled) matrix and, with BORDER, E holds
+// M^{-1} E.  pl: the pair's UP+2 line (pivot column, E_k).  Returns false if
+// a pivot was not positive and finite (not HPD).
+template <int UP, bool BORDER>
+__device__ __forceinline__ bool fold_sweep(float2 (&A)[Fold<UP>::NSLOT], float2 (&E)[4], float2* pl, const int (&row)[4],
+                                           int l) {
+    using F = Fold<UP>;
+    constexpr int L = F::L;
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < UP; ++k) {
+        const int mk = k / L;
+        const int lk = (mk & 1) ? (mk + 1) * L - 1 - k : k - mk * L;   // owner lane of row k
+        __syncwarp();
+        // publish column k of the current matrix: c_j = a_jk (rows >= k from
+        // every lane's slot k, rows < k as conj of the owner's row k)
+        float2* const dump = pl + UP + 1;
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+            if (k < (m + 1) * L) *(row[m] >= k ? pl + row[m] : dump) = A[F::off(m) + k];
+        if (l == lk) {
+#pragma unroll
+            for (int t = 0; t < k && t < (mk + 1) * L; ++t) pl[t] = c_conj(A[F::off(mk) + t]);
+            if (BORDER) pl[UP] = E[mk];
+        }
+        __syncwarp();
+        float2 cr[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) cr[m] = pl[row[m]];
+        const float2 Ek = BORDER ? pl[UP] : make_float2(0.f, 0.f);
+        const float piv = pl[k].x;
+        const bool good = (piv > 0.f) && (piv < INFINITY);
+        ok = ok && good;
+        const float ip = good ? (DBP_PF_RCPRN ? __frcp_rn(piv) : rcp_approx(piv)) : 0.f;
+        float2 f[4];
+        bool me[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            // pivot row: a_kt / a_kk = a_kt - (1 - 1/a_kk) a_kt (no cancellation: a_kk <= 1)
+            me[m] = row[m] == k;
+            f[m] = me[m] ? make_float2(1.f - ip, 0.f) : c_scale(cr[m], ip);
+            if (BORDER) {    // E -= f E_k
+                E[m].x = fmaf(-f[m].x, Ek.x, fmaf(f[m].y, Ek.y, E[m].x));
+                E[m].y = fmaf(-f[m].x, Ek.y, fmaf(-f[m].y, Ek.x, E[m].y));
+            }
+        }
+        // t-outer: each broadcast c_t (two per LDS.128) is live only across its R slots
+#pragma unroll
+        for (int t2 = 0; t2 < UP; t2 += 2) {
+            const float4 cc = *reinterpret_cast<const float4*>(pl + t2);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int t = t2 + h;
+                const float2 ct = h ? make_float2(cc.z, cc.w) : make_float2(cc.x, cc.y);
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    if (t >= (m + 1) * L) continue;
+                    float2& x = A[F::off(m) + t];
+                    if (t == k) {
+                        x = me[m] ? make_float2(-ip, 0.f) : c_scale(x, ip);
+                    } else {    // x -= f conj(c_t)
+                        x.x = fmaf(-f[m].x, ct.x, fmaf(-f[m].y, ct.y, x.x));
+                        x.y = fmaf(-f[m].y, ct.x, fmaf(f[m].x, ct.y, x.y));
+                    }
+                }
+            }
+        }
+    }
+    return ok;
+}
+
+// After fold_sweep on the Jacobi-scaled matrix: M^{-1}_rt = -d_r d_t A_rt,
+// (M^{-1} b)_r = d_r E_r; `scale` multiplies the inverse (e.g. rho).
+template <int UP, bool BORDER>
+__device__ __forceinline__ void fold_unscale(float2 (&A)[Fold<UP>::NSLOT], float2 (&E)[4], const float (&dr)[4],
+                                             const float* dline, float scale) {
+    using F = Fold<UP>;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+#pragma unroll
+        for (int t = 0; t < (m + 1) * F::L; ++t) A[F::off(m) + t] = c_scale(A[F::off(m) + t], -scale * dr[m] * dline[t]);
+        if (BORDER) E[m] = c_scale(E[m], dr[m]);
+    }
+}
+
+// Packed lower-triangle store of the valid slots.
+template <int UP>
+__device__ __forceinline__ void fold_store(float2* G, const float2 (&A)[Fold<UP>::NSLOT], const int (&row)[4]) {
+    using F = Fold<UP>;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        float2* Gr = G + (row[m] * (row[m] + 1)) / 2;
+#pragma unroll
+        for (int t = 0; t < (m + 1) * F::L; ++t)
+            if (t <= row[m]) Gr[t] = A[F::off(m) + t];
+    }
+}
+
+// Mat-vec form of a Hermitian matrix in folded slots: junk slots zeroed and
+// the diagonal halved, so y = M v is  y_r = sum_slots(r) S_rt v_t  +
+// sum_lanes sum_slots(t, r) conj(S_tr) v_t  with no validity predicates.
+template <int UP>
+__device__ __forceinline__ void fold_mv_prep(float2 (&A)[Fold<UP>::NSLOT], const int (&row)[4]) {
+    using F = Fold<UP>;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        const unsigned vmask = (2u << row[m]) - 1u, dmask = 1u << row[m];
+#pragma unroll
+        for (int t = 0; t < (m + 1) * F::L; ++t) {
+            const bool v = (vmask >> t) & 1u, d = (dmask >> t) & 1u;
+            float2& x = A[F::off(m) + t];
+            const float sc = v ? (d ? 0.5f : 1.f) : 0.f;
+            x = c_scale(x, sc);
+        }
+    }
+}
+
+// y_{r_m} = (M v)_{r_m} for the pair's 4 rows per lane.  vline: the pair's
+// UP-line; ybuf: the pair's L x UP partial-sum block.  Both in shared memory.
+template <int UP>
+__device__ __forceinline__ void fold_mv(const float2 (&A)[Fold<UP>::NSLOT], const float2 (&v)[4], float2 (&y)[4],
+                                        float2* vline, float2* ybuf, const int (&row)[4], int l) {
+    using F = Fold<UP>;
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < 4; ++m) vline[row[m]] = v[m];
+    __syncwarp();
+    float2 col[UP];
+#pragma unroll
+    for (int t = 0; t < UP; ++t) col[t] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int t2 = 0; t2 < (m + 1) * F::L; t2 += 2) {
+            const float4 vv = *reinterpret_cast<const float4*>(vline + t2);
+            c_fma(acc, A[F::off(m) + t2], make_float2(vv.x, vv.y));
+            c_fmac(col[t2], A[F::off(m) + t2], v[m]);
+            if (t2 + 1 < (m + 1) * F::L) {
+                c_fma(acc, A[F::off(m) + t2 + 1], make_float2(vv.z, vv.w));
+                c_fmac(col[t2 + 1], A[F::off(m) + t2 + 1], v[m]);
+            }
+        }
+        y[m] = acc;
+    }
+    float4* yb = reinterpret_cast<float4*>(ybuf + l * UP);
+#pragma unroll
+    for (int t2 = 0; t2 < UP; t2 += 2) yb[t2 / 2] = make_float4(col[t2].x, col[t2].y, col[t2 + 1].x, col[t2 + 1].y);
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int ll = 0; ll < F::L; ++ll) y[m] = c_add(y[m], ybuf[ll * UP + row[m]]);
+}
+
+}  // namespace dbp

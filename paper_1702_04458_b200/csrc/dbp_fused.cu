@@ -1,0 +1,406 @@
+// dbp_fused.cu -- k_fused: one launch per solver on one GPU (world == 1),
+// SURVEY 8(a) rows a1-a8 (Alg. 1), b1-b5 (Alg. 2), c1-c4 (Alg. 3).
+//
+// A CTA owns NPC subcarriers with all C clusters of each (WPS = C/PW warps
+// per subcarrier, NPC * WPS = 4 warps), so the whole per-subcarrier method --
+// local preprocessing, every consensus round, the output -- runs on chip:
+//
+//   SOLVER 1 (ADMM-UL, Alg. 1): Gram + matched filter (folded rows, per-warp
+//     TMA ring, dbp_fold.cuh), Hermitian sweep with the bordered matched
+//     filter -> rho B_c^{-1} and y^reg_c in registers; T consensus rounds:
+//     z_c = y^reg_c + rho B_c^{-1}(s - lambda_c) (folded Hermitian mat-vec),
+//     w = sum_c (z_c + lambda_c) in fixed cluster order through shared
+//     memory (the consensus "allreduce" of P744 over the CTA), prox (E2),
+//     lambda update (E3); s_hat + hard bits.
+//   SOLVER 2 (ADMM-DL, Alg. 3): B_c = H_c H_c^H + rho^{-1} I, sweep -> B_c^{-1};
+//     exact m-form iterations (reading 12); output x_c = H_c^H B_c^{-1} q_c
+//     re-streams H_c through the same ring (second pass, L2-resident: it was
+//     read microseconds earlier by the same CTA).
+//   SOLVER 0 (CG-UL, Alg. 2): Gram + matched filter, the cluster sums
+//     G = sum_c G_c and y^MRC = sum_c H_c^H y_c (P416 footnote; the per-round
+//     allreduce of w_c = G_c p degenerates to this sum at world == 1), then T
+//     CG iterations on UP lanes per subcarrier (shuffle dot products, P715).
+//
+// Versus the split path (k_prefold -> B^{-1} in HBM -> iteration kernels):
+// no per-pair inverse is written or re-read (2 x 42 MB for config C/D), the
+// DL output's second H read hits L2, and each solver is a single launch.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "dbp_device.cuh"
+#include "dbp_fold.cuh"
+#include "dbp_internal.h"
+
+#pragma nv_diag_suppress 128   // SOLVER 0 continues before the inverse: "loop is not reachable"
+
+namespace dbp {
+
+template <int UP, int SOLVER>
+struct FZ {
+    using F = Fold<UP>;
+    static constexpr bool DL = SOLVER == 2;
+    static constexpr bool MF = !DL;
+    using G = FoldStage<UP, DL, MF>;
+    static constexpr int WARPS = 4;
+    static constexpr int NST = 2;
+    static constexpr int PWL = F::PW * (UP + 2);          // pivot / vector lines (float2)
+    static constexpr int DLN = F::PW * UP;                // Jacobi scales (float)
+    static constexpr int YB = F::PW * F::L * UP;          // mat-vec partials (float2)
+    static constexpr int WREG = (NST * G::STG + PWL * 8 + DLN * 4 + YB * 8 + 127) / 128 * 128;
+    // CTA-shared: consensus buffer [WARPS*PW pairs][UP] + [4][UP] sums; CG: packed Gram per pair
+    static constexpr int CBUF = WARPS * F::PW * UP * 8 + WARPS * UP * 8;
+    static constexpr int GBUF = SOLVER == 0 ? WARPS * F::PW * F::TRI * 8 + WARPS * F::TRI * 8 : 0;
+    static constexpr size_t SMEM = 128 + (size_t)WARPS * WREG + CBUF + GBUF;
+};
+
+struct FuArgs {
+    int S, U, N, C, T, WPS, NPC;
+    float rho, gamma, delta;
+    // UL outputs (SOLVER 0, 1)
+    float2* s_hat;        // [N][U]
+    uint8_t* hard;        // [N][U] or null
+    Prox px;
+    Modem md;
+    // DL (SOLVER 2)
+    const float2* s;      // [N][U]
+    float2* x;            // [C][N][S]
+    float rho_inv, a0, inv_c;
+    int* flag;
+};
+
+template <int UP, int SOLVER>
+__global__ void __launch_bounds__(128, 3)
+k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmY, FuArgs a) {
+    using Z = FZ<UP, SOLVER>;
+    using F = Fold<UP>;
+    using G = typename Z::G;
+    constexpr int L = F::L, PW = F::PW, SC = F::SC, NST = Z::NST, R = F::R, TRI = F::TRI;
+    constexpr bool DL = Z::DL, MF = Z::MF;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw) + warp * NST;
+    unsigned char* wbase = smem_raw + 128 + (size_t)warp * Z::WREG;
+    const int q = lane / L, l = lane % L;
+    float2* pl = reinterpret_cast<float2*>(wbase + NST * G::STG) + q * (UP + 2);           // pivots / vectors
+    float* dline = reinterpret_cast<float*>(wbase + NST * G::STG + Z::PWL * 8) + q * UP;
+    float2* ybuf = reinterpret_cast<float2*>(wbase + NST * G::STG + Z::PWL * 8 + Z::DLN * 4) + q * L * UP;
+    float2* Wb = reinterpret_cast<float2*>(smem_raw + 128 + (size_t)Z::WARPS * Z::WREG);   // [4*PW][UP]
+    float2* Sv = Wb + Z::WARPS * PW * UP;                                                  // [4][UP]
+    float2* Gb = Sv + Z::WARPS * UP;                                                       // CG: [4*PW][TRI]
+    float2* Gs = Gb + (SOLVER == 0 ? Z::WARPS * PW * TRI : 0);                             // CG: [4][TRI]
+
+    int row[R];
+#pragma unroll
+    for (int m = 0; m < R; ++m) row[m] = F::row(m, l);
+
+    const int WPS = a.WPS, NPC = a.NPC;
+    const int j = warp / WPS;                          // subcarrier slot of this warp
+    const int cb = warp - j * WPS;                     // cluster block
+    const int c = cb * PW + q;                         // this pair's cluster
+    const int pslot = warp * PW + q;                   // pair slot in the CTA (== j*WPS*PW + c)
+    const int ngroups = (a.N + NPC - 1) / NPC;
+    const int nitems = blockIdx.x < ngroups ? (ngroups - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int nch = (a.S + SC - 1) / SC;
+    const int per_item = DL ? 2 * nch : nch;           // DL: Gram pass + output pass
+    const int nseq = nitems * per_item;
+
+    auto issue = [&](int sqn, int st) {
+        const int item = sqn / per_item;
+        int ch = sqn - item * per_item;
+        if (ch >= nch) ch -= nch;
+        const int n = (blockIdx.x + item * gridDim.x) * NPC + j;
+        unsigned char* dst = wbase + st * G::STG;
+        mbar_arrive_expect_tx(&bar[st], (uint32_t)G::BYTES);
+        if (DL) {
+            tma_load4(dst, &tmH, ch * SC, 0, n, cb * PW, &bar[st]);
+        } else {
+            tma_load4(dst, &tmH, 0, ch * SC, n, cb * PW, &bar[st]);
+            tma_load4(dst + G::HSZ * 8, &tmY, ch * SC, 0, n, cb * PW, &bar[st]);
+        }
+    };
+    if (lane == 0) {
+        for (int s = 0; s < NST; ++s) mbar_init(&bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    if (lane == 0)
+        for (int s = 0; s < NST && s < nseq; ++s) issue(s, s);
+
+    int sq = 0, st = 0;
+    uint32_t phase = 0;
+    auto next_stage = [&]() {
+        __syncwarp();
+        if (lane == 0 && sq + NST < nseq) {
+            fence_proxy_async();
+            issue(sq + NST, st);
+        }
+        ++sq;
+        if (++st == NST) { st = 0; phase ^= 1u; }
+    };
+
+    for (int it = 0; it < nitems; ++it) {
+        const int n = (blockIdx.x + it * gridDim.x) * NPC + j;
+        const bool valid = n < a.N && c < a.C;
+
+        // ------------------------------------------------ local Gram (+ matched filter)
+        float2 A[F::NSLOT];
+#pragma unroll
+        for (int e = 0; e < F::NSLOT; ++e) A[e] = make_float2(0.f, 0.f);
+        float2 E[R];
+#pragma unroll
+        for (int m = 0; m < R; ++m) E[m] = make_float2(0.f, 0.f);
+        for (int ch = 0; ch < nch; ++ch) {
+            mbar_wait(&bar[st], phase);
+            const float2* stage = reinterpret_cast<const float2*>(wbase + st * G::STG);
+            if (DL) fold_gram_dl<UP>(A, stage, q, row);
+            else fold_gram_ul<UP, true>(A, E, stage, q, row);
+            next_stage();
+        }
+        float dg[R];
+        fold_diag<UP>(A, row, a.delta, dg);
+
+        if constexpr (SOLVER == 0) {
+            // ---------------------------------------------- CG: cluster sums, then CG per subcarrier
+#pragma unroll
+            for (int m = 0; m < R; ++m) {
+                float2* Gr = Gb + (size_t)pslot * TRI + (row[m] * (row[m] + 1)) / 2;
+#pragma unroll
+                for (int t = 0; t < (m + 1) * L; ++t)
+                    if (t <= row[m]) Gr[t] = valid ? A[F::off(m) + t] : make_float2(0.f, 0.f);
+                Wb[pslot * UP + row[m]] = valid ? E[m] : make_float2(0.f, 0.f);
+            }
+            __syncthreads();
+            const int cpad = WPS * PW;
+            for (int e = tid; e < NPC * (TRI + UP); e += Z::WARPS * 32) {      // fixed cluster order
+                const int jj = e / (TRI + UP), f = e - jj * (TRI + UP);
+                float2 acc = make_float2(0.f, 0.f);
+                if (f < TRI) {
+                    for (int cc = 0; cc < a.C; ++cc) acc = c_add(acc, Gb[(size_t)(jj * cpad + cc) * TRI + f]);
+                    Gs[jj * TRI + f] = acc;
+                } else {
+                    for (int cc = 0; cc < a.C; ++cc) acc = c_add(acc, Wb[(jj * cpad + cc) * UP + f - TRI]);
+                    Sv[jj * UP + f - TRI] = acc;
+                }
+            }
+            __syncthreads();
+            if (warp < NPC) {                           // warp w runs the CG of subcarrier slot w
+                const int nn = (blockIdx.x + it * gridDim.x) * NPC + warp;
+                const int u = lane % UP;
+                const float2* Gj = Gs + warp * TRI;
+                float2* P = pl - q * (UP + 2) + (lane / UP) * (UP + 2);       // a per-group line
+                float2 r = Sv[warp * UP + u];           // line 6: r = y^MRC, p = r, x = 0
+                float2 p = r, x = make_float2(0.f, 0.f);
+                float rr = group_sum<UP>(c_norm2(r));
+                for (int t = 0; t < a.T; ++t) {
+                    __syncwarp();
+                    P[u] = p;
+                    __syncwarp();
+                    const float2 w = herm_mv_row<UP>(Gj, P, u);                 // lines 9-11
+                    cg_update<UP>(x, r, p, rr, w, a.rho);                        // lines 13-18
+                }
+                if (lane < UP && u < a.U && nn < a.N) {
+                    a.s_hat[(size_t)nn * a.U + u] = x;
+                    if (a.hard) a.hard[(size_t)nn * a.U + u] = slice_bits(x, a.md);
+                }
+            }
+            __syncthreads();                            // Gb / Wb / Sv reused by the next item
+            continue;
+        }
+
+        // ------------------------------------------------ B^{-1} (+ y^reg) by the Hermitian sweep
+        float dr[R];
+        fold_jacobi<UP, !DL>(A, E, dg, dr, dline, row);
+        const bool ok = fold_sweep<UP, !DL>(A, E, pl, row, l);
+        if (!ok && valid) atomicOr(a.flag, 1);
+        fold_unscale<UP, !DL>(A, E, dr, dline, DL ? 1.f : a.rho);   // UL: rho B^{-1} (eq. (3))
+        fold_mv_prep<UP>(A, row);
+
+        // consensus over the subcarrier's clusters: Wb[pslot] <- w_c, Sv[j] <- f(sum_c w_c)
+        auto consensus = [&](const float2 (&w)[R], bool do_prox) {
+#pragma unroll
+            for (int m = 0; m < R; ++m) Wb[pslot * UP + row[m]] = valid ? w[m] : make_float2(0.f, 0.f);
+            __syncthreads();
+            if (tid < NPC * UP) {
+                const int jj = tid / UP, u = tid - jj * UP;
+                float2 acc = make_float2(0.f, 0.f);
+                for (int cc = 0; cc < a.C; ++cc) acc = c_add(acc, Wb[(jj * WPS * PW + cc) * UP + u]);
+                Sv[tid] = do_prox ? prox(acc, a.px) : acc;
+            }
+            __syncthreads();
+        };
+
+        if constexpr (SOLVER == 1) {
+            // ---------------------------------------------- ADMM-UL iterations (Alg. 1 lines 10-19)
+            float2 yreg[R], lam[R], z[R], w[R];
+#pragma unroll
+            for (int m = 0; m < R; ++m) {
+                yreg[m] = E[m];
+                lam[m] = make_float2(0.f, 0.f);
+                z[m] = yreg[m];
+                w[m] = yreg[m];
+            }
+            consensus(w, true);
+            for (int t = 2; t <= a.T; ++t) {
+                float2 v[R], bv[R];
+#pragma unroll
+                for (int m = 0; m < R; ++m) {
+                    const float2 s = Sv[j * UP + row[m]];
+                    lam[m] = c_add(lam[m], c_scale(c_sub(z[m], s), a.gamma));    // line 12
+                    v[m] = c_sub(s, lam[m]);
+                }
+                fold_mv<UP>(A, v, bv, pl, ybuf, row, l);                          // rho B^{-1} (s - lambda)
+#pragma unroll
+                for (int m = 0; m < R; ++m) {
+                    z[m] = c_add(yreg[m], bv[m]);                                 // line 15
+                    w[m] = c_add(z[m], lam[m]);                                   // line 17
+                }
+                consensus(w, true);                                               // lines 18-19
+            }
+            if (warp == j * WPS && lane < UP) {
+                const int u = lane;
+                if (u < a.U && n < a.N) {
+                    const float2 s = Sv[j * UP + u];
+                    a.s_hat[(size_t)n * a.U + u] = s;
+                    if (a.hard) a.hard[(size_t)n * a.U + u] = slice_bits(s, a.md);
+                }
+            }
+        } else {
+            // ---------------------------------------------- ADMM-DL iterations (Alg. 3, m-form)
+            float2 sv[R], lam[R], qv[R];
+#pragma unroll
+            for (int m = 0; m < R; ++m) {
+                sv[m] = (row[m] < a.U && n < a.N) ? a.s[(size_t)n * a.U + row[m]] : make_float2(0.f, 0.f);
+                lam[m] = make_float2(0.f, 0.f);
+                qv[m] = c_scale(sv[m], a.a0);                                     // line 8
+            }
+            for (int t = 2; t <= a.T; ++t) {
+                float2 bq[R], mm[R], w[R];
+                fold_mv<UP>(A, qv, bq, pl, ybuf, row, l);
+#pragma unroll
+                for (int m = 0; m < R; ++m) {
+                    mm[m] = c_sub(qv[m], c_scale(bq[m], a.rho_inv));               // line 11
+                    w[m] = c_sub(mm[m], lam[m]);                                   // line 12
+                }
+                consensus(w, false);                                               // line 13
+#pragma unroll
+                for (int m = 0; m < R; ++m) {
+                    const float2 z = c_add(w[m], c_scale(c_sub(sv[m], Sv[j * UP + row[m]]), a.inv_c));   // line 14
+                    lam[m] = c_sub(lam[m], c_scale(c_sub(mm[m], z), a.gamma));                          // line 15
+                    qv[m] = c_add(z, lam[m]);
+                }
+            }
+            float2 rv[R];
+            fold_mv<UP>(A, qv, rv, pl, ybuf, row, l);                             // r = B^{-1} q
+            // publish r for the pair; every lane takes all UP entries
+            __syncwarp();
+#pragma unroll
+            for (int m = 0; m < R; ++m) pl[row[m]] = rv[m];
+            __syncwarp();
+            float2 r[UP];
+            read_vec<UP>(pl, r);
+            // output pass: x_c[s] = sum_u conj(H_us) r_u, lane l takes antennas l, l+L, ... of each stage
+            using GD = FoldStage<UP, true, false>;
+            float2* xo = a.x + ((size_t)c * a.N + n) * a.S;
+            for (int ch = 0; ch < nch; ++ch) {
+                mbar_wait(&bar[st], phase);
+                const float2* hq = reinterpret_cast<const float2*>(wbase + st * G::STG) + q * GD::NL * GD::HL;
+#pragma unroll
+                for (int sl = l; sl < SC; sl += L) {
+                    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int u = 0; u < UP; ++u) c_fmac(acc, hq[u * GD::HL + sl], r[u]);
+                    const int s = ch * SC + sl;
+                    if (valid && s < a.S) xo[s] = acc;
+                }
+                next_stage();
+            }
+        }
+    }
+}
+
+static int g_sms_fz = 0;
+
+template <int UP, int SOLVER>
+static bool launch_fz_t(const LaunchCtx& L, const float2* H, const float2* y, FuArgs a) {
+    using Z = FZ<UP, SOLVER>;
+    using F = Fold<UP>;
+    CUtensorMap tmH{}, tmY{};
+    // H: UL [C][N][S][U] -> dims (U, S, N, C); DL [C][N][U][S] -> dims (S, U, N, C); y [C][N][1][S]
+    if (SOLVER != 2) {
+        if (!make_map4(&tmH, H, a.U, a.S, a.N, a.C, UP + 2, F::SC, 1, F::PW)) return false;
+        if (!make_map4(&tmY, y, a.S, 1, a.N, a.C, F::SC, 1, 1, F::PW)) return false;
+    } else {
+        if (!make_map4(&tmH, H, a.S, a.U, a.N, a.C, F::SC, UP + 1, 1, F::PW)) return false;
+    }
+    if (!g_sms_fz) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_sms_fz, cudaDevAttrMultiProcessorCount, dev);
+    }
+    auto k = k_fused<UP, SOLVER>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z::SMEM) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, Z::WARPS * 32, Z::SMEM);
+    const int ngroups = (a.N + a.NPC - 1) / a.NPC;
+    const int grid = std::min(ngroups, g_sms_fz * std::max(per_sm, 1));
+    k<<<grid, Z::WARPS * 32, Z::SMEM, L.stream>>>(tmH, tmY, a);
+    L.count(1);
+    return true;
+}
+
+// Shape gate of the fused path (the caller falls back to the split kernels).
+bool fused_ok(int UP, int C, int N, int J, int S, int U) {
+    if (UP > 16 || J != 1 || N <= 0 || C <= 0 || N > (1 << 30)) return false;
+    const int PW = 32 / (UP / 4);
+    if (C > 4 * PW) return false;
+    return (U % 2 == 0) && (S % 2 == 0);
+}
+
+static void fz_shape(int UP, int C, FuArgs& a) {
+    const int PW = 32 / (UP / 4);
+    const int need = (C + PW - 1) / PW;
+    a.WPS = need <= 1 ? 1 : need <= 2 ? 2 : 4;
+    a.NPC = 4 / a.WPS;
+}
+
+bool launch_fused_ul(const LaunchCtx& L, int UP, bool cg, const float2* H, const float2* y, int C, int N, int S, int U,
+                     int T, float rho, float gamma, float N0, float Es, Prox px, Modem md, float2* s_hat,
+                     uint8_t* hard) {
+    if (!fused_ok(UP, C, N, 1, S, U)) return false;
+    FuArgs a{};
+    a.S = S; a.U = U; a.N = N; a.C = C; a.T = T;
+    a.rho = rho; a.gamma = gamma; a.delta = cg ? 0.f : rho;
+    a.s_hat = s_hat; a.hard = hard; a.px = px; a.md = md; a.flag = L.flag;
+    (void)N0; (void)Es;
+    fz_shape(UP, C, a);
+    switch (UP) {
+        case 4: return cg ? launch_fz_t<4, 0>(L, H, y, a) : launch_fz_t<4, 1>(L, H, y, a);
+        case 8: return cg ? launch_fz_t<8, 0>(L, H, y, a) : launch_fz_t<8, 1>(L, H, y, a);
+        case 16: return cg ? launch_fz_t<16, 0>(L, H, y, a) : launch_fz_t<16, 1>(L, H, y, a);
+        default: return false;
+    }
+}
+
+bool launch_fused_dl(const LaunchCtx& L, int UP, const float2* Hd, const float2* s, int C, int N, int S, int U, int T,
+                     float rho, float gamma, float a0, float2* x) {
+    if (!fused_ok(UP, C, N, 1, S, U)) return false;
+    FuArgs a{};
+    a.S = S; a.U = U; a.N = N; a.C = C; a.T = T;
+    a.rho = rho; a.gamma = gamma; a.delta = 1.f / rho;
+    a.s = s; a.x = x; a.rho_inv = 1.f / rho; a.a0 = a0; a.inv_c = 1.f / (float)C; a.flag = L.flag;
+    fz_shape(UP, C, a);
+    switch (UP) {
+        case 4: return launch_fz_t<4, 2>(L, Hd, nullptr, a);
+        case 8: return launch_fz_t<8, 2>(L, Hd, nullptr, a);
+        case 16: return launch_fz_t<16, 2>(L, Hd, nullptr, a);
+        default: return false;
+    }
+}
+
+}  // namespace dbp

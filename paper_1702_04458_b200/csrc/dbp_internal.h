@@ -48,7 +48,16 @@ struct CgArgs {
 // the tensor: out-of-bounds elements are zero-filled).  false if unsupported.
 bool make_map3(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1,
                uint32_t b2);
+bool make_map4(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3, uint32_t b0,
+               uint32_t b1, uint32_t b2, uint32_t b3);
 size_t pre_smem(int UP, int S, int U, int J, int mode);
+// single-kernel per-subcarrier solvers (dbp_fused.cu), world == 1
+bool fused_ok(int UP, int C, int N, int J, int S, int U);
+bool launch_fused_ul(const LaunchCtx& L, int UP, bool cg, const float2* H, const float2* y, int C, int N, int S, int U,
+                     int T, float rho, float gamma, float N0, float Es, Prox px, Modem md, float2* s_hat,
+                     uint8_t* hard);
+bool launch_fused_dl(const LaunchCtx& L, int UP, const float2* Hd, const float2* s, int C, int N, int S, int U, int T,
+                     float rho, float gamma, float a0, float2* x);
 size_t prelr_smem(int UP, int S, int U, int J, bool ul);
 bool launch_prefold(const LaunchCtx& L, int UP, int mode, const float2* H, const float2* y, int S, int U, int J,
                     long npairs, float delta, float2* Gout, float2* vout);

@@ -63,33 +63,6 @@ __global__ void k_cg_gsum(const float2* __restrict__ Gp, const float2* __restric
 
 
 
-// sum over the UP-lane group (xor butterfly, the paper's shuffle allreduce P715)
-template <int UP>
-__device__ __forceinline__ float group_sum(float v) {
-#pragma unroll
-    for (int o = UP / 2; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-// One replicated CG update (Alg. 2 lines 13-18) for lane u given w = sum_c w_c.
-template <int UP>
-__device__ __forceinline__ void cg_update(float2& x, float2& r, float2& p, float& rr, float2 w, float rho) {
-    float2 e = c_add(c_scale(p, rho), w);                                   // line 13
-    float phe = group_sum<UP>(fmaf(p.x, e.x, p.y * e.y));                   // Re(p^H e)
-    const bool live = rr > 0.f;                                             // reading 4
-    float alpha = live ? rr / phe : 0.f;                                    // line 14
-    float2 xn = c_add(x, c_scale(p, alpha));                                // line 15
-    float2 rn = c_sub(r, c_scale(e, alpha));                                // line 16 (e^(t))
-    float rr1 = group_sum<UP>(c_norm2(rn));
-    float beta = live ? rr1 / rr : 0.f;                                     // line 17
-    if (live) {
-        x = xn;
-        r = rn;
-        p = c_add(rn, c_scale(p, beta));                                    // line 18
-        rr = rr1;
-    }
-}
-
 // Split CG launch: finish the previous iteration from the allreduced w, then
 // form the local w = G_loc p.  Fused (world == 1): all T iterations.
 template <int UP, bool FUSED>

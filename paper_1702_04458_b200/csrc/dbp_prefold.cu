@@ -42,52 +42,24 @@
 #include <algorithm>
 
 #include "dbp_device.cuh"
+#include "dbp_fold.cuh"
 #include "dbp_internal.h"
-#include "dbp_lanerow.cuh"
 
-// tuning knobs (build.py -D...): TMA ring depth, UL antenna-loop unroll
-#ifndef DBP_PF_NST
-#define DBP_PF_NST 3
-#endif
-#ifndef DBP_PF_UNROLL
-#define DBP_PF_UNROLL 2
-#endif
-#ifndef DBP_PF_RCPRN
-#define DBP_PF_RCPRN 1
-#endif
-#ifndef DBP_PF_PUB_BRANCH
-#define DBP_PF_PUB_BRANCH 1
-#endif
 #pragma nv_diag_suppress 128   // MODE 0 returns before the inverse: "loop is not reachable"
 
 namespace dbp {
 
-constexpr int PF_UNROLL = DBP_PF_UNROLL;
-
 template <int UP>
-struct PF {
-    static constexpr int R = 4;
-    static constexpr int L = UP / R;                 // lanes per pair: 1, 2, 4
-    static constexpr int PW = 32 / L;                // pairs per warp: 32, 16, 8
-    static constexpr int SC = 4;                     // antennas per stage
+struct PF : Fold<UP> {
     static constexpr int WARPS = 4;
-    static constexpr int NST = DBP_PF_NST;
-    static constexpr int NSLOT = 10 * L;             // L * R(R+1)/2
 };
-
-__host__ __device__ constexpr int pf_off(int m, int L) { return L * m * (m + 1) / 2; }
 
 template <int UP, bool DL, int MODE>
 struct PFL {
     using P = PF<UP>;
-    static constexpr bool MF = !DL && MODE != 2;
-    static constexpr int HL = DL ? P::SC : UP + 2;              // smem line (float2)
-    static constexpr int NL = DL ? UP + 1 : P::SC;              // lines per pair
-    static constexpr int HSZ = P::PW * NL * HL;                 // float2
-    static constexpr int YSZ = MF ? P::PW * P::SC : 0;
-    static constexpr int STG = ((HSZ + YSZ) * 8 + 127) / 128 * 128;   // bytes
+    using G = FoldStage<UP, DL, !DL && MODE != 2>;
     static constexpr int PLN = P::PW * (UP + 2);                // pivot lines (float2)
-    static constexpr int WREG = (P::NST * STG + PLN * 8 + P::PW * UP * 4 + 127) / 128 * 128;
+    static constexpr int WREG = (P::NST * G::STG + PLN * 8 + P::PW * UP * 4 + 127) / 128 * 128;
     static constexpr size_t SMEM = 128 + (size_t)P::WARPS * WREG;
 };
 
@@ -105,20 +77,20 @@ __global__ void __launch_bounds__(128, 3)
 k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmY, PfArgs a) {
     using P = PF<UP>;
     using Q = PFL<UP, DL, MODE>;
+    using G = typename Q::G;
     constexpr int L = P::L, PW = P::PW, SC = P::SC, NST = P::NST, R = P::R;
-    constexpr int HL = Q::HL, NL = Q::NL, TRI = tri(UP);
-    constexpr bool MF = Q::MF, INV = MODE != 0;
+    constexpr bool MF = !DL && MODE != 2, INV = MODE != 0;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw) + warp * NST;
     unsigned char* wbase = smem_raw + 128 + (size_t)warp * Q::WREG;
     const int q = lane / L, l = lane % L;
-    float2* pl = reinterpret_cast<float2*>(wbase + NST * Q::STG) + q * (UP + 2);    // pivot column + E_k
-    float* dline = reinterpret_cast<float*>(wbase + NST * Q::STG + Q::PLN * 8) + q * UP;   // Jacobi scales
+    float2* pl = reinterpret_cast<float2*>(wbase + NST * G::STG) + q * (UP + 2);    // pivot column + E_k
+    float* dline = reinterpret_cast<float*>(wbase + NST * G::STG + Q::PLN * 8) + q * UP;   // Jacobi scales
 
     int row[R];
 #pragma unroll
-    for (int m = 0; m < R; ++m) row[m] = (m & 1) ? (m + 1) * L - 1 - l : m * L + l;
+    for (int m = 0; m < R; ++m) row[m] = P::row(m, l);
 
     // (pair counts fit in int: launch_prefold takes npairs <= 2^30)
     const int ngroups = (int)((a.npairs + PW - 1) / PW);
@@ -127,17 +99,17 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
     const int nch = (a.S + SC - 1) / SC;
     const int nseq = nitems * nch;
 
-    // sequence number sq -> (item, chunk, stage); issued NST ahead of consumption
+    // sequence number sq -> (item, chunk) in stage st; issued NST ahead of consumption
     auto issue = [&](int sq, int st) {
         const int item = sq / nch, ch = sq - item * nch;
         const int p0 = (gw + item * W) * PW;
-        unsigned char* dst = wbase + st * Q::STG;
-        mbar_arrive_expect_tx(&bar[st], (uint32_t)((Q::HSZ + Q::YSZ) * 8));
+        unsigned char* dst = wbase + st * G::STG;
+        mbar_arrive_expect_tx(&bar[st], (uint32_t)G::BYTES);
         if (DL) {
             tma_load3(dst, &tmH, ch * SC, 0, p0, &bar[st]);
         } else {
             tma_load3(dst, &tmH, 0, ch * SC, p0, &bar[st]);
-            if (MF) tma_load3(dst + Q::HSZ * 8, &tmY, ch * SC, 0, p0, &bar[st]);
+            if (MF) tma_load3(dst + G::HSZ * 8, &tmY, ch * SC, 0, p0, &bar[st]);
         }
     };
     if (lane == 0) {
@@ -154,7 +126,6 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
         const long p = (long)(gw + it * W) * PW + q;
         const bool valid = p < a.npairs;
 
-        // ------------------------------------------------ Gram slots (+ matched filter)
         float2 A[P::NSLOT];
 #pragma unroll
         for (int e = 0; e < P::NSLOT; ++e) A[e] = make_float2(0.f, 0.f);
@@ -164,50 +135,9 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
 
         for (int ch = 0; ch < nch; ++ch) {
             mbar_wait(&bar[st], phase);
-            const float2* hs = reinterpret_cast<const float2*>(wbase + st * Q::STG);
-            if (!DL) {
-                const float2* hq = hs + q * NL * HL;
-                const float2* yq = hs + Q::HSZ + q * SC;
-#pragma unroll PF_UNROLL
-                for (int s = 0; s < SC; ++s) {
-                    const int sr = (s + (q >> 1)) & (SC - 1);     // pair-rotated antenna: conflict-free LDS.128
-                    const float2* hrow = hq + sr * HL;
-                    float2 h[UP];
-                    read_vec<UP>(hrow, h);
-                    float2 o[R];
-#pragma unroll
-                    for (int m = 0; m < R; ++m) o[m] = hrow[row[m]];
-#pragma unroll
-                    for (int m = 0; m < R; ++m)
-#pragma unroll
-                        for (int t = 0; t < (m + 1) * L; ++t) c_fmac(A[pf_off(m, L) + t], o[m], h[t]);  // conj(h_sr) h_st
-                    if (MF) {
-                        const float2 yv = yq[sr];
-#pragma unroll
-                        for (int m = 0; m < R; ++m) c_fmac(E[m], o[m], yv);
-                    }
-                }
-            } else {
-                const float2* hq = hs + q * NL * HL;
-#pragma unroll 1
-                for (int s0 = 0; s0 < SC; s0 += 2) {
-                    const int s = (s0 + 2 * (q >> 2)) & (SC - 1);       // pair-rotated antenna pair
-                    float4 o[R];
-#pragma unroll
-                    for (int m = 0; m < R; ++m) o[m] = *reinterpret_cast<const float4*>(hq + row[m] * HL + s);
-#pragma unroll
-                    for (int t = 0; t < UP; ++t) {
-                        const float4 v = *reinterpret_cast<const float4*>(hq + t * HL + s);
-#pragma unroll
-                        for (int m = 0; m < R; ++m) {
-                            if (t < (m + 1) * L) {     // B_rt += H_rs conj(H_ts)
-                                c_fmacb(A[pf_off(m, L) + t], make_float2(o[m].x, o[m].y), make_float2(v.x, v.y));
-                                c_fmacb(A[pf_off(m, L) + t], make_float2(o[m].z, o[m].w), make_float2(v.z, v.w));
-                            }
-                        }
-                    }
-                }
-            }
+            const float2* stage = reinterpret_cast<const float2*>(wbase + st * G::STG);
+            if (DL) fold_gram_dl<UP>(A, stage, q, row);
+            else fold_gram_ul<UP, MF>(A, E, stage, q, row);
             __syncwarp();
             if (lane == 0 && sq + NST < nseq) {
                 fence_proxy_async();
@@ -216,138 +146,26 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
             ++sq;
             if (++st == NST) { st = 0; phase ^= 1u; }
         }
-
-        // diagonal: real, + delta
-        // (bit-mask predicates: a "t == row" compare chain gets folded into a
-        // dynamically indexed local-memory access by the compiler)
         float dg[R];
-#pragma unroll
-        for (int m = 0; m < R; ++m) {
-            dg[m] = 0.f;
-            const unsigned dmask = 1u << row[m];
-#pragma unroll
-            for (int t = 0; t < (m + 1) * L; ++t) {
-                const bool d = (dmask >> t) & 1u;
-                float2& x = A[pf_off(m, L) + t];
-                x.x = d ? x.x + a.delta : x.x;
-                x.y = d ? 0.f : x.y;
-                dg[m] += d ? x.x : 0.f;
-            }
-        }
+        fold_diag<UP>(A, row, a.delta, dg);
         if constexpr (!INV) {
             if (valid) {
-                float2* G = a.Gout + (size_t)p * TRI;
+                fold_store<UP>(a.Gout + (size_t)p * P::TRI, A, row);
 #pragma unroll
-                for (int m = 0; m < R; ++m) {
-                    float2* Gr = G + (row[m] * (row[m] + 1)) / 2;
-#pragma unroll
-                    for (int t = 0; t < (m + 1) * L; ++t)
-                        if (t <= row[m]) Gr[t] = A[pf_off(m, L) + t];
-                    a.vout[(size_t)p * UP + row[m]] = E[m];
-                }
+                for (int m = 0; m < R; ++m) a.vout[(size_t)p * UP + row[m]] = E[m];
             }
             continue;
         }
-
-        // ------------------------------------------------ Jacobi scaling to unit diagonal
         float dr[R];
-#pragma unroll
-        for (int m = 0; m < R; ++m) dr[m] = dg[m] > 0.f ? rsqrtf(dg[m]) : 1.f;
-        __syncwarp();
-#pragma unroll
-        for (int m = 0; m < R; ++m) dline[row[m]] = dr[m];
-        __syncwarp();
-#pragma unroll
-        for (int m = 0; m < R; ++m) {
-#pragma unroll
-            for (int t = 0; t < (m + 1) * L; ++t)
-                A[pf_off(m, L) + t] = c_scale(A[pf_off(m, L) + t], dr[m] * dline[t]);
-            E[m] = c_scale(E[m], dr[m]);
-        }
-
-        // ------------------------------------------------ Hermitian sweep, pivots k = 0..UP-1
-        bool ok = true;
-#pragma unroll
-        for (int k = 0; k < UP; ++k) {
-            const int mk = k / L;
-            const int lk = (mk & 1) ? (mk + 1) * L - 1 - k : k - mk * L;   // owner lane of row k
-            __syncwarp();
-            // publish column k of the current matrix: c_j = a_jk.  Stores are
-            // unconditional with the address selected (pl[UP+1] is a dump slot),
-            // so the sweep has no divergent branch and ptxas emits no
-            // divergent-path copy of it around __syncwarp.
-            float2* const dump = pl + UP + 1;
-#pragma unroll
-            for (int m = 0; m < R; ++m)
-                if (k < (m + 1) * L) *(row[m] >= k ? pl + row[m] : dump) = A[pf_off(m, L) + k];
-#if DBP_PF_PUB_BRANCH
-            if (l == lk) {
-#pragma unroll
-                for (int t = 0; t < k && t < (mk + 1) * L; ++t) pl[t] = c_conj(A[pf_off(mk, L) + t]);
-                if (MODE == 1) pl[UP] = E[mk];
-            }
-#else
-            {
-                const bool own = l == lk;
-#pragma unroll
-                for (int t = 0; t < k && t < (mk + 1) * L; ++t) *(own ? pl + t : dump) = c_conj(A[pf_off(mk, L) + t]);
-                if (MODE == 1) *(own ? pl + UP : dump) = E[mk];
-            }
-#endif
-            __syncwarp();
-            float2 cr[R];
-#pragma unroll
-            for (int m = 0; m < R; ++m) cr[m] = pl[row[m]];
-            const float2 Ek = MODE == 1 ? pl[UP] : make_float2(0.f, 0.f);
-            const float piv = pl[k].x;
-            const bool good = (piv > 0.f) && (piv < INFINITY);
-            ok = ok && good;
-            const float ip = good ? (DBP_PF_RCPRN ? __frcp_rn(piv) : rcp_approx(piv)) : 0.f;
-            float2 f[R];
-            bool me[R];
-#pragma unroll
-            for (int m = 0; m < R; ++m) {
-                me[m] = row[m] == k;
-                f[m] = me[m] ? make_float2(1.f - ip, 0.f) : c_scale(cr[m], ip);
-                if (MODE == 1) {    // border: E -= f E_k
-                    E[m].x = fmaf(-f[m].x, Ek.x, fmaf(f[m].y, Ek.y, E[m].x));
-                    E[m].y = fmaf(-f[m].x, Ek.y, fmaf(-f[m].y, Ek.x, E[m].y));
-                }
-            }
-            // t-outer so each broadcast c_t (two per LDS.128) is live only across its R slots
-#pragma unroll
-            for (int t2 = 0; t2 < UP; t2 += 2) {
-                const float4 cc = *reinterpret_cast<const float4*>(pl + t2);
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int t = t2 + h;
-                    const float2 ct = h ? make_float2(cc.z, cc.w) : make_float2(cc.x, cc.y);
-#pragma unroll
-                    for (int m = 0; m < R; ++m) {
-                        if (t >= (m + 1) * L) continue;
-                        float2& x = A[pf_off(m, L) + t];
-                        if (t == k) {
-                            x = me[m] ? make_float2(-ip, 0.f) : c_scale(x, ip);
-                        } else {    // x -= f conj(c_t)
-                            x.x = fmaf(-f[m].x, ct.x, fmaf(-f[m].y, ct.y, x.x));
-                            x.y = fmaf(-f[m].y, ct.x, fmaf(f[m].x, ct.y, x.y));
-                        }
-                    }
-                }
-            }
-        }
+        fold_jacobi<UP, MODE == 1>(A, E, dg, dr, dline, row);
+        const bool ok = fold_sweep<UP, MODE == 1>(A, E, pl, row, l);
         if (!ok && valid) atomicOr(a.flag, 1);
-
-        // ------------------------------------------------ G^{-1} = -D (swept) D, y^reg = D (border)
+        fold_unscale<UP, MODE == 1>(A, E, dr, dline, 1.f);
         if (valid) {
-            float2* G = a.Gout + (size_t)p * TRI;
+            fold_store<UP>(a.Gout + (size_t)p * P::TRI, A, row);
+            if (MODE == 1) {
 #pragma unroll
-            for (int m = 0; m < R; ++m) {
-                float2* Gr = G + (row[m] * (row[m] + 1)) / 2;
-#pragma unroll
-                for (int t = 0; t < (m + 1) * L; ++t)
-                    if (t <= row[m]) Gr[t] = c_scale(A[pf_off(m, L) + t], -dr[m] * dline[t]);
-                if (MODE == 1) a.vout[(size_t)p * UP + row[m]] = c_scale(E[m], dr[m]);
+                for (int m = 0; m < R; ++m) a.vout[(size_t)p * UP + row[m]] = E[m];
             }
         }
     }
@@ -362,7 +180,7 @@ static bool launch_pf_t(const LaunchCtx& L, const float2* H, const float2* y, Pf
     CUtensorMap tmH{}, tmY{};
     if (!DL) {
         if (!make_map3(&tmH, H, a.U, a.S, a.npairs, UP + 2, P::SC, P::PW)) return false;
-        if (Q::MF && !make_map3(&tmY, y, a.S, 1, a.npairs, P::SC, 1, P::PW)) return false;
+        if (MODE != 2 && !make_map3(&tmY, y, a.S, 1, a.npairs, P::SC, 1, P::PW)) return false;
     } else {
         if (!make_map3(&tmH, H, a.S, a.U, a.npairs, P::SC, UP + 1, P::PW)) return false;
     }

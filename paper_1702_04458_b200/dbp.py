@@ -23,6 +23,7 @@ MOD = {"bpsk": 1, "qpsk": 2, "qam16": 4, "qam64": 6}
 ALGO = {"admm_ul": 0, "cg_ul": 1, "admm_dl": 2}
 OPT_FORCE_SPLIT = 1
 OPT_KERNEL_TIMING = 2
+OPT_NO_FUSED = 3
 
 EXPORTS = ["dbp_get_unique_id", "dbp_ctx_create", "dbp_ctx_destroy", "dbp_set_option", "dbp_get_stats",
            "dbp_last_error", "dbp_workspace_bytes", "dbp_detect_admm", "dbp_detect_cg",
