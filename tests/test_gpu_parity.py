@@ -53,11 +53,20 @@ def check_hard(hard_gpu, hard_ref, soft_ref, mod):
     return int(len(v))
 
 
+PATHS = ["fused", "twokernel", "split"]   # k_fused / preprocessing + iteration kernels / per-round split path
+
+
+def set_path(env, path):
+    dbp, ctx = env[0], env[1]
+    ctx.set_option(dbp.OPT_FORCE_SPLIT, int(path == "split"))
+    ctx.set_option(dbp.OPT_NO_FUSED, int(path == "twokernel"))
+
+
 def run_admm(env, cfg, split=False, reg="mmse", T=None, host=False):
     dbp, ctx, oracle, torch = env
     T = cfg.T if T is None else T
     H, y, _ = synth.uplink_frame(cfg)
-    ctx.set_option(dbp.OPT_FORCE_SPLIT, int(split))
+    set_path(env, split if isinstance(split, str) else ("split" if split else "fused"))
     if host:
         s, hard = dbp.detect_admm(ctx, H, y, rho=cfg.rho, N0=cfg.N0, reg=reg, mod=cfg.mod, T=T)
     else:
@@ -65,7 +74,7 @@ def run_admm(env, cfg, split=False, reg="mmse", T=None, host=False):
                                   N0=cfg.N0, reg=reg, mod=cfg.mod, T=T)
         ctx.sync()
         s, hard = s.cpu().numpy(), hard.cpu().numpy()
-    ctx.set_option(dbp.OPT_FORCE_SPLIT, 0)
+    set_path(env, "fused")
     s_ref, hard_ref = oracle.detect_admm(H, y, rho=cfg.rho, N0=cfg.N0, reg=reg, mod=cfg.mod, T=T)
     return s, hard, s_ref, hard_ref
 
@@ -80,11 +89,13 @@ SMALL_UL = [
     synth.Config("s<u", "admm_ul", C=4, S=4, U=12, N=6, mod="qpsk", snr_db=15),    # S < U
     synth.Config("nsym", "admm_ul", C=2, S=16, U=8, N=10, N_sym=3, mod="qam64", snr_db=30),
     synth.Config("u20", "admm_ul", C=2, S=24, U=20, N=7, mod="qam16", snr_db=25),
+    synth.Config("c20", "admm_ul", C=20, S=12, U=14, N=13, mod="qam16", snr_db=22),  # partial cluster blocks
+    synth.Config("c5", "admm_ul", C=5, S=8, U=6, N=10, mod="qpsk", snr_db=12),       # 4 subcarriers per CTA
 ]
 
 
 @pytest.mark.parametrize("cfg", SMALL_UL, ids=lambda c: f"{c.name}-C{c.C}S{c.S}U{c.U}N{c.N}J{c.N_sym}")
-@pytest.mark.parametrize("split", [False, True], ids=["fused", "split"])
+@pytest.mark.parametrize("split", PATHS)
 def test_admm_parity(env, cfg, split):
     s, hard, s_ref, hard_ref = run_admm(env, cfg, split)
     assert rel(s, s_ref) < TOL
@@ -95,7 +106,7 @@ def test_admm_parity(env, cfg, split):
 @pytest.mark.parametrize("T", [1, 2, 9])
 def test_admm_regs_and_T(env, reg, T):
     cfg = synth.Config("r", "admm_ul", C=4, S=8, U=8, N=12, mod="qpsk", snr_db=5)
-    for split in (False, True):
+    for split in PATHS:
         s, hard, s_ref, hard_ref = run_admm(env, cfg, split, reg=reg, T=T)
         assert rel(s, s_ref) < TOL
         check_hard(hard, hard_ref, s_ref, cfg.mod)
@@ -121,11 +132,11 @@ def run_cg(env, cfg, split=False, T=None):
     dbp, ctx, oracle, torch = env
     T = cfg.T if T is None else T
     H, y, _ = synth.uplink_frame(cfg)
-    ctx.set_option(dbp.OPT_FORCE_SPLIT, int(split))
+    set_path(env, split if isinstance(split, str) else ("split" if split else "fused"))
     x, hard = dbp.detect_cg(ctx, torch.from_numpy(H).cuda(), torch.from_numpy(y).cuda(), rho=cfg.N0,
                             mod=cfg.mod, T=T)
     ctx.sync()
-    ctx.set_option(dbp.OPT_FORCE_SPLIT, 0)
+    set_path(env, "fused")
     x_ref, hard_ref = oracle.detect_cg(H, y, rho=cfg.N0, mod=cfg.mod, T=T)
     return x.cpu().numpy(), hard.cpu().numpy(), x_ref, hard_ref
 
@@ -137,11 +148,13 @@ SMALL_CG = [
     synth.CONFIGS["A"],
     synth.Config("odd", "cg_ul", C=3, S=7, U=5, N=11, mod="qam16", snr_db=20),
     synth.Config("nsym", "cg_ul", C=2, S=16, U=8, N=10, N_sym=4, mod="qam64", snr_db=30),
+    synth.Config("c20", "cg_ul", C=20, S=12, U=14, N=13, mod="qam16", snr_db=22),
+    synth.Config("c5", "cg_ul", C=5, S=8, U=6, N=10, mod="qpsk", snr_db=12),
 ]
 
 
 @pytest.mark.parametrize("cfg", SMALL_CG, ids=lambda c: f"{c.name}-C{c.C}S{c.S}U{c.U}N{c.N}J{c.N_sym}")
-@pytest.mark.parametrize("split", [False, True], ids=["fused", "split"])
+@pytest.mark.parametrize("split", PATHS)
 def test_cg_parity(env, cfg, split):
     x, hard, x_ref, hard_ref = run_cg(env, cfg, split)
     assert rel(x, x_ref) < TOL
@@ -151,7 +164,7 @@ def test_cg_parity(env, cfg, split):
 @pytest.mark.parametrize("T", [1, 2, 16])
 def test_cg_iteration_counts(env, T):
     cfg = synth.CONFIGS["B"].scaled(N=20)
-    for split in (False, True):
+    for split in PATHS:
         x, _, x_ref, _ = run_cg(env, cfg, split, T=T)
         assert rel(x, x_ref) < TOL
 
@@ -170,10 +183,10 @@ def run_bf(env, cfg, split=False, T=None):
     dbp, ctx, oracle, torch = env
     T = cfg.T if T is None else T
     Hd, s = synth.downlink_frame(cfg)
-    ctx.set_option(dbp.OPT_FORCE_SPLIT, int(split))
+    set_path(env, split if isinstance(split, str) else ("split" if split else "fused"))
     x = dbp.beamform_admm(ctx, torch.from_numpy(Hd).cuda(), torch.from_numpy(s).cuda(), rho=cfg.rho, T=T)
     ctx.sync()
-    ctx.set_option(dbp.OPT_FORCE_SPLIT, 0)
+    set_path(env, "fused")
     x_ref = oracle.beamform_admm(Hd, s, rho=cfg.rho, T=T)
     return x.cpu().numpy(), x_ref
 
@@ -186,11 +199,13 @@ SMALL_DL = [
     synth.Config("odd", "admm_dl", C=3, S=7, U=5, N=11, mod="qam16"),
     synth.Config("s<u", "admm_dl", C=4, S=4, U=12, N=6, mod="qpsk"),
     synth.Config("nsym", "admm_dl", C=2, S=16, U=8, N=10, N_sym=3, mod="qam64"),
+    synth.Config("c20", "admm_dl", C=20, S=12, U=14, N=13, mod="qam16"),
+    synth.Config("c5", "admm_dl", C=5, S=8, U=6, N=10, mod="qpsk"),
 ]
 
 
 @pytest.mark.parametrize("cfg", SMALL_DL, ids=lambda c: f"{c.name}-C{c.C}S{c.S}U{c.U}N{c.N}J{c.N_sym}")
-@pytest.mark.parametrize("split", [False, True], ids=["fused", "split"])
+@pytest.mark.parametrize("split", PATHS)
 def test_bf_parity(env, cfg, split):
     x, x_ref = run_bf(env, cfg, split)
     assert rel(x, x_ref) < TOL
@@ -199,7 +214,7 @@ def test_bf_parity(env, cfg, split):
 @pytest.mark.parametrize("T", [1, 2, 12])
 def test_bf_iteration_counts(env, T):
     cfg = synth.CONFIGS["D"].scaled(N=10, C=8)
-    for split in (False, True):
+    for split in PATHS:
         x, x_ref = run_bf(env, cfg, split, T=T)
         assert rel(x, x_ref) < TOL
 
@@ -211,8 +226,8 @@ def test_consensus_round_counts(env):
     H, y, _ = synth.uplink_frame(cfg)
     Hd, s = synth.downlink_frame(cfg)
     Hg, yg = torch.from_numpy(H).cuda(), torch.from_numpy(y).cuda()
-    for split in (0, 1):
-        ctx.set_option(dbp.OPT_FORCE_SPLIT, split)
+    for path in PATHS:
+        set_path(env, path)
         for T in (1, 4):
             r0 = ctx.stats()["consensus_rounds"]
             dbp.detect_admm(ctx, Hg, yg, N0=cfg.N0, mod=cfg.mod, T=T)
@@ -222,7 +237,7 @@ def test_consensus_round_counts(env):
             dbp.beamform_admm(ctx, torch.from_numpy(Hd).cuda(), torch.from_numpy(s).cuda(), T=T)
             r3 = ctx.stats()["consensus_rounds"]
             assert (r1 - r0, r2 - r1, r3 - r2) == (T, T + 1, T - 1)
-    ctx.set_option(dbp.OPT_FORCE_SPLIT, 0)
+    set_path(env, "fused")
     ctx.sync()
 
 
@@ -273,11 +288,14 @@ def test_invalid_arguments(env):
 
 
 # ------------------------------------------------------- full BASELINE sizes
+@pytest.mark.parametrize("path", ["fused", "twokernel"])
 @pytest.mark.parametrize("name", ["B", "C", "D"])
-def test_full_size_sampled(env, name):
-    """BASELINE configs at full size in the bench launch configuration; the
-    oracle checks 24 sampled subcarriers (each subcarrier is independent)."""
+def test_full_size_sampled(env, name, path):
+    """BASELINE configs at full size in the bench launch configuration (fused)
+    and through the two-kernel path; the oracle checks 24 sampled subcarriers
+    (each subcarrier is independent)."""
     dbp, ctx, oracle, torch = env
+    set_path(env, path)
     cfg = synth.CONFIGS[name]
     rng = np.random.default_rng(7)
     ns = np.sort(rng.choice(cfg.N, 24, replace=False))
@@ -285,6 +303,7 @@ def test_full_size_sampled(env, name):
         Hd, s = synth.downlink_frame(cfg)
         x = dbp.beamform_admm(ctx, torch.from_numpy(Hd).cuda(), torch.from_numpy(s).cuda(), rho=cfg.rho, T=cfg.T)
         ctx.sync()
+        set_path(env, "fused")
         x = x.cpu().numpy()[:, ns]
         x_ref = oracle.beamform_admm(Hd[:, ns], s[ns], rho=cfg.rho, T=cfg.T)
         assert rel(x, x_ref) < TOL
@@ -302,6 +321,7 @@ def test_full_size_sampled(env, name):
         out = out.cpu().numpy()[ns]
         assert rel(out, ref) < TOL, algo
         check_hard(hard.cpu().numpy()[ns], hard_ref, ref, cfg.mod)
+    set_path(env, "fused")
 
 
 def test_config_E_shape_sampled(env):
@@ -322,8 +342,15 @@ def test_config_E_shape_sampled(env):
     check_hard(hard.cpu().numpy()[ns], hard_ref, ref, sub.mod)
 
 
-def test_deterministic(env):
+@pytest.mark.parametrize("path", PATHS)
+def test_deterministic(env, path):
     """Fixed-order sums: two runs are bitwise identical."""
-    a = run_admm(env, synth.CONFIGS["C"].scaled(N=16))[0]
-    b = run_admm(env, synth.CONFIGS["C"].scaled(N=16))[0]
+    a = run_admm(env, synth.CONFIGS["C"].scaled(N=16), path)[0]
+    b = run_admm(env, synth.CONFIGS["C"].scaled(N=16), path)[0]
     assert np.array_equal(a, b)
+    x1 = run_bf(env, synth.CONFIGS["D"].scaled(N=16), path)[0]
+    x2 = run_bf(env, synth.CONFIGS["D"].scaled(N=16), path)[0]
+    assert np.array_equal(x1, x2)
+    c1 = run_cg(env, synth.CONFIGS["C"].scaled(N=16), path)[0]
+    c2 = run_cg(env, synth.CONFIGS["C"].scaled(N=16), path)[0]
+    assert np.array_equal(c1, c2)
