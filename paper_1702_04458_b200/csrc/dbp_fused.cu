@@ -45,14 +45,18 @@ struct FZ {
     static constexpr bool MF = !DL;
     using G = FoldStage<UP, DL, MF>;
     static constexpr int WARPS = 4;
-    static constexpr int NST = 2;
+#ifndef DBP_FZ_NST
+#define DBP_FZ_NST 2
+#endif
+    static constexpr int NST = DBP_FZ_NST;
     static constexpr int PWL = F::PW * (UP + 2);          // pivot / vector lines (float2)
     static constexpr int DLN = F::PW * UP;                // Jacobi scales (float)
     static constexpr int YB = F::PW * F::L * UP;          // mat-vec partials (float2)
     static constexpr int WREG = (NST * G::STG + PWL * 8 + DLN * 4 + YB * 8 + 127) / 128 * 128;
-    // CTA-shared: consensus buffer [WARPS*PW pairs][UP] + [4][UP] sums; CG: packed Gram per pair
-    static constexpr int CBUF = WARPS * F::PW * UP * 8 + WARPS * UP * 8;
-    static constexpr int GBUF = SOLVER == 0 ? WARPS * F::PW * F::TRI * 8 + WARPS * F::TRI * 8 : 0;
+    // CTA-shared: per-warp consensus partials [WARPS][UP] + per-subcarrier sums [4][UP];
+    // CG: per-warp Gram partials [WARPS][TRI] + per-subcarrier Gram [4][TRI]
+    static constexpr int CBUF = WARPS * UP * 8 + WARPS * UP * 8;
+    static constexpr int GBUF = SOLVER == 0 ? 2 * WARPS * F::TRI * 8 : 0;
     static constexpr size_t SMEM = 128 + (size_t)WARPS * WREG + CBUF + GBUF;
 };
 
@@ -87,10 +91,10 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     float2* pl = reinterpret_cast<float2*>(wbase + NST * G::STG) + q * (UP + 2);           // pivots / vectors
     float* dline = reinterpret_cast<float*>(wbase + NST * G::STG + Z::PWL * 8) + q * UP;
     float2* ybuf = reinterpret_cast<float2*>(wbase + NST * G::STG + Z::PWL * 8 + Z::DLN * 4) + q * L * UP;
-    float2* Wb = reinterpret_cast<float2*>(smem_raw + 128 + (size_t)Z::WARPS * Z::WREG);   // [4*PW][UP]
-    float2* Sv = Wb + Z::WARPS * PW * UP;                                                  // [4][UP]
-    float2* Gb = Sv + Z::WARPS * UP;                                                       // CG: [4*PW][TRI]
-    float2* Gs = Gb + (SOLVER == 0 ? Z::WARPS * PW * TRI : 0);                             // CG: [4][TRI]
+    float2* Wp = reinterpret_cast<float2*>(smem_raw + 128 + (size_t)Z::WARPS * Z::WREG);   // [4 warps][UP]
+    float2* Sv = Wp + Z::WARPS * UP;                                                       // [4 subc.][UP]
+    float2* Gp = Sv + Z::WARPS * UP;                                                       // CG: [4 warps][TRI]
+    float2* Gs = Gp + (SOLVER == 0 ? Z::WARPS * TRI : 0);                                  // CG: [4 subc.][TRI]
 
     int row[R];
 #pragma unroll
@@ -100,7 +104,6 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     const int j = warp / WPS;                          // subcarrier slot of this warp
     const int cb = warp - j * WPS;                     // cluster block
     const int c = cb * PW + q;                         // this pair's cluster
-    const int pslot = warp * PW + q;                   // pair slot in the CTA (== j*WPS*PW + c)
     const int ngroups = (a.N + NPC - 1) / NPC;
     const int nitems = blockIdx.x < ngroups ? (ngroups - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const int nch = (a.S + SC - 1) / SC;
@@ -164,24 +167,42 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
 
         if constexpr (SOLVER == 0) {
             // ---------------------------------------------- CG: cluster sums, then CG per subcarrier
+            // sum over the warp's pairs (xor butterfly over the pair bits of the lane), then
+            // over the subcarrier's WPS warps in fixed order: G = sum_c G_c, y^MRC = sum_c H_c^H y_c
+#pragma unroll
+            for (int e = 0; e < F::NSLOT; ++e) {
+                float2 v = valid ? A[e] : make_float2(0.f, 0.f);
+#pragma unroll
+                for (int o = L; o < 32; o <<= 1) {
+                    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+                    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+                }
+                A[e] = v;
+            }
 #pragma unroll
             for (int m = 0; m < R; ++m) {
-                float2* Gr = Gb + (size_t)pslot * TRI + (row[m] * (row[m] + 1)) / 2;
+                float2 v = valid ? E[m] : make_float2(0.f, 0.f);
 #pragma unroll
-                for (int t = 0; t < (m + 1) * L; ++t)
-                    if (t <= row[m]) Gr[t] = valid ? A[F::off(m) + t] : make_float2(0.f, 0.f);
-                Wb[pslot * UP + row[m]] = valid ? E[m] : make_float2(0.f, 0.f);
+                for (int o = L; o < 32; o <<= 1) {
+                    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+                    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+                }
+                E[m] = v;
+            }
+            if (lane < L) {
+                fold_store<UP>(Gp + warp * TRI, A, row);
+#pragma unroll
+                for (int m = 0; m < R; ++m) Wp[warp * UP + row[m]] = E[m];
             }
             __syncthreads();
-            const int cpad = WPS * PW;
-            for (int e = tid; e < NPC * (TRI + UP); e += Z::WARPS * 32) {      // fixed cluster order
+            for (int e = tid; e < NPC * (TRI + UP); e += Z::WARPS * 32) {
                 const int jj = e / (TRI + UP), f = e - jj * (TRI + UP);
                 float2 acc = make_float2(0.f, 0.f);
                 if (f < TRI) {
-                    for (int cc = 0; cc < a.C; ++cc) acc = c_add(acc, Gb[(size_t)(jj * cpad + cc) * TRI + f]);
+                    for (int w2 = 0; w2 < WPS; ++w2) acc = c_add(acc, Gp[(jj * WPS + w2) * TRI + f]);
                     Gs[jj * TRI + f] = acc;
                 } else {
-                    for (int cc = 0; cc < a.C; ++cc) acc = c_add(acc, Wb[(jj * cpad + cc) * UP + f - TRI]);
+                    for (int w2 = 0; w2 < WPS; ++w2) acc = c_add(acc, Wp[(jj * WPS + w2) * UP + f - TRI]);
                     Sv[jj * UP + f - TRI] = acc;
                 }
             }
@@ -206,7 +227,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                     if (a.hard) a.hard[(size_t)nn * a.U + u] = slice_bits(x, a.md);
                 }
             }
-            __syncthreads();                            // Gb / Wb / Sv reused by the next item
+            __syncthreads();                            // Gp / Wp / Sv reused by the next item
             continue;
         }
 
@@ -218,15 +239,28 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
         fold_unscale<UP, !DL>(A, E, dr, dline, DL ? 1.f : a.rho);   // UL: rho B^{-1} (eq. (3))
         fold_mv_prep<UP>(A, row);
 
-        // consensus over the subcarrier's clusters: Wb[pslot] <- w_c, Sv[j] <- f(sum_c w_c)
+        // consensus over the subcarrier's clusters, Sv[j] <- f(sum_c w_c): xor butterfly over the
+        // warp's pairs, then the WPS warp partials in fixed order (deterministic)
         auto consensus = [&](const float2 (&w)[R], bool do_prox) {
+            float2 ps[R];
 #pragma unroll
-            for (int m = 0; m < R; ++m) Wb[pslot * UP + row[m]] = valid ? w[m] : make_float2(0.f, 0.f);
+            for (int m = 0; m < R; ++m) {
+                ps[m] = valid ? w[m] : make_float2(0.f, 0.f);
+#pragma unroll
+                for (int o = L; o < 32; o <<= 1) {
+                    ps[m].x += __shfl_xor_sync(0xffffffffu, ps[m].x, o);
+                    ps[m].y += __shfl_xor_sync(0xffffffffu, ps[m].y, o);
+                }
+            }
+            if (lane < L) {
+#pragma unroll
+                for (int m = 0; m < R; ++m) Wp[warp * UP + row[m]] = ps[m];
+            }
             __syncthreads();
             if (tid < NPC * UP) {
                 const int jj = tid / UP, u = tid - jj * UP;
                 float2 acc = make_float2(0.f, 0.f);
-                for (int cc = 0; cc < a.C; ++cc) acc = c_add(acc, Wb[(jj * WPS * PW + cc) * UP + u]);
+                for (int w2 = 0; w2 < WPS; ++w2) acc = c_add(acc, Wp[(jj * WPS + w2) * UP + u]);
                 Sv[tid] = do_prox ? prox(acc, a.px) : acc;
             }
             __syncthreads();

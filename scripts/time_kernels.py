@@ -13,10 +13,15 @@ ap.add_argument("--solver", default="admm")
 ap.add_argument("--config", default="C")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--split", type=int, default=0)
+ap.add_argument("--T", type=int, default=0)
+ap.add_argument("--nofused", type=int, default=0)
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
+if a.T:
+    cfg = cfg.scaled(T=a.T)
 ctx = dbp.Context(0)
 ctx.set_option(dbp.OPT_FORCE_SPLIT, a.split)
+ctx.set_option(dbp.OPT_NO_FUSED, a.nofused)
 if a.solver == "bf":
     Hd, s = synth.downlink_frame(cfg)
     Hd, s = torch.from_numpy(Hd).cuda(), torch.from_numpy(s).cuda()
@@ -39,4 +44,4 @@ for _ in range(a.reps):
     flush.view(torch.int64).sum()
     run()
 kt = ctx.kernel_times(reset=True)
-print(a.solver, a.config, {k: round(v[1] / v[0] * 1e3, 1) for k, v in kt.items()}, "us")
+print(a.solver, a.config, f"T={cfg.T}", {k: round(v[1] / v[0] * 1e3, 1) for k, v in kt.items()}, "us")
