@@ -185,10 +185,16 @@ def algorithmic(kernel: str, C_loc: int):
     P = C_loc * N
     c8 = 8
     gram, mf, inv, yreg = S * tri, S * U * J, U * tri, U * U * J
+    T = UL.T
+    mv = U * U                                   # one Hermitian mat-vec per pair and round
     flops = {
         "pre_cg": P * (gram + mf) * 8,
         "pre_ul": P * (gram + mf + inv + yreg) * 8,
         "pre_dl": P * (gram + inv) * 8,
+        # single-kernel solvers: local preprocessing + the per-round local updates
+        "fused_cg": (P * (gram + mf) + N * T * mv) * 8,
+        "fused_ul": P * (gram + mf + inv + yreg + (T - 1) * mv) * 8,
+        "fused_dl": P * (gram + inv + T * mv + S * U * J) * 8,
     }
     if kernel in flops:
         return "alu", float(flops[kernel])

@@ -1,9 +1,8 @@
 // dbp_device.cuh -- device building blocks of libdbp (sm_100a).
 //
-// Complex arithmetic on float2, packed-triangular indexing, the TMA bulk-copy
-// (cp.async.bulk + mbarrier) helpers, the per-pair dense linear algebra used
-// by the preprocessing kernels (Gram tiles, Cholesky, triangular inverse,
-// triangular mat-vecs) and the constellation slicer / proximal operators.
+// Complex arithmetic on float2, packed-triangular indexing, the TMA
+// (cp.async.bulk / cp.async.bulk.tensor + mbarrier) helpers, the constellation
+// slicer / proximal operators and the replicated CG update.
 //
 // A "pair" is one (cluster c, subcarrier n) of the paper's per-cluster,
 // per-subcarrier local problem (P149-155, P706).  Inside a CTA a pair is
@@ -144,104 +143,6 @@ __device__ __forceinline__ float2 prox(float2 w, const Prox& p) {
 }
 
 // --------------------------------------------------- per-pair dense algebra
-// Work split of the packed lower triangle of a UP x UP Hermitian Gram matrix
-// into 4x4 tiles: NOFF strictly-lower off-diagonal tiles (a > b) plus NDIAG
-// jobs that each own two diagonal tiles (2e, 2e+1) -- or the single diagonal
-// tile when UP == 4.  Every job costs 64 real FMAs per antenna row (16
-// complex MACs, or 2 x (4 real + 6 complex) MACs), and off-diagonal and
-// diagonal jobs live in different warps, so no warp diverges.
-template <int UP>
-struct Tiles {
-    static constexpr int NB = UP / 4;
-    static constexpr int NOFF = NB * (NB - 1) / 2;
-    static constexpr int NDIAG = NB >= 2 ? NB / 2 : 1;
-};
-
-__device__ __forceinline__ void off_tile_coords(int q, int& a, int& b) {
-    a = 1;
-    while (q >= a) { q -= a; ++a; }
-    b = q;
-}
-
-// Row `s` of the per-pair channel tile in shared memory, 4 users starting at
-// u0.  UL: tile is S x U row-major (element (s,u) at s*U+u).  DL: tile is
-// U x S row-major (H^d, element (u,s) at u*S+s) and the Gram is formed on its
-// transpose.  FULL: U == UP (no padding mask, vector loads in UL).
-template <bool DL, bool FULL>
-__device__ __forceinline__ void load4(const float2* tile, int s, int u0, int U, int S, float2 (&v)[4]) {
-    if (!DL && FULL) {
-        const float4* p = reinterpret_cast<const float4*>(tile + s * U + u0);
-        float4 a = p[0], b = p[1];
-        v[0] = make_float2(a.x, a.y); v[1] = make_float2(a.z, a.w);
-        v[2] = make_float2(b.x, b.y); v[3] = make_float2(b.z, b.w);
-    } else {
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            int u = u0 + r;
-            if (FULL || u < U) v[r] = DL ? tile[u * S + s] : tile[s * U + u];
-            else v[r] = make_float2(0.f, 0.f);
-        }
-    }
-}
-
-// Row ownership for triangular mat-vecs: a row pair {g, UP-1-g} has UP+1
-// terms in both X v and X^H v.  TR threads share a row pair (split terms),
-// each thread owns RPT row pairs.
-template <int UP, int TPP>
-struct RowMap {
-    static constexpr int RP = UP / 2;
-    static constexpr int TR = TPP > RP ? TPP / RP : 1;   // threads per row pair
-    static constexpr int RPT = RP > TPP ? RP / TPP : 1;  // row pairs per thread
-    static constexpr int NR = 2 * RPT;                   // rows owned per thread
-    __device__ static int row(int t, int k) {            // k-th owned row of thread t
-        int g = (t / TR) * RPT + (k >> 1);
-        return (k & 1) ? (UP - 1 - g) : g;
-    }
-    __device__ static int sub(int t) { return t % TR; }
-};
-
-// out_r = sum_{k<=r} X[r][k] v_k for the owned rows (team-local).
-template <int UP, int TPP>
-__device__ __forceinline__ void tri_mv(const float2* X, const float2* v, int t, float2 (&out)[RowMap<UP, TPP>::NR]) {
-    using RM = RowMap<UP, TPP>;
-    const int sb = RM::sub(t);
-#pragma unroll
-    for (int k = 0; k < RM::NR; ++k) {
-        int r = RM::row(t, k);
-        float2 acc = make_float2(0.f, 0.f);
-        for (int j = sb; j <= r; j += RM::TR) c_fma(acc, X[pidx(r, j)], v[j]);
-        if (RM::TR > 1) {
-#pragma unroll
-            for (int o = 1; o < RM::TR; o <<= 1) {
-                acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-                acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
-            }
-        }
-        out[k] = acc;
-    }
-}
-
-// out_r = sum_{k>=r} conj(X[k][r]) v_k for the owned rows (X^H v).
-template <int UP, int TPP>
-__device__ __forceinline__ void tri_mv_h(const float2* X, const float2* v, int t, float2 (&out)[RowMap<UP, TPP>::NR]) {
-    using RM = RowMap<UP, TPP>;
-    const int sb = RM::sub(t);
-#pragma unroll
-    for (int k = 0; k < RM::NR; ++k) {
-        int r = RM::row(t, k);
-        float2 acc = make_float2(0.f, 0.f);
-        for (int j = r + sb; j < UP; j += RM::TR) c_fmac(acc, X[pidx(j, r)], v[j]);
-        if (RM::TR > 1) {
-#pragma unroll
-            for (int o = 1; o < RM::TR; o <<= 1) {
-                acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-                acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
-            }
-        }
-        out[k] = acc;
-    }
-}
-
 // Hermitian mat-vec with a packed lower Hermitian matrix G (row r of G v).
 template <int UP>
 __device__ __forceinline__ float2 herm_mv_row(const float2* G, const float2* v, int r) {

@@ -50,7 +50,6 @@ bool make_map3(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint6
                uint32_t b2);
 bool make_map4(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3, uint32_t b0,
                uint32_t b1, uint32_t b2, uint32_t b3);
-size_t pre_smem(int UP, int S, int U, int J, int mode);
 // single-kernel per-subcarrier solvers (dbp_fused.cu), world == 1
 bool fused_ok(int UP, int C, int N, int J, int S, int U);
 bool launch_fused_ul(const LaunchCtx& L, int UP, bool cg, const float2* H, const float2* y, int C, int N, int S, int U,
@@ -65,8 +64,6 @@ bool launch_prefold(const LaunchCtx& L, int UP, int mode, const float2* H, const
 cudaError_t launch_prelr(const LaunchCtx& L, int UP, int mode, const float2* H, const float2* y, int S, int U, int J,
                          long npairs, float delta, float2* Gout, float2* vout);
 // Gram (+ delta I) per pair -> Gout [pairs][tri(UP)]; matched filter -> mfout [pairs][J][UP] (not for BF)
-cudaError_t launch_gram(const LaunchCtx& L, int UP, int mode, const float2* H, const float2* y, int S, int U,
-                        int J, long npairs, float delta, float2* Gout, float2* mfout);
 
 cudaError_t launch_prox_out(const LaunchCtx& L, int UP, const float2* wbuf, int N, int J, int U, Prox px,
                             Modem md, float2* s_hat, uint8_t* hard);
@@ -111,10 +108,8 @@ size_t iter_smem(int UP, int NT, int C);
 bool iter_cfg(int UP, int C_loc, int N, int max_smem, int* NT);
 size_t split_smem(int UP, int NT, int CCH, int J);
 void split_cfg(int UP, int C_loc, int N, int J, int* NT, int* CCH);
-cudaError_t launch_inv_ul(const LaunchCtx& L, int UP, UlArgs a, long npairs);
 cudaError_t launch_admm_gj(const LaunchCtx& L, int UP, UlArgs a);
 cudaError_t launch_admm_it(const LaunchCtx& L, int UP, UlArgs a, int CCH);
-cudaError_t launch_inv_dl(const LaunchCtx& L, int UP, DlArgs a, long npairs);
 cudaError_t launch_bf_gj(const LaunchCtx& L, int UP, DlArgs a);
 cudaError_t launch_bf_it(const LaunchCtx& L, int UP, DlArgs a, int CCH);
 

@@ -1,25 +1,18 @@
-// dbp_iter.cu -- inverse + consensus iterations of ADMM-UL (Alg. 1) and
-// ADMM-DL (Alg. 3), SURVEY 8(a) rows a2, a4-a8 and c1-c4.
+// dbp_iter.cu -- consensus iterations of ADMM-UL (Alg. 1) and ADMM-DL
+// (Alg. 3) on a per-pair inverse computed by the preprocessing kernel
+// (k_prefold, or k_prelr for UP = 32), SURVEY 8(a) rows a4-a8 and c2-c4.
+// Used by the two-kernel path (world == 1 outside k_fused's shapes, or
+// DBP_OPT_NO_FUSED) and by the split path (world > 1, DBP_OPT_FORCE_SPLIT).
 //
 // Layout: one lane per row of the U x U operator ("lane = user"), UP lanes per
 // (cluster, subcarrier) pair, all lanes of a pair inside one warp.
-//
-//  * Inverse: Gauss-Jordan elimination on the HPD matrix G (no pivoting is
-//    needed for HPD input; a non-positive or non-finite pivot raises the
-//    DBP_ERR_NOT_HPD flag, the same condition as a failed Cholesky pivot,
-//    SPEC S44).  Each step broadcasts the pivot row through a per-pair
-//    shared-memory line (UP/2 LDS.128) and updates all UP entries of every
-//    row: no triangular waste, no shuffles, and the result -- row i of
-//    G^{-1} -- is exactly what the iterations need in lane i's registers.
-//    DESIGN.md section 5 discusses this against the paper's LU/Cholesky
-//    inversion (P704); the algebraic result is the same matrix.
 //  * Iterations: every local update is one row of a Hermitian mat-vec with
 //    the vector broadcast through shared memory; the consensus sum over the
 //    CTA's clusters is taken in fixed cluster order (deterministic).
-//  * Fused kernels (world == 1): inverse + all T iterations + outputs in one
-//    launch, G^{-1} never leaves the register file.  Split kernels (any
-//    world): k_inv writes G^{-1} (packed) once; each iteration launch reloads
-//    its rows and leaves the partial consensus sum for the NCCL allreduce.
+//  * k_admm_gj / k_bf_gj (world == 1): all T iterations + outputs in one
+//    launch, the rows of B^{-1} stay in registers.  k_admm_it / k_bf_it (any
+//    world): one round per launch, leaving the partial consensus sum for the
+//    NCCL allreduce.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -33,26 +26,6 @@ namespace dbp {
 
 // ============================================================ ADMM-UL
 
-
-// Split path, preprocessing: G^{-1} and yreg = G^{-1} mf per pair (lane = row).
-template <int UP>
-__global__ void __launch_bounds__(256, UP == 32 ? 1 : 3) k_inv_ul(UlArgs a, long npairs) {
-    __shared__ __align__(16) float2 sbuf[256 / UP][UP];
-    const int q = threadIdx.x / UP, i = threadIdx.x % UP;
-    const long p = (long)blockIdx.x * (256 / UP) + q;
-    const bool valid = p < npairs;
-    const long pp = valid ? p : npairs - 1;
-    float2 R[UP];
-    load_herm_row<UP>(a.G + (size_t)pp * tri(UP), i, R);
-    const bool ok = gj_invert<UP>(R, sbuf[q], i);
-    if (!ok && valid) atomicOr(a.flag, 1);
-    if (valid) store_herm_row<UP>(a.Ginv + (size_t)p * tri(UP), i, R);
-    for (int j = 0; j < a.J; ++j) {
-        const float2 m = a.mf[((size_t)pp * a.J + j) * UP + i];
-        const float2 yr = row_apply<UP>(R, sbuf[q], i, m);
-        if (valid) a.yreg[((size_t)p * a.J + j) * UP + i] = yr;
-    }
-}
 
 // Fused (world == 1): G^{-1} in registers, all T iterations of Alg. 1 on chip.
 // CTA = NT subcarriers x C clusters x UP lanes.
@@ -73,7 +46,7 @@ __global__ void __launch_bounds__(512) k_admm_gj(UlArgs a) {
     float2* buf = pbuf + (size_t)q * UP;
 
     float2 R[UP];
-    load_herm_row<UP>(a.Ginv + pair * tri(UP), i, R); // row i of B_c^{-1} (k_inv_ul)
+    load_herm_row<UP>(a.Ginv + pair * tri(UP), i, R); // row i of B_c^{-1} (k_prefold / k_prelr)
 #pragma unroll
     for (int j = 0; j < UP; ++j) R[j] = c_scale(R[j], a.rho);   // rho B_c^{-1} (eq. (3))
 
@@ -194,21 +167,6 @@ __device__ __forceinline__ void bf_output(const float2* __restrict__ Hd, float2*
     __syncwarp();
 }
 
-// Split path: B^{-1} per pair.
-template <int UP>
-__global__ void __launch_bounds__(256, UP == 32 ? 1 : 3) k_inv_dl(DlArgs a, long npairs) {
-    __shared__ __align__(16) float2 sbuf[256 / UP][UP];
-    const int q = threadIdx.x / UP, i = threadIdx.x % UP;
-    const long p = (long)blockIdx.x * (256 / UP) + q;
-    const bool valid = p < npairs;
-    const long pp = valid ? p : npairs - 1;
-    float2 R[UP];
-    load_herm_row<UP>(a.G + (size_t)pp * tri(UP), i, R);
-    const bool ok = gj_invert<UP>(R, sbuf[q], i);
-    if (!ok && valid) atomicOr(a.flag, 1);
-    if (valid) store_herm_row<UP>(a.Binv + (size_t)p * tri(UP), i, R);
-}
-
 // Fused (world == 1): B^{-1} in registers; init, T-1 consensus iterations of
 // Alg. 3 in the exact m-form (m_c = q - rho^{-1} B^{-1} q, q = z + lambda;
 // DESIGN.md section 5) and the output pass x_c = H_c^H B^{-1} q.
@@ -237,7 +195,7 @@ __global__ void __launch_bounds__(512) k_bf_gj(DlArgs a) {
                          "r"((uint32_t)bytes) : "memory");
     }
     float2 R[UP];
-    load_herm_row<UP>(a.Binv + pair * tri(UP), i, R);  // row i of B_c^{-1} (k_inv_dl)
+    load_herm_row<UP>(a.Binv + pair * tri(UP), i, R);  // row i of B_c^{-1} (k_prefold / k_prelr)
 
     for (int jj = 0; jj < a.J; ++jj) {
         const float2 sv = i < a.U ? a.s[((size_t)nn * a.J + jj) * a.U + i] : make_float2(0.f, 0.f);
@@ -352,12 +310,6 @@ static void big_smem(K k, size_t smem) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
-cudaError_t launch_inv_ul(const LaunchCtx& L, int UP, UlArgs a, long npairs) {
-    DBP_DISPATCH_UP(UP, k_inv_ul<UPc><<<cdiv_i(npairs, 256 / UPc), 256, 0, L.stream>>>(a, npairs));
-    L.count(1);
-    return cudaGetLastError();
-}
-
 cudaError_t launch_admm_gj(const LaunchCtx& L, int UP, UlArgs a) {
     const size_t smem = iter_smem(UP, a.NT, a.C_loc);
     DBP_DISPATCH_UP(UP, big_smem(k_admm_gj<UPc>, smem);
@@ -380,12 +332,6 @@ cudaError_t launch_admm_it(const LaunchCtx& L, int UP, UlArgs a, int CCH) {
     const size_t smem = split_smem(UP, a.NT, CCH, a.J);
     DBP_DISPATCH_UP(UP, big_smem(k_admm_it<UPc>, smem);
                     k_admm_it<UPc><<<cdiv_i(a.N, a.NT), a.NT * CCH * UPc, smem, L.stream>>>(a, CCH));
-    L.count(1);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_inv_dl(const LaunchCtx& L, int UP, DlArgs a, long npairs) {
-    DBP_DISPATCH_UP(UP, k_inv_dl<UPc><<<cdiv_i(npairs, 256 / UPc), 256, 0, L.stream>>>(a, npairs));
     L.count(1);
     return cudaGetLastError();
 }

@@ -1,16 +1,14 @@
-// dbp_kernels.cu -- sm_100a kernels of libdbp and their launchers.
+// dbp_kernels.cu -- small kernels of libdbp and their launchers.
 //
 // Kernel map (SURVEY.md 8(a) rows -> kernels):
-//   k_pre      a1-a3 / b1 / c1  per (cluster, subcarrier) pair -- dbp_pre.cu.
-//   k_admm_it  a4-a7            ADMM-UL consensus iterations: split (one step
-//                               per launch + NCCL between) or fused (all T
-//                               iterations on chip, world == 1).
+//   k_fused    all rows         one launch per solver at world == 1 (dbp_fused.cu)
+//   k_prefold  a1-a3 / b1 / c1  per-pair Gram + inverse, UP <= 16 (dbp_prefold.cu)
+//   k_prelr    a1-a3 / b1 / c1  the same for UP = 32 or N_sym > 1 (dbp_prelr.cu)
+//   k_admm_gj, k_admm_it, k_bf_gj, k_bf_it   iterations (dbp_iter.cu)
 //   k_cg_gsum  b1 (sum)         per-GPU Gram sum G_loc = sum_c H_c^H H_c
 //                               (Alg. 2 line 9 footnote, P416) + local y^MRC.
 //   k_cg_it    b2-b5            replicated CG updates with shuffle allreduce
 //                               dot products (P715), split or fused.
-//   k_bf_it    c2-c4            ADMM-DL iterations in the exact m-form,
-//                               split or fused, incl. the final x_c pass.
 //   k_prox_out a7-a8            final prox + hard slicing of the split path.
 //   k_slice                     stand-alone slicer (P210).
 #include <cuda_runtime.h>

@@ -19,7 +19,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PROF = os.path.join(ROOT, "profiles")
 
 # libdbp kernel symbol -> bench kernel-timer name
-NAMES = [(r"k_prefold<\d+, 0, 0", "pre_cg"), (r"k_prefold<\d+, 0, 1", "pre_ul"), (r"k_prefold<\d+, 1, 2", "pre_dl"),
+NAMES = [(r"k_fused<\d+, 0>", "fused_cg"), (r"k_fused<\d+, 1>", "fused_ul"), (r"k_fused<\d+, 2>", "fused_dl"),
+         (r"k_prefold<\d+, 0, 0", "pre_cg"), (r"k_prefold<\d+, 0, 1", "pre_ul"), (r"k_prefold<\d+, 1, 2", "pre_dl"),
          (r"k_prelr<\d+, 0, 0", "pre_cg"), (r"k_prelr<\d+, 0, 1", "pre_ul"), (r"k_prelr<\d+, 1, 2", "pre_dl"),
          (r"k_gram<\d+, 0, 1", "gram_ul"), (r"k_gram<\d+, 1,", "gram_dl"), (r"k_inv_ul", "inv_ul"),
          (r"k_inv_dl", "inv_dl"), (r"k_admm_gj", "admm_fused"), (r"k_bf_gj", "bf_fused"),
