@@ -40,6 +40,56 @@ __device__ __forceinline__ void c_fmacb(float2& acc, float2 a, float2 b) {
 }
 __device__ __forceinline__ float c_norm2(float2 a) { return fmaf(a.x, a.x, a.y * a.y); }
 
+// ---- packed f32x2 complex MACs (sm_100 FFMA2: two FP32 FMAs per instruction).
+// A complex value is one 64-bit register pair (re, im).  In every helper the
+// reused operand `a` / `f` is the FIRST source, so ptxas expresses the sign
+// and swap patterns as operand modifiers of that natural pair (.NP negates the
+// high half, .LO_HI swaps) and the per-call values become scalar broadcasts
+// (.F32): each complex MAC is exactly 2 FFMA2 with no pair construction
+// (checked in SASS; the reverse operand order costs a MOV per use).
+typedef unsigned long long f2x;
+__device__ __forceinline__ f2x pk2(float x, float y) {
+    f2x r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+    return r;
+}
+__device__ __forceinline__ f2x pk2(float2 v) { return pk2(v.x, v.y); }
+__device__ __forceinline__ float2 upk2(f2x r) {
+    float2 v;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+    return v;
+}
+__device__ __forceinline__ f2x ffma2(f2x a, f2x b, f2x c) {
+    f2x d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+// acc += a b          = b.x a + (-b.y) (a.y, -a.x)
+__device__ __forceinline__ void x2_mac(f2x& acc, float2 a, float bx, float by) {
+    acc = ffma2(pk2(a.x, a.y), pk2(bx, bx), acc);
+    acc = ffma2(pk2(a.y, -a.x), pk2(-by, -by), acc);
+}
+// acc += conj(a) b    = b.x (a.x, -a.y) + b.y (a.y, a.x)
+__device__ __forceinline__ void x2_cmac(f2x& acc, float2 a, float bx, float by) {
+    acc = ffma2(pk2(a.x, -a.y), pk2(bx, bx), acc);
+    acc = ffma2(pk2(a.y, a.x), pk2(by, by), acc);
+}
+// acc += a conj(b)    = b.x a + b.y (a.y, -a.x)
+__device__ __forceinline__ void x2_macc(f2x& acc, float2 a, float bx, float by) {
+    acc = ffma2(pk2(a.x, a.y), pk2(bx, bx), acc);
+    acc = ffma2(pk2(a.y, -a.x), pk2(by, by), acc);
+}
+// x -= f conj(c)      = (-c.x) f + (-c.y) (f.y, -f.x)
+__device__ __forceinline__ void x2_fmsc(f2x& x, float2 f, float cx, float cy) {
+    x = ffma2(pk2(f.x, f.y), pk2(-cx, -cx), x);
+    x = ffma2(pk2(f.y, -f.x), pk2(-cy, -cy), x);
+}
+// x -= f e            = (-e.x) f + e.y (f.y, -f.x)
+__device__ __forceinline__ void x2_fms(f2x& x, float2 f, float ex, float ey) {
+    x = ffma2(pk2(f.x, f.y), pk2(-ex, -ex), x);
+    x = ffma2(pk2(f.y, -f.x), pk2(ey, ey), x);
+}
+
 __device__ __forceinline__ float rcp_approx(float x) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));

@@ -59,7 +59,7 @@ struct FoldStage {
 // UL: G_rt += conj(h_sr) h_st (and b_r += conj(h_sr) y_s) over one stage.
 // Pair q reads antenna (s + q/2) mod 4: the 8 pairs' LDS.128 hit distinct bank groups.
 template <int UP, bool MF>
-__device__ __forceinline__ void fold_gram_ul(float2 (&A)[Fold<UP>::NSLOT], float2 (&E)[4], const float2* stage, int q,
+__device__ __forceinline__ void fold_gram_ul(f2x (&A)[Fold<UP>::NSLOT], f2x (&E)[4], const float2* stage, int q,
                                              const int (&row)[4]) {
     using F = Fold<UP>;
     using G = FoldStage<UP, false, MF>;
@@ -77,18 +77,18 @@ __device__ __forceinline__ void fold_gram_ul(float2 (&A)[Fold<UP>::NSLOT], float
 #pragma unroll
         for (int m = 0; m < 4; ++m)
 #pragma unroll
-            for (int t = 0; t < (m + 1) * F::L; ++t) c_fmac(A[F::off(m) + t], o[m], h[t]);
+            for (int t = 0; t < (m + 1) * F::L; ++t) x2_cmac(A[F::off(m) + t], o[m], h[t].x, h[t].y);
         if (MF) {
             const float2 yv = yq[sr];
 #pragma unroll
-            for (int m = 0; m < 4; ++m) c_fmac(E[m], o[m], yv);
+            for (int m = 0; m < 4; ++m) x2_cmac(E[m], o[m], yv.x, yv.y);
         }
     }
 }
 
 // DL: B_rt += H_rs conj(H_ts); pair q reads antenna pair (s/2 + q/4) mod 2.
 template <int UP>
-__device__ __forceinline__ void fold_gram_dl(float2 (&A)[Fold<UP>::NSLOT], const float2* stage, int q, const int (&row)[4]) {
+__device__ __forceinline__ void fold_gram_dl(f2x (&A)[Fold<UP>::NSLOT], const float2* stage, int q, const int (&row)[4]) {
     using F = Fold<UP>;
     using G = FoldStage<UP, true, false>;
     const float2* hq = stage + q * G::NL * G::HL;
@@ -104,8 +104,8 @@ __device__ __forceinline__ void fold_gram_dl(float2 (&A)[Fold<UP>::NSLOT], const
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
                 if (t < (m + 1) * F::L) {
-                    c_fmacb(A[F::off(m) + t], make_float2(o[m].x, o[m].y), make_float2(v.x, v.y));
-                    c_fmacb(A[F::off(m) + t], make_float2(o[m].z, o[m].w), make_float2(v.z, v.w));
+                    x2_macc(A[F::off(m) + t], make_float2(o[m].x, o[m].y), v.x, v.y);
+                    x2_macc(A[F::off(m) + t], make_float2(o[m].z, o[m].w), v.z, v.w);
                 }
             }
         }
@@ -116,7 +116,7 @@ __device__ __forceinline__ void fold_gram_dl(float2 (&A)[Fold<UP>::NSLOT], const
 // a "t == row" compare chain gets folded into a dynamically indexed
 // local-memory access by the compiler.)
 template <int UP>
-__device__ __forceinline__ void fold_diag(float2 (&A)[Fold<UP>::NSLOT], const int (&row)[4], float delta, float (&dg)[4]) {
+__device__ __forceinline__ void fold_diag(f2x (&A)[Fold<UP>::NSLOT], const int (&row)[4], float delta, float (&dg)[4]) {
     using F = Fold<UP>;
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
@@ -125,10 +125,11 @@ __device__ __forceinline__ void fold_diag(float2 (&A)[Fold<UP>::NSLOT], const in
 #pragma unroll
         for (int t = 0; t < (m + 1) * F::L; ++t) {
             const bool d = (dmask >> t) & 1u;
-            float2& x = A[F::off(m) + t];
+            float2 x = upk2(A[F::off(m) + t]);
             x.x = d ? x.x + delta : x.x;
             x.y = d ? 0.f : x.y;
             dg[m] += d ? x.x : 0.f;
+            A[F::off(m) + t] = pk2(x);
         }
     }
 }
@@ -136,7 +137,7 @@ __device__ __forceinline__ void fold_diag(float2 (&A)[Fold<UP>::NSLOT], const in
 // Jacobi scaling to unit diagonal: A_rt *= d_r d_t, E_r *= d_r (d = dg^-1/2,
 // published to the pair's dline for the column factors).
 template <int UP, bool BORDER>
-__device__ __forceinline__ void fold_jacobi(float2 (&A)[Fold<UP>::NSLOT], float2 (&E)[4], const float (&dg)[4],
+__device__ __forceinline__ void fold_jacobi(f2x (&A)[Fold<UP>::NSLOT], f2x (&E)[4], const float (&dg)[4],
                                             float (&dr)[4], float* dline, const int (&row)[4]) {
     using F = Fold<UP>;
 #pragma unroll
@@ -148,8 +149,8 @@ __device__ __forceinline__ void fold_jacobi(float2 (&A)[Fold<UP>::NSLOT], float2
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
 #pragma unroll
-        for (int t = 0; t < (m + 1) * F::L; ++t) A[F::off(m) + t] = c_scale(A[F::off(m) + t], dr[m] * dline[t]);
-        if (BORDER) E[m] = c_scale(E[m], dr[m]);
+        for (int t = 0; t < (m + 1) * F::L; ++t) A[F::off(m) + t] = pk2(c_scale(upk2(A[F::off(m) + t]), dr[m] * dline[t]));
+        if (BORDER) E[m] = pk2(c_scale(upk2(E[m]), dr[m]));
     }
 }
 
@@ -158,7 +159,7 @@ __device__ __forceinline__ void fold_jacobi(float2 (&A)[Fold<UP>::NSLOT], float2
 // M^{-1} E.  pl: the pair's UP+2 line (pivot column, E_k).  Returns false if
 // a pivot was not positive and finite (not HPD).
 template <int UP, bool BORDER>
-__device__ __forceinline__ bool fold_sweep(float2 (&A)[Fold<UP>::NSLOT], float2 (&E)[4], float2* pl, const int (&row)[4],
+__device__ __forceinline__ bool fold_sweep(f2x (&A)[Fold<UP>::NSLOT], f2x (&E)[4], float2* pl, const int (&row)[4],
                                            int l) {
     using F = Fold<UP>;
     constexpr int L = F::L;
@@ -173,11 +174,11 @@ __device__ __forceinline__ bool fold_sweep(float2 (&A)[Fold<UP>::NSLOT], float2 
         float2* const dump = pl + UP + 1;
 #pragma unroll
         for (int m = 0; m < 4; ++m)
-            if (k < (m + 1) * L) *(row[m] >= k ? pl + row[m] : dump) = A[F::off(m) + k];
+            if (k < (m + 1) * L) *(row[m] >= k ? pl + row[m] : dump) = upk2(A[F::off(m) + k]);
         if (l == lk) {
 #pragma unroll
-            for (int t = 0; t < k && t < (mk + 1) * L; ++t) pl[t] = c_conj(A[F::off(mk) + t]);
-            if (BORDER) pl[UP] = E[mk];
+            for (int t = 0; t < k && t < (mk + 1) * L; ++t) pl[t] = c_conj(upk2(A[F::off(mk) + t]));
+            if (BORDER) pl[UP] = upk2(E[mk]);
         }
         __syncwarp();
         float2 cr[4];
@@ -195,10 +196,7 @@ __device__ __forceinline__ bool fold_sweep(float2 (&A)[Fold<UP>::NSLOT], float2 
             // pivot row: a_kt / a_kk = a_kt - (1 - 1/a_kk) a_kt (no cancellation: a_kk <= 1)
             me[m] = row[m] == k;
             f[m] = me[m] ? make_float2(1.f - ip, 0.f) : c_scale(cr[m], ip);
-            if (BORDER) {    // E -= f E_k
-                E[m].x = fmaf(-f[m].x, Ek.x, fmaf(f[m].y, Ek.y, E[m].x));
-                E[m].y = fmaf(-f[m].x, Ek.y, fmaf(-f[m].y, Ek.x, E[m].y));
-            }
+            if (BORDER) x2_fms(E[m], f[m], Ek.x, Ek.y);    // E -= f E_k
         }
         // t-outer: each broadcast c_t (two per LDS.128) is live only across its R slots
 #pragma unroll
@@ -211,12 +209,11 @@ __device__ __forceinline__ bool fold_sweep(float2 (&A)[Fold<UP>::NSLOT], float2 
 #pragma unroll
                 for (int m = 0; m < 4; ++m) {
                     if (t >= (m + 1) * L) continue;
-                    float2& x = A[F::off(m) + t];
+                    f2x& x = A[F::off(m) + t];
                     if (t == k) {
-                        x = me[m] ? make_float2(-ip, 0.f) : c_scale(x, ip);
+                        x = me[m] ? pk2(-ip, 0.f) : pk2(c_scale(upk2(x), ip));
                     } else {    // x -= f conj(c_t)
-                        x.x = fmaf(-f[m].x, ct.x, fmaf(-f[m].y, ct.y, x.x));
-                        x.y = fmaf(-f[m].y, ct.x, fmaf(f[m].x, ct.y, x.y));
+                        x2_fmsc(x, f[m], ct.x, ct.y);
                     }
                 }
             }
@@ -228,27 +225,28 @@ __device__ __forceinline__ bool fold_sweep(float2 (&A)[Fold<UP>::NSLOT], float2 
 // After fold_sweep on the Jacobi-scaled matrix: M^{-1}_rt = -d_r d_t A_rt,
 // (M^{-1} b)_r = d_r E_r; `scale` multiplies the inverse (e.g. rho).
 template <int UP, bool BORDER>
-__device__ __forceinline__ void fold_unscale(float2 (&A)[Fold<UP>::NSLOT], float2 (&E)[4], const float (&dr)[4],
+__device__ __forceinline__ void fold_unscale(f2x (&A)[Fold<UP>::NSLOT], f2x (&E)[4], const float (&dr)[4],
                                              const float* dline, float scale) {
     using F = Fold<UP>;
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
 #pragma unroll
-        for (int t = 0; t < (m + 1) * F::L; ++t) A[F::off(m) + t] = c_scale(A[F::off(m) + t], -scale * dr[m] * dline[t]);
-        if (BORDER) E[m] = c_scale(E[m], dr[m]);
+        for (int t = 0; t < (m + 1) * F::L; ++t)
+            A[F::off(m) + t] = pk2(c_scale(upk2(A[F::off(m) + t]), -scale * dr[m] * dline[t]));
+        if (BORDER) E[m] = pk2(c_scale(upk2(E[m]), dr[m]));
     }
 }
 
 // Packed lower-triangle store of the valid slots.
 template <int UP>
-__device__ __forceinline__ void fold_store(float2* G, const float2 (&A)[Fold<UP>::NSLOT], const int (&row)[4]) {
+__device__ __forceinline__ void fold_store(float2* G, const f2x (&A)[Fold<UP>::NSLOT], const int (&row)[4]) {
     using F = Fold<UP>;
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
         float2* Gr = G + (row[m] * (row[m] + 1)) / 2;
 #pragma unroll
         for (int t = 0; t < (m + 1) * F::L; ++t)
-            if (t <= row[m]) Gr[t] = A[F::off(m) + t];
+            if (t <= row[m]) Gr[t] = upk2(A[F::off(m) + t]);
     }
 }
 
@@ -256,7 +254,7 @@ __device__ __forceinline__ void fold_store(float2* G, const float2 (&A)[Fold<UP>
 // the diagonal halved, so y = M v is  y_r = sum_slots(r) S_rt v_t  +
 // sum_lanes sum_slots(t, r) conj(S_tr) v_t  with no validity predicates.
 template <int UP>
-__device__ __forceinline__ void fold_mv_prep(float2 (&A)[Fold<UP>::NSLOT], const int (&row)[4]) {
+__device__ __forceinline__ void fold_mv_prep(f2x (&A)[Fold<UP>::NSLOT], const int (&row)[4]) {
     using F = Fold<UP>;
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
@@ -264,9 +262,8 @@ __device__ __forceinline__ void fold_mv_prep(float2 (&A)[Fold<UP>::NSLOT], const
 #pragma unroll
         for (int t = 0; t < (m + 1) * F::L; ++t) {
             const bool v = (vmask >> t) & 1u, d = (dmask >> t) & 1u;
-            float2& x = A[F::off(m) + t];
             const float sc = v ? (d ? 0.5f : 1.f) : 0.f;
-            x = c_scale(x, sc);
+            A[F::off(m) + t] = pk2(c_scale(upk2(A[F::off(m) + t]), sc));
         }
     }
 }
@@ -274,34 +271,39 @@ __device__ __forceinline__ void fold_mv_prep(float2 (&A)[Fold<UP>::NSLOT], const
 // y_{r_m} = (M v)_{r_m} for the pair's 4 rows per lane.  vline: the pair's
 // UP-line; ybuf: the pair's L x UP partial-sum block.  Both in shared memory.
 template <int UP>
-__device__ __forceinline__ void fold_mv(const float2 (&A)[Fold<UP>::NSLOT], const float2 (&v)[4], float2 (&y)[4],
+__device__ __forceinline__ void fold_mv(const f2x (&A)[Fold<UP>::NSLOT], const float2 (&v)[4], float2 (&y)[4],
                                         float2* vline, float2* ybuf, const int (&row)[4], int l) {
     using F = Fold<UP>;
     __syncwarp();
 #pragma unroll
     for (int m = 0; m < 4; ++m) vline[row[m]] = v[m];
     __syncwarp();
-    float2 col[UP];
+    f2x col[UP];
 #pragma unroll
-    for (int t = 0; t < UP; ++t) col[t] = make_float2(0.f, 0.f);
+    for (int t = 0; t < UP; ++t) col[t] = 0ull;
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
-        float2 acc = make_float2(0.f, 0.f);
+        f2x acc = 0ull;
 #pragma unroll
         for (int t2 = 0; t2 < (m + 1) * F::L; t2 += 2) {
             const float4 vv = *reinterpret_cast<const float4*>(vline + t2);
-            c_fma(acc, A[F::off(m) + t2], make_float2(vv.x, vv.y));
-            c_fmac(col[t2], A[F::off(m) + t2], v[m]);
+            const float2 s0 = upk2(A[F::off(m) + t2]);
+            x2_mac(acc, s0, vv.x, vv.y);                   // y_r += S_rt v_t
+            x2_cmac(col[t2], s0, v[m].x, v[m].y);          // y_t += conj(S_rt) v_r
             if (t2 + 1 < (m + 1) * F::L) {
-                c_fma(acc, A[F::off(m) + t2 + 1], make_float2(vv.z, vv.w));
-                c_fmac(col[t2 + 1], A[F::off(m) + t2 + 1], v[m]);
+                const float2 s1 = upk2(A[F::off(m) + t2 + 1]);
+                x2_mac(acc, s1, vv.z, vv.w);
+                x2_cmac(col[t2 + 1], s1, v[m].x, v[m].y);
             }
         }
-        y[m] = acc;
+        y[m] = upk2(acc);
     }
     float4* yb = reinterpret_cast<float4*>(ybuf + l * UP);
 #pragma unroll
-    for (int t2 = 0; t2 < UP; t2 += 2) yb[t2 / 2] = make_float4(col[t2].x, col[t2].y, col[t2 + 1].x, col[t2 + 1].y);
+    for (int t2 = 0; t2 < UP; t2 += 2) {
+        const float2 c0 = upk2(col[t2]), c1 = upk2(col[t2 + 1]);
+        yb[t2 / 2] = make_float4(c0.x, c0.y, c1.x, c1.y);
+    }
     __syncwarp();
 #pragma unroll
     for (int m = 0; m < 4; ++m)

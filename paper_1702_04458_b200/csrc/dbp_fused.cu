@@ -149,12 +149,12 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
         const bool valid = n < a.N && c < a.C;
 
         // ------------------------------------------------ local Gram (+ matched filter)
-        float2 A[F::NSLOT];
+        f2x A[F::NSLOT];
 #pragma unroll
-        for (int e = 0; e < F::NSLOT; ++e) A[e] = make_float2(0.f, 0.f);
-        float2 E[R];
+        for (int e = 0; e < F::NSLOT; ++e) A[e] = 0ull;
+        f2x E[R];
 #pragma unroll
-        for (int m = 0; m < R; ++m) E[m] = make_float2(0.f, 0.f);
+        for (int m = 0; m < R; ++m) E[m] = 0ull;
         for (int ch = 0; ch < nch; ++ch) {
             mbar_wait(&bar[st], phase);
             const float2* stage = reinterpret_cast<const float2*>(wbase + st * G::STG);
@@ -171,28 +171,28 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
             // over the subcarrier's WPS warps in fixed order: G = sum_c G_c, y^MRC = sum_c H_c^H y_c
 #pragma unroll
             for (int e = 0; e < F::NSLOT; ++e) {
-                float2 v = valid ? A[e] : make_float2(0.f, 0.f);
+                float2 v = valid ? upk2(A[e]) : make_float2(0.f, 0.f);
 #pragma unroll
                 for (int o = L; o < 32; o <<= 1) {
                     v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
                     v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
                 }
-                A[e] = v;
+                A[e] = pk2(v);
             }
 #pragma unroll
             for (int m = 0; m < R; ++m) {
-                float2 v = valid ? E[m] : make_float2(0.f, 0.f);
+                float2 v = valid ? upk2(E[m]) : make_float2(0.f, 0.f);
 #pragma unroll
                 for (int o = L; o < 32; o <<= 1) {
                     v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
                     v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
                 }
-                E[m] = v;
+                E[m] = pk2(v);
             }
             if (lane < L) {
                 fold_store<UP>(Gp + warp * TRI, A, row);
 #pragma unroll
-                for (int m = 0; m < R; ++m) Wp[warp * UP + row[m]] = E[m];
+                for (int m = 0; m < R; ++m) Wp[warp * UP + row[m]] = upk2(E[m]);
             }
             __syncthreads();
             for (int e = tid; e < NPC * (TRI + UP); e += Z::WARPS * 32) {
@@ -271,7 +271,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
             float2 yreg[R], lam[R], z[R], w[R];
 #pragma unroll
             for (int m = 0; m < R; ++m) {
-                yreg[m] = E[m];
+                yreg[m] = upk2(E[m]);
                 lam[m] = make_float2(0.f, 0.f);
                 z[m] = yreg[m];
                 w[m] = yreg[m];
@@ -382,7 +382,10 @@ static bool launch_fz_t(const LaunchCtx& L, const float2* H, const float2* y, Fu
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, Z::WARPS * 32, Z::SMEM);
     const int ngroups = (a.N + a.NPC - 1) / a.NPC;
-    const int grid = std::min(ngroups, g_sms_fz * std::max(per_sm, 1));
+#ifndef DBP_FZ_PERSIST
+#define DBP_FZ_PERSIST 1
+#endif
+    const int grid = DBP_FZ_PERSIST ? std::min(ngroups, g_sms_fz * std::max(per_sm, 1)) : ngroups;
     k<<<grid, Z::WARPS * 32, Z::SMEM, L.stream>>>(tmH, tmY, a);
     L.count(1);
     return true;

@@ -126,12 +126,12 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
         const long p = (long)(gw + it * W) * PW + q;
         const bool valid = p < a.npairs;
 
-        float2 A[P::NSLOT];
+        f2x A[P::NSLOT];
 #pragma unroll
-        for (int e = 0; e < P::NSLOT; ++e) A[e] = make_float2(0.f, 0.f);
-        float2 E[R];
+        for (int e = 0; e < P::NSLOT; ++e) A[e] = 0ull;
+        f2x E[R];
 #pragma unroll
-        for (int m = 0; m < R; ++m) E[m] = make_float2(0.f, 0.f);
+        for (int m = 0; m < R; ++m) E[m] = 0ull;
 
         for (int ch = 0; ch < nch; ++ch) {
             mbar_wait(&bar[st], phase);
@@ -152,7 +152,7 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
             if (valid) {
                 fold_store<UP>(a.Gout + (size_t)p * P::TRI, A, row);
 #pragma unroll
-                for (int m = 0; m < R; ++m) a.vout[(size_t)p * UP + row[m]] = E[m];
+                for (int m = 0; m < R; ++m) a.vout[(size_t)p * UP + row[m]] = upk2(E[m]);
             }
             continue;
         }
@@ -165,7 +165,7 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
             fold_store<UP>(a.Gout + (size_t)p * P::TRI, A, row);
             if (MODE == 1) {
 #pragma unroll
-                for (int m = 0; m < R; ++m) a.vout[(size_t)p * UP + row[m]] = E[m];
+                for (int m = 0; m < R; ++m) a.vout[(size_t)p * UP + row[m]] = upk2(E[m]);
             }
         }
     }
