@@ -94,7 +94,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     float2* Wp = reinterpret_cast<float2*>(smem_raw + 128 + (size_t)Z::WARPS * Z::WREG);   // [4 warps][UP]
     float2* Sv = Wp + Z::WARPS * UP;                                                       // [4 subc.][UP]
     float2* Gp = Sv + Z::WARPS * UP;                                                       // CG: [4 warps][TRI]
-    float2* Gs = Gp + (SOLVER == 0 ? Z::WARPS * TRI : 0);                                  // CG: [4 subc.][TRI]
+    float2* Gs = Gp + (SOLVER == 0 ? Z::WARPS * TRI : 0);                                  // CG queue: [4][TRI]
 
     int row[R];
 #pragma unroll
@@ -132,8 +132,10 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     if (lane == 0)
         for (int s = 0; s < NST && s < nseq; ++s) issue(s, s);
 
-    int sq = 0, st = 0;
+    int sq = 0, st = 0, qn = 0;
     uint32_t phase = 0;
+    static_assert(Z::WARPS * NST * 8 <= 96, "mbarriers overlap the CG queue indices");
+    int* qsub = reinterpret_cast<int*>(smem_raw + 96);     // CG queue: subcarrier of each slot
     auto next_stage = [&]() {
         __syncwarp();
         if (lane == 0 && sq + NST < nseq) {
@@ -195,22 +197,31 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                 for (int m = 0; m < R; ++m) Wp[warp * UP + row[m]] = upk2(E[m]);
             }
             __syncthreads();
+            // the subcarrier sums go to CG queue slots qn..qn+NPC-1 (4 slots, one per warp)
             for (int e = tid; e < NPC * (TRI + UP); e += Z::WARPS * 32) {
                 const int jj = e / (TRI + UP), f = e - jj * (TRI + UP);
                 float2 acc = make_float2(0.f, 0.f);
                 if (f < TRI) {
                     for (int w2 = 0; w2 < WPS; ++w2) acc = c_add(acc, Gp[(jj * WPS + w2) * TRI + f]);
-                    Gs[jj * TRI + f] = acc;
+                    Gs[(qn + jj) * TRI + f] = acc;
                 } else {
                     for (int w2 = 0; w2 < WPS; ++w2) acc = c_add(acc, Wp[(jj * WPS + w2) * UP + f - TRI]);
-                    Sv[jj * UP + f - TRI] = acc;
+                    Sv[(qn + jj) * UP + f - TRI] = acc;
                 }
             }
+            if (tid < NPC) qsub[qn + tid] = (blockIdx.x + it * gridDim.x) * NPC + tid;
+            qn += NPC;
             __syncthreads();
-            if (warp < NPC) {                           // warp w runs the CG of subcarrier slot w
-                const int nn = (blockIdx.x + it * gridDim.x) * NPC + warp;
+            if (qn < Z::WARPS && it + 1 < nitems) continue;
+            // the CG iterations of up to 4 queued subcarriers, one per warp (all warps busy)
+            if (warp < qn) {
+                const int nn = qsub[warp];
                 const int u = lane % UP;
                 const float2* Gj = Gs + warp * TRI;
+                float2 grow[UP];                        // row u of G in registers
+#pragma unroll
+                for (int jc = 0; jc < UP; ++jc)
+                    grow[jc] = jc <= u ? Gj[(u * (u + 1)) / 2 + jc] : c_conj(Gj[(jc * (jc + 1)) / 2 + u]);
                 float2* P = pl - q * (UP + 2) + (lane / UP) * (UP + 2);       // a per-group line
                 float2 r = Sv[warp * UP + u];           // line 6: r = y^MRC, p = r, x = 0
                 float2 p = r, x = make_float2(0.f, 0.f);
@@ -219,7 +230,11 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                     __syncwarp();
                     P[u] = p;
                     __syncwarp();
-                    const float2 w = herm_mv_row<UP>(Gj, P, u);                 // lines 9-11
+                    float2 pv[UP];
+                    read_vec<UP>(P, pv);
+                    float2 w = make_float2(0.f, 0.f);                            // lines 9-11: w = G p
+#pragma unroll
+                    for (int jc = 0; jc < UP; ++jc) c_fma(w, grow[jc], pv[jc]);
                     cg_update<UP>(x, r, p, rr, w, a.rho);                        // lines 13-18
                 }
                 if (lane < UP && u < a.U && nn < a.N) {
@@ -227,7 +242,8 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                     if (a.hard) a.hard[(size_t)nn * a.U + u] = slice_bits(x, a.md);
                 }
             }
-            __syncthreads();                            // Gp / Wp / Sv reused by the next item
+            qn = 0;
+            __syncthreads();                            // queue slots reused
             continue;
         }
 
