@@ -179,6 +179,26 @@ dbp_status dbp_slice(dbp_ctx* ctx, int mod, int64_t count, const dbp_cf32* x, ui
 dbp_status dbp_get_kernel_times(dbp_ctx* ctx, dbp_kernel_time* out, int max_entries, int* n_entries,
                                 int reset);
 
+/* ---- Table I (P566-595): real-multiplication counts of the decentralized and
+ * centralized algorithms, the paper's complexity model (P616-622).  Host-only
+ * arithmetic, no context or GPU needed.
+ *   algo    DBP_CPLX_ADMM_DL, _ADMM_UL, _CG_UL (decentralized, with `mode`
+ *           and `metric`), _ZF_DL, _MMSE_UL (centralized: mode and metric are
+ *           ignored, the whole count is returned as `total` and `pre`)
+ *   mode    DBP_CPLX_SxS or DBP_CPLX_UxU (ignored for CG-UL)
+ *   metric  DBP_CPLX_TM (timing: one cluster's PE) or DBP_CPLX_AR (all PEs)
+ *   out     [0] preprocessing, [1] first iteration, [2] each subsequent
+ *           iteration, [3] total(T) = [0] + [1] + (T - 1) [2]
+ * Every Table I expression is integral for integer U, S, C (the 1/3 terms
+ * combine to multiples of 3), so the counts are exact.  Errors: U, S, C, T < 1
+ * or an unknown algo / mode / metric -> DBP_ERR_INVALID_ARG. */
+typedef enum { DBP_CPLX_ADMM_DL = 0, DBP_CPLX_ADMM_UL = 1, DBP_CPLX_CG_UL = 2, DBP_CPLX_ZF_DL = 3,
+               DBP_CPLX_MMSE_UL = 4 } dbp_cplx_algo;
+typedef enum { DBP_CPLX_SxS = 0, DBP_CPLX_UxU = 1 } dbp_cplx_mode;
+typedef enum { DBP_CPLX_TM = 0, DBP_CPLX_AR = 1 } dbp_cplx_metric;
+dbp_status dbp_complexity(int algo, int mode, int metric, int64_t U, int64_t S, int64_t C, int64_t T,
+                          int64_t out[4]);
+
 /* Synchronise `stream`; returns DBP_ERR_NOT_HPD if a Cholesky pivot failed in
  * any call since the previous dbp_sync (and clears the flag), or
  * DBP_ERR_CUDA / DBP_ERR_NCCL for deferred runtime errors. */

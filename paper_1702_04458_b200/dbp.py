@@ -27,7 +27,10 @@ OPT_NO_FUSED = 3
 
 EXPORTS = ["dbp_get_unique_id", "dbp_ctx_create", "dbp_ctx_destroy", "dbp_set_option", "dbp_get_stats",
            "dbp_last_error", "dbp_workspace_bytes", "dbp_detect_admm", "dbp_detect_cg",
-           "dbp_beamform_admm", "dbp_slice", "dbp_sync", "dbp_get_kernel_times"]
+           "dbp_beamform_admm", "dbp_slice", "dbp_sync", "dbp_get_kernel_times", "dbp_complexity"]
+CPLX_ALGO = {"admm_dl": 0, "admm_ul": 1, "cg_ul": 2, "zf_dl": 3, "mmse_ul": 4}
+CPLX_MODE = {"SxS": 0, "UxU": 1, None: 1}
+CPLX_METRIC = {"TM": 0, "AR": 1}
 
 
 class DbpError(RuntimeError):
@@ -76,6 +79,7 @@ def load() -> ctypes.CDLL:
         "dbp_slice": [P, I, I64, P, P, P],
         "dbp_sync": [P, P],
         "dbp_get_kernel_times": [P, P, I, P, I],
+        "dbp_complexity": [I, I, I, I64, I64, I64, I64, P],
     }
     for name, args in sigs.items():
         fn = getattr(lib, name)
@@ -244,6 +248,14 @@ def beamform_admm(ctx: Context, Hd, s, *, rho=1.0, gamma=1.0, eps=0.0, T=5, x=No
     _check(load().dbp_beamform_admm(ctx._h, ctypes.byref(d), _ptr(Hd), _ptr(s), rho, gamma, eps, T, _ptr(x),
                                     _ptr(ws), wsb, _stream(stream, Hd)))
     return x
+
+
+def complexity(algo: str, mode, metric: str, U: int, S: int, C: int, T: int = 1) -> dict:
+    """Table I (P566-595) real-multiplication counts: preprocessing, first and each
+    subsequent iteration, and total(T) (host-only; see include/dbp.h)."""
+    out = (ctypes.c_int64 * 4)()
+    _check(load().dbp_complexity(CPLX_ALGO[algo], CPLX_MODE[mode], CPLX_METRIC[metric], U, S, C, T, out))
+    return {"pre": out[0], "first": out[1], "next": out[2], "total": out[3]}
 
 
 def slice_bits(ctx: Context, x, mod: str, out=None, stream=None):
