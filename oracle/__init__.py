@@ -70,6 +70,8 @@ def _load():
             "dbpo_detect_cg_trace": [P, P, P, d, i, i, i, P, P, P],
             "dbpo_beamform_admm": [P, P, P, d, d, d, i, i, P],
             "dbpo_beamform_admm_trace": [P, P, P, d, d, d, i, i, i, i, P, P, P, P],
+            "dbpo_mmse_centralized": [P, P, P, d, d, i, P, P],
+            "dbpo_zf_centralized": [P, P, P, P],
         }
         for name, args in sig.items():
             fn = getattr(lib, name)
@@ -196,3 +198,23 @@ def beamform_admm_trace(Hd, s, *, rho=1.0, gamma=1.0, eps=0.0, T=5, mode="paper"
                                             T, MODE[mode], n, j, _ptr(x), _ptr(z), _ptr(lam),
                                             _ptr(w)), "beamform_admm_trace")
     return x, z, lam, w
+
+
+def mmse_centralized(H, y, *, N0=0.0, Es=1.0, mod="qam64"):
+    """Centralized MMSE-UL (N0 = 0: ZF) over all clusters -> (x_hat [N][Nsym][U] c128, hard u8)."""
+    H, y = _c64(H), _c64(y)
+    d = _dims(H, y)
+    x = np.empty((d.N, d.N_sym, d.U), dtype=np.complex128)
+    hard = np.empty((d.N, d.N_sym, d.U), dtype=np.uint8)
+    _check(_load().dbpo_mmse_centralized(ctypes.byref(d), _ptr(H), _ptr(y), N0, Es, MOD[mod], _ptr(x),
+                                         _ptr(hard)), "mmse_centralized")
+    return x, hard
+
+
+def zf_centralized(Hd, s):
+    """Centralized ZF-DL precoder x_c = H_c^H (sum_c H_c H_c^H)^{-1} s -> x [C][N][Nsym][S] c128."""
+    Hd, s = _c64(Hd), _c64(s)
+    d = _dims(Hd, s, uplink=False)
+    x = np.empty((d.C, d.N, d.N_sym, d.S), dtype=np.complex128)
+    _check(_load().dbpo_zf_centralized(ctypes.byref(d), _ptr(Hd), _ptr(s), _ptr(x)), "zf_centralized")
+    return x

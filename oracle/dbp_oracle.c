@@ -632,3 +632,100 @@ int dbpo_beamform_admm_trace(const dbpo_dims* d, const float* Hd, const float* s
     return bf_run(d, Hd, s, rho, gamma, eps, T, mode, NULL, n_tr, j_tr, x_tr, z_tr, lam_tr,
                   w_tr);
 }
+
+/* ================================= centralized baselines (P210-218, P431, P594) */
+
+/* MMSE-UL (P212-218; SPEC mmse_centralized S218-221): for the full array
+ * H = [H_1; ...; H_C] (B x U, B = CS), x = (H^H H + (N0/Es) I_U)^{-1} H^H y,
+ * with H^H H = sum_c H_c^H H_c and H^H y = sum_c H_c^H y_c summed in cluster
+ * order.  N0 = 0 is ZF detection.  Solved by Cholesky + forward/backward
+ * substitution (hpd_inverse, then one mat-vec). */
+int dbpo_mmse_centralized(const dbpo_dims* d, const float* H, const float* y, double N0, double Es,
+                          int mod, double* x_hat, uint8_t* hard) {
+    if (!dims_ok(d) || !H || !y || !x_hat || !(N0 >= 0) || !(Es > 0) || d->U > 32) return 1;
+    float sc; int nax;
+    if (hard && !axis_levels(mod, &sc, &nax)) return 1;
+    const int C = d->C, S = d->S, U = d->U, N = d->N, J = d->N_sym;
+    int status = 0;
+#pragma omp parallel for schedule(dynamic)
+    for (int n = 0; n < N; ++n) {
+        cd* G = malloc(sizeof(cd) * U * U);
+        cd* Gc = malloc(sizeof(cd) * U * U);
+        cd* Gi = malloc(sizeof(cd) * U * U);
+        cd* Hc = malloc(sizeof(cd) * S * U);
+        cd* yc = malloc(sizeof(cd) * S);
+        cd* b = malloc(sizeof(cd) * U);
+        cd* bc = malloc(sizeof(cd) * U);
+        cd* x = malloc(sizeof(cd) * U);
+        for (int i = 0; i < U * U; ++i) G[i] = 0;
+        for (int c = 0; c < C; ++c) {
+            for (int i = 0; i < S * U; ++i) Hc[i] = ldf(H, ((size_t)c * N + n) * S * U + i);
+            gram_cols(S, U, Hc, 0.0, Gc);
+            for (int i = 0; i < U * U; ++i) G[i] += Gc[i];
+        }
+        for (int u = 0; u < U; ++u) G[u * U + u] += N0 / Es;
+        int st = hpd_inverse(U, G, Gi);
+        for (int j = 0; j < J && st == 0; ++j) {
+            for (int u = 0; u < U; ++u) b[u] = 0;
+            for (int c = 0; c < C; ++c) {
+                for (int i = 0; i < S * U; ++i) Hc[i] = ldf(H, ((size_t)c * N + n) * S * U + i);
+                for (int k = 0; k < S; ++k) yc[k] = ldf(y, (((size_t)c * N + n) * J + j) * S + k);
+                matvec_h(S, U, Hc, yc, bc);
+                for (int u = 0; u < U; ++u) b[u] += bc[u];
+            }
+            matvec(U, U, Gi, b, x);
+            for (int u = 0; u < U; ++u) std_(x_hat, ((size_t)n * J + j) * U + u, x[u]);
+            if (hard) {
+                float f[64];
+                for (int u = 0; u < U; ++u) { f[2 * u] = (float)creal(x[u]); f[2 * u + 1] = (float)cimag(x[u]); }
+                dbpo_slice(mod, U, f, hard + ((size_t)n * J + j) * U);
+            }
+        }
+        if (st) {
+#pragma omp critical
+            status = st;
+        }
+        free(G); free(Gc); free(Gi); free(Hc); free(yc); free(b); free(bc); free(x);
+    }
+    return status;
+}
+
+/* ZF-DL (P431; SPEC zf_centralized S300-308): for the full downlink matrix
+ * H = [H_1^d, ..., H_C^d] (U x B), x = H^H (H H^H)^{-1} s, i.e. r = (sum_c
+ * H_c H_c^H)^{-1} s and x_c = H_c^H r per cluster.  x: [C][N][Nsym][S]. */
+int dbpo_zf_centralized(const dbpo_dims* d, const float* Hd, const float* s, double* x) {
+    if (!dims_ok(d) || !Hd || !s || !x || d->U > 32) return 1;
+    const int C = d->C, S = d->S, U = d->U, N = d->N, J = d->N_sym;
+    int status = 0;
+#pragma omp parallel for schedule(dynamic)
+    for (int n = 0; n < N; ++n) {
+        cd* B = malloc(sizeof(cd) * U * U);
+        cd* Bc = malloc(sizeof(cd) * U * U);
+        cd* Bi = malloc(sizeof(cd) * U * U);
+        cd* Hn = malloc(sizeof(cd) * C * U * S);
+        cd* sv = malloc(sizeof(cd) * U);
+        cd* r = malloc(sizeof(cd) * U);
+        cd* xc = malloc(sizeof(cd) * S);
+        for (int i = 0; i < U * U; ++i) B[i] = 0;
+        for (int c = 0; c < C; ++c) {
+            for (int i = 0; i < U * S; ++i) Hn[(size_t)c * U * S + i] = ldf(Hd, ((size_t)c * N + n) * U * S + i);
+            gram_rows(U, S, Hn + (size_t)c * U * S, 0.0, Bc);
+            for (int i = 0; i < U * U; ++i) B[i] += Bc[i];
+        }
+        int st = hpd_inverse(U, B, Bi);
+        for (int j = 0; j < J && st == 0; ++j) {
+            for (int u = 0; u < U; ++u) sv[u] = ldf(s, ((size_t)n * J + j) * U + u);
+            matvec(U, U, Bi, sv, r);
+            for (int c = 0; c < C; ++c) {
+                matvec_h(U, S, Hn + (size_t)c * U * S, r, xc);
+                for (int k = 0; k < S; ++k) std_(x, (((size_t)c * N + n) * J + j) * S + k, xc[k]);
+            }
+        }
+        if (st) {
+#pragma omp critical
+            status = st;
+        }
+        free(B); free(Bc); free(Bi); free(Hn); free(sv); free(r); free(xc);
+    }
+    return status;
+}

@@ -78,6 +78,14 @@ int dbpo_beamform_admm_trace(const dbpo_dims* d, const float* Hd, const float* s
                              int n_tr, int j_tr, double* x_tr, double* z_tr,
                              double* lam_tr, double* w_tr);
 
+/* Centralized baselines (Table I rows ZF-DL / MMSE-UL, P594-595):
+ * MMSE-UL x = (H^H H + (N0/Es) I)^{-1} H^H y over all C clusters (N0 = 0: ZF),
+ * x_hat [N][Nsym][U];  ZF-DL x_c = H_c^H (sum_c H_c H_c^H)^{-1} s,
+ * x [C][N][Nsym][S].  Status 3 if the Gram is not HPD (rank deficiency). */
+int dbpo_mmse_centralized(const dbpo_dims* d, const float* H, const float* y, double N0, double Es,
+                          int mod, double* x_hat, uint8_t* hard);
+int dbpo_zf_centralized(const dbpo_dims* d, const float* Hd, const float* s, double* x);
+
 #ifdef __cplusplus
 }
 #endif
