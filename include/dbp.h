@@ -68,7 +68,8 @@ typedef enum { DBP_REG_MMSE = 0, DBP_REG_ZF = 1, DBP_REG_BOX = 2 } dbp_reg;
 /* Gray-mapped constellation O (P143), Es = 1; value = bits per symbol. */
 typedef enum { DBP_BPSK = 1, DBP_QPSK = 2, DBP_QAM16 = 4, DBP_QAM64 = 6 } dbp_mod;
 
-typedef enum { DBP_ALGO_ADMM_UL = 0, DBP_ALGO_CG_UL = 1, DBP_ALGO_ADMM_DL = 2 } dbp_algo;
+typedef enum { DBP_ALGO_ADMM_UL = 0, DBP_ALGO_CG_UL = 1, DBP_ALGO_ADMM_DL = 2, DBP_ALGO_MMSE_UL = 3,
+               DBP_ALGO_ZF_DL = 4 } dbp_algo;
 
 /* C = total clusters (all ranks), S = B_c antennas per cluster (P150),
  * U users, N subcarriers, N_sym symbols sharing one channel (P706-709).
@@ -167,6 +168,26 @@ dbp_status dbp_detect_cg(dbp_ctx* ctx, const dbp_dims* dims, const dbp_cf32* H,
 dbp_status dbp_beamform_admm(dbp_ctx* ctx, const dbp_dims* dims, const dbp_cf32* Hd,
                              const dbp_cf32* s, float rho, float gamma, float eps, int32_t T,
                              dbp_cf32* x, void* ws, size_t ws_bytes, void* stream);
+
+/* Centralized baselines (NEXT-3; Table I rows MMSE-UL / ZF-DL, P594-595,
+ * the comparison of P622 / P789-792): the whole array H = [H_1; ...; H_C]
+ * solved exactly per subcarrier.  Each rank forms its clusters' Gram and
+ * matched-filter sums; world > 1 adds ONE allreduce of [sum_c G_c | sum_c
+ * H_c^H y_c] (N (U(U+1)/2 + N_sym U) complex values; it is not a consensus
+ * round), then every rank solves the U x U system (DBP_ERR_NOT_HPD on a
+ * rank-deficient Gram).
+ *
+ * dbp_detect_mmse: x_hat = (H^H H + (N0/Es) I)^{-1} H^H y (P212-218);
+ *   N0 = 0 gives ZF detection.  H, y, x_hat, hard as in dbp_detect_admm.
+ * dbp_precode_zf:  x = H^H (H H^H)^{-1} s for H = [H_1^d, ..., H_C^d]
+ *   (P431), i.e. x_c = H_c^H r with r = (sum_c H_c H_c^H)^{-1} s.
+ *   Hd, s, x as in dbp_beamform_admm.
+ * Workspace: dbp_workspace_bytes with DBP_ALGO_MMSE_UL / DBP_ALGO_ZF_DL. */
+dbp_status dbp_detect_mmse(dbp_ctx* ctx, const dbp_dims* dims, const dbp_cf32* H, const dbp_cf32* y,
+                           float N0, float Es, int mod, dbp_cf32* x_hat, uint8_t* hard, void* ws,
+                           size_t ws_bytes, void* stream);
+dbp_status dbp_precode_zf(dbp_ctx* ctx, const dbp_dims* dims, const dbp_cf32* Hd, const dbp_cf32* s,
+                          dbp_cf32* x, void* ws, size_t ws_bytes, void* stream);
 
 /* Hard slicer alone (P210): bits[i] = Gray label of the nearest point of `mod`
  * to x[i] (decided in fp32, same rule as the detectors' `hard`).  Device or

@@ -214,11 +214,16 @@ static Layout layout(const Shape& sh, int algo) {
         sz[5] = vecn;                      // r
         sz[6] = vecn;                      // p
         sz[7] = (size_t)sh.N * sh.J * 4;   // rr
-    } else {
+    } else if (algo == DBP_ALGO_ADMM_DL) {
         sz[0] = P * T * 8;   // B, then B^{-1} in place (split path)
         sz[1] = vecp;        // m
         sz[2] = vecp;        // lam
         sz[3] = vecn;        // wbuf
+    } else {                 // centralized MMSE-UL / ZF-DL
+        sz[0] = P * T * 8;                               // per-pair Gram
+        sz[1] = algo == DBP_ALGO_MMSE_UL ? vecp : 0;     // per-pair matched filter
+        sz[2] = (size_t)sh.N * T * 8;                    // Gram sum (allreduced)
+        sz[3] = vecn;                                    // y^MRC sum (UL) or r (DL)
     }
     size_t o = 0;
     for (int i = 0; i < 8; ++i) { L.off[i] = o; o += al(sz[i]); }
@@ -228,7 +233,7 @@ static Layout layout(const Shape& sh, int algo) {
 
 extern "C" dbp_status dbp_workspace_bytes(const dbp_ctx* c, const dbp_dims* d, int algo, size_t* bytes) {
     if (!bytes) return fail(DBP_ERR_INVALID_ARG, "bytes is NULL");
-    if (algo < 0 || algo > 2) return fail(DBP_ERR_INVALID_ARG, "algo %d", algo);
+    if (algo < 0 || algo > 4) return fail(DBP_ERR_INVALID_ARG, "algo %d", algo);
     Shape sh;
     dbp_status st = check_dims(c, d, &sh);
     if (st) return st;
@@ -322,8 +327,8 @@ static dbp_status end_call(dbp_ctx*, Call& k, cudaStream_t st) {
     return DBP_OK;
 }
 
-static dbp_status allreduce(dbp_ctx* c, float2* buf, size_t nfloat2, cudaStream_t st) {
-    c->consensus_rounds += 1;
+static dbp_status allreduce(dbp_ctx* c, float2* buf, size_t nfloat2, cudaStream_t st, bool round = true) {
+    if (round) c->consensus_rounds += 1;
     if (c->world == 1) return DBP_OK;
     NC(ncclAllReduce(buf, buf, nfloat2 * 2, ncclFloat32, ncclSum, c->comm, st));
     c->allreduce_calls += 1;
@@ -580,6 +585,91 @@ extern "C" dbp_status dbp_beamform_admm(dbp_ctx* c, const dbp_dims* d, const dbp
         a.step = T + 1;
         KT("bf_final", launch_bf_it(L, sh.UP, a, CCH));                    // output x_c^(T) (P525)
     }
+    return end_call(c, k, s);
+}
+
+// ============================================================ centralized baselines
+extern "C" dbp_status dbp_detect_mmse(dbp_ctx* c, const dbp_dims* d, const dbp_cf32* H, const dbp_cf32* y, float N0,
+                                      float Es, int mod, dbp_cf32* x_hat, uint8_t* hard, void* ws, size_t ws_bytes,
+                                      void* stream) {
+    Shape sh;
+    dbp_status st = check_dims(c, d, &sh);
+    if (st) return st;
+    if (!H || !y || !x_hat) return fail(DBP_ERR_INVALID_ARG, "H, y and x_hat are required");
+    if (!(N0 >= 0.f) || !std::isfinite(N0) || !(Es > 0.f) || !std::isfinite(Es))
+        return fail(DBP_ERR_INVALID_ARG, "need N0 >= 0, Es > 0");
+    if (!mod_ok(mod)) return fail(DBP_ERR_INVALID_ARG, "mod %d", mod);
+    if (prelr_smem(sh.UP, sh.S, sh.U, sh.J, true) > (size_t)c->max_smem) return fail(DBP_ERR_UNSUPPORTED, "S too large for the preprocessing tile");
+    CU(cudaSetDevice(c->device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const Layout Lw = layout(sh, DBP_ALGO_MMSE_UL);
+    Call k;
+    k.io[0] = {H, nullptr, (size_t)sh.pairs() * sh.S * sh.U * 8, nullptr};
+    k.io[1] = {y, nullptr, (size_t)sh.pairs() * sh.J * sh.S * 8, nullptr};
+    k.io[2] = {nullptr, x_hat, (size_t)sh.N * sh.J * sh.U * 8, nullptr};
+    k.io[3] = {nullptr, hard, hard ? (size_t)sh.N * sh.J * sh.U : 0, nullptr};
+    k.nio = 4;
+    if ((st = begin_call(c, k, Lw, ws, ws_bytes, s))) return st;
+    LaunchCtx L{s, c->d_flag, &c->launches};
+    const float2* dH = static_cast<const float2*>(k.io[0].dev);
+    const float2* dy = static_cast<const float2*>(k.io[1].dev);
+    float2* xo = static_cast<float2*>(k.io[2].dev);
+    uint8_t* ho = static_cast<uint8_t*>(k.io[3].dev);
+    const float reg = N0 / Es;
+    if (c->world == 1 && !c->force_split && !c->no_fused && fused_ok(sh.UP, sh.C, sh.N, sh.J, sh.S, sh.U)) {
+        bool launched = false;
+        KT("fused_mmse", (launched = launch_fused_central(L, sh.UP, false, dH, dy, sh.C, sh.N, sh.S, sh.U, reg,
+                                                          modem_of(mod), xo, ho), cudaGetLastError()));
+        if (launched) return end_call(c, k, s);
+    }
+    float2* Gp = reinterpret_cast<float2*>(k.ws + Lw.off[0]);
+    float2* mf = reinterpret_cast<float2*>(k.ws + Lw.off[1]);
+    float2* Gloc = reinterpret_cast<float2*>(k.ws + Lw.off[2]);
+    float2* b = reinterpret_cast<float2*>(k.ws + Lw.off[3]);
+    KT("pre_cg", launch_prelr(L, sh.UP, 0, dH, dy, sh.S, sh.U, sh.J, sh.pairs(), 0.f, Gp, mf));
+    KT("cg_gsum", launch_cg_gsum(L, sh.UP, Gp, mf, sh.C_loc, sh.N, sh.J, Gloc, b));
+    const size_t ng = (size_t)sh.N * sh.UP * (sh.UP + 1) / 2, nb = (size_t)sh.N * sh.J * sh.UP;
+    if ((st = allreduce(c, Gloc, ng, s, false))) return st;             // gather the whole array's Gram
+    if ((st = allreduce(c, b, nb, s, false))) return st;                // and matched filter
+    KT("central_solve", launch_central_solve(L, sh.UP, false, Gloc, b, reg, sh.N, sh.J, sh.U, xo, ho, modem_of(mod)));
+    return end_call(c, k, s);
+}
+
+extern "C" dbp_status dbp_precode_zf(dbp_ctx* c, const dbp_dims* d, const dbp_cf32* Hd, const dbp_cf32* sv,
+                                     dbp_cf32* x, void* ws, size_t ws_bytes, void* stream) {
+    Shape sh;
+    dbp_status st = check_dims(c, d, &sh);
+    if (st) return st;
+    if (!Hd || !sv || !x) return fail(DBP_ERR_INVALID_ARG, "Hd, s and x are required");
+    if (prelr_smem(sh.UP, sh.S, sh.U, sh.J, false) > (size_t)c->max_smem) return fail(DBP_ERR_UNSUPPORTED, "S too large for the preprocessing tile");
+    CU(cudaSetDevice(c->device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const Layout Lw = layout(sh, DBP_ALGO_ZF_DL);
+    Call k;
+    k.io[0] = {Hd, nullptr, (size_t)sh.pairs() * sh.S * sh.U * 8, nullptr};
+    k.io[1] = {sv, nullptr, (size_t)sh.N * sh.J * sh.U * 8, nullptr};
+    k.io[2] = {nullptr, x, (size_t)sh.pairs() * sh.J * sh.S * 8, nullptr};
+    k.nio = 3;
+    if ((st = begin_call(c, k, Lw, ws, ws_bytes, s))) return st;
+    LaunchCtx L{s, c->d_flag, &c->launches};
+    const float2* dH = static_cast<const float2*>(k.io[0].dev);
+    const float2* ds = static_cast<const float2*>(k.io[1].dev);
+    float2* xo = static_cast<float2*>(k.io[2].dev);
+    if (c->world == 1 && !c->force_split && !c->no_fused && fused_ok(sh.UP, sh.C, sh.N, sh.J, sh.S, sh.U)) {
+        bool launched = false;
+        KT("fused_zf", (launched = launch_fused_central(L, sh.UP, true, dH, ds, sh.C, sh.N, sh.S, sh.U, 0.f,
+                                                        modem_of(DBP_QPSK), xo, nullptr), cudaGetLastError()));
+        if (launched) return end_call(c, k, s);
+    }
+    float2* Gp = reinterpret_cast<float2*>(k.ws + Lw.off[0]);
+    float2* Gloc = reinterpret_cast<float2*>(k.ws + Lw.off[2]);
+    float2* r = reinterpret_cast<float2*>(k.ws + Lw.off[3]);
+    KT("pre_dl", launch_prelr(L, sh.UP, 3, dH, nullptr, sh.S, sh.U, sh.J, sh.pairs(), 0.f, Gp, nullptr));
+    KT("cg_gsum", launch_cg_gsum(L, sh.UP, Gp, nullptr, sh.C_loc, sh.N, 0, Gloc, nullptr));
+    if ((st = allreduce(c, Gloc, (size_t)sh.N * sh.UP * (sh.UP + 1) / 2, s, false))) return st;
+    KT("central_solve", launch_central_solve(L, sh.UP, true, Gloc, ds, 0.f, sh.N, sh.J, sh.U, r, nullptr,
+                                             modem_of(DBP_QPSK)));
+    KT("zf_out", launch_zf_out(L, sh.UP, dH, r, sh.N, sh.J, sh.U, sh.S, sh.pairs(), xo));
     return end_call(c, k, s);
 }
 

@@ -41,7 +41,8 @@ namespace dbp {
 template <int UP, int SOLVER>
 struct FZ {
     using F = Fold<UP>;
-    static constexpr bool DL = SOLVER == 2;
+    static constexpr bool DL = SOLVER == 2 || SOLVER == 4;
+    static constexpr bool SUMS = SOLVER == 0 || SOLVER == 3 || SOLVER == 4;   // cluster-summed Gram
     static constexpr bool MF = !DL;
     using G = FoldStage<UP, DL, MF>;
     static constexpr int WARPS = 4;
@@ -56,7 +57,7 @@ struct FZ {
     // CTA-shared: per-warp consensus partials [WARPS][UP] + per-subcarrier sums [4][UP];
     // CG: per-warp Gram partials [WARPS][TRI] + per-subcarrier Gram [4][TRI]
     static constexpr int CBUF = WARPS * UP * 8 + WARPS * UP * 8;
-    static constexpr int GBUF = SOLVER == 0 ? 2 * WARPS * F::TRI * 8 : 0;
+    static constexpr int GBUF = SUMS ? 2 * WARPS * F::TRI * 8 : 0;
     static constexpr size_t SMEM = 128 + (size_t)WARPS * WREG + CBUF + GBUF;
 };
 
@@ -94,7 +95,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     float2* Wp = reinterpret_cast<float2*>(smem_raw + 128 + (size_t)Z::WARPS * Z::WREG);   // [4 warps][UP]
     float2* Sv = Wp + Z::WARPS * UP;                                                       // [4 subc.][UP]
     float2* Gp = Sv + Z::WARPS * UP;                                                       // CG: [4 warps][TRI]
-    float2* Gs = Gp + (SOLVER == 0 ? Z::WARPS * TRI : 0);                                  // CG queue: [4][TRI]
+    float2* Gs = Gp + (Z::SUMS ? Z::WARPS * TRI : 0);                                      // queue: [4][TRI]
 
     int row[R];
 #pragma unroll
@@ -146,6 +147,26 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
         if (++st == NST) { st = 0; phase ^= 1u; }
     };
 
+    // DL output pass: x_c[s] = sum_u conj(H_us) r_u, re-streaming H_c through the ring (its second
+    // pass, L2-resident); lane l takes antennas l, l+L, ... of each stage
+    auto dl_output = [&](const float2 (&r)[UP], int n, bool valid) {
+        using GD = FoldStage<UP, true, false>;
+        float2* xo = a.x + ((size_t)c * a.N + n) * a.S;
+        for (int ch = 0; ch < nch; ++ch) {
+            mbar_wait(&bar[st], phase);
+            const float2* hq = reinterpret_cast<const float2*>(wbase + st * G::STG) + q * GD::NL * GD::HL;
+#pragma unroll
+            for (int sl = l; sl < SC; sl += L) {
+                float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int u = 0; u < UP; ++u) c_fmac(acc, hq[u * GD::HL + sl], r[u]);
+                const int s = ch * SC + sl;
+                if (valid && s < a.S) xo[s] = acc;
+            }
+            next_stage();
+        }
+    };
+
     for (int it = 0; it < nitems; ++it) {
         const int n = (blockIdx.x + it * gridDim.x) * NPC + j;
         const bool valid = n < a.N && c < a.C;
@@ -167,8 +188,8 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
         float dg[R];
         fold_diag<UP>(A, row, a.delta, dg);
 
-        if constexpr (SOLVER == 0) {
-            // ---------------------------------------------- CG: cluster sums, then CG per subcarrier
+        if constexpr (Z::SUMS) {
+            // ---------------------------------------------- cluster sums (CG, MMSE-UL, ZF-DL)
             // sum over the warp's pairs (xor butterfly over the pair bits of the lane), then
             // over the subcarrier's WPS warps in fixed order: G = sum_c G_c, y^MRC = sum_c H_c^H y_c
 #pragma unroll
@@ -212,39 +233,82 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
             if (tid < NPC) qsub[qn + tid] = (blockIdx.x + it * gridDim.x) * NPC + tid;
             qn += NPC;
             __syncthreads();
-            if (qn < Z::WARPS && it + 1 < nitems) continue;
-            // the CG iterations of up to 4 queued subcarriers, one per warp (all warps busy)
-            if (warp < qn) {
-                const int nn = qsub[warp];
+            // exact solve of queue slot w on the warp's UP-lane groups (lane-row Gauss-Jordan,
+            // dbp_lanerow.cuh): returns ((G_w + delta I)^{-1} rhs)_u for u = lane % UP
+            auto solve = [&](int w, float delta, float2 rhs_u, bool live) {
                 const int u = lane % UP;
-                const float2* Gj = Gs + warp * TRI;
-                float2 grow[UP];                        // row u of G in registers
+                const float2* Gj = Gs + w * TRI;
+                float2 grow[UP];
 #pragma unroll
-                for (int jc = 0; jc < UP; ++jc)
+                for (int jc = 0; jc < UP; ++jc) {
                     grow[jc] = jc <= u ? Gj[(u * (u + 1)) / 2 + jc] : c_conj(Gj[(jc * (jc + 1)) / 2 + u]);
+                    // + delta on the diagonal, + 1 for padded users (u >= U): the padding stays decoupled
+                    // and exact at delta = 0 (ZF); (jc == u) as a bit test, without local memory
+                    grow[jc].x += ((1u << jc) >> u) & 1u ? delta + (u >= a.U ? 1.f : 0.f) : 0.f;
+                }
                 float2* P = pl - q * (UP + 2) + (lane / UP) * (UP + 2);       // a per-group line
-                float2 r = Sv[warp * UP + u];           // line 6: r = y^MRC, p = r, x = 0
-                float2 p = r, x = make_float2(0.f, 0.f);
-                float rr = group_sum<UP>(c_norm2(r));
-                for (int t = 0; t < a.T; ++t) {
+                const bool ok = gj_invert<UP>(grow, P, u);
+                if (!ok && live) atomicOr(a.flag, 1);        // padding subcarriers (n >= N) have G = 0
+                return row_apply<UP>(grow, P, u, rhs_u);
+            };
+            if constexpr (SOLVER == 4) {
+                // ZF-DL: r = (sum_c H_c H_c^H)^{-1} s per subcarrier, then x_c = H_c^H r (P431)
+                if (warp < NPC) {
+                    const int nn = (blockIdx.x + it * gridDim.x) * NPC + warp;
+                    const int u = lane % UP;
+                    const float2 sv = (u < a.U && nn < a.N) ? a.s[(size_t)nn * a.U + u] : make_float2(0.f, 0.f);
+                    const float2 r = solve(warp, 0.f, sv, nn < a.N);
                     __syncwarp();
-                    P[u] = p;
-                    __syncwarp();
-                    float2 pv[UP];
-                    read_vec<UP>(P, pv);
-                    float2 w = make_float2(0.f, 0.f);                            // lines 9-11: w = G p
+                    if (lane < UP) Sv[warp * UP + u] = r;
+                }
+                qn = 0;
+                __syncthreads();
+                float2 r[UP];
+                read_vec<UP>(Sv + j * UP, r);
+                dl_output(r, n, valid);
+                __syncthreads();                        // Sv / Gs reused by the next item
+                continue;
+            } else {
+                if (qn < Z::WARPS && it + 1 < nitems) continue;
+                // up to 4 queued subcarriers, one per warp (all warps busy)
+                if (warp < qn) {
+                    const int nn = qsub[warp];
+                    const int u = lane % UP;
+                    float2 x;
+                    if constexpr (SOLVER == 3) {
+                        x = solve(warp, a.rho, Sv[warp * UP + u], nn < a.N); // (G + N0/Es I)^{-1} y^MRC
+                    } else {
+                        const float2* Gj = Gs + warp * TRI;
+                        float2 grow[UP];                        // row u of G in registers
 #pragma unroll
-                    for (int jc = 0; jc < UP; ++jc) c_fma(w, grow[jc], pv[jc]);
-                    cg_update<UP>(x, r, p, rr, w, a.rho);                        // lines 13-18
+                        for (int jc = 0; jc < UP; ++jc)
+                            grow[jc] = jc <= u ? Gj[(u * (u + 1)) / 2 + jc] : c_conj(Gj[(jc * (jc + 1)) / 2 + u]);
+                        float2* P = pl - q * (UP + 2) + (lane / UP) * (UP + 2);       // a per-group line
+                        float2 r = Sv[warp * UP + u];           // line 6: r = y^MRC, p = r, x = 0
+                        float2 p = r;
+                        x = make_float2(0.f, 0.f);
+                        float rr = group_sum<UP>(c_norm2(r));
+                        for (int t = 0; t < a.T; ++t) {
+                            __syncwarp();
+                            P[u] = p;
+                            __syncwarp();
+                            float2 pv[UP];
+                            read_vec<UP>(P, pv);
+                            float2 w = make_float2(0.f, 0.f);                            // lines 9-11: w = G p
+#pragma unroll
+                            for (int jc = 0; jc < UP; ++jc) c_fma(w, grow[jc], pv[jc]);
+                            cg_update<UP>(x, r, p, rr, w, a.rho);                        // lines 13-18
+                        }
+                    }
+                    if (lane < UP && u < a.U && nn < a.N) {
+                        a.s_hat[(size_t)nn * a.U + u] = x;
+                        if (a.hard) a.hard[(size_t)nn * a.U + u] = slice_bits(x, a.md);
+                    }
                 }
-                if (lane < UP && u < a.U && nn < a.N) {
-                    a.s_hat[(size_t)nn * a.U + u] = x;
-                    if (a.hard) a.hard[(size_t)nn * a.U + u] = slice_bits(x, a.md);
-                }
+                qn = 0;
+                __syncthreads();                        // queue slots reused
+                continue;
             }
-            qn = 0;
-            __syncthreads();                            // queue slots reused
-            continue;
         }
 
         // ------------------------------------------------ B^{-1} (+ y^reg) by the Hermitian sweep
@@ -351,22 +415,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
             __syncwarp();
             float2 r[UP];
             read_vec<UP>(pl, r);
-            // output pass: x_c[s] = sum_u conj(H_us) r_u, lane l takes antennas l, l+L, ... of each stage
-            using GD = FoldStage<UP, true, false>;
-            float2* xo = a.x + ((size_t)c * a.N + n) * a.S;
-            for (int ch = 0; ch < nch; ++ch) {
-                mbar_wait(&bar[st], phase);
-                const float2* hq = reinterpret_cast<const float2*>(wbase + st * G::STG) + q * GD::NL * GD::HL;
-#pragma unroll
-                for (int sl = l; sl < SC; sl += L) {
-                    float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-                    for (int u = 0; u < UP; ++u) c_fmac(acc, hq[u * GD::HL + sl], r[u]);
-                    const int s = ch * SC + sl;
-                    if (valid && s < a.S) xo[s] = acc;
-                }
-                next_stage();
-            }
+            dl_output(r, n, valid);
         }
     }
 }
@@ -379,7 +428,7 @@ static bool launch_fz_t(const LaunchCtx& L, const float2* H, const float2* y, Fu
     using F = Fold<UP>;
     CUtensorMap tmH{}, tmY{};
     // H: UL [C][N][S][U] -> dims (U, S, N, C); DL [C][N][U][S] -> dims (S, U, N, C); y [C][N][1][S]
-    if (SOLVER != 2) {
+    if (!Z::DL) {
         if (!make_map4(&tmH, H, a.U, a.S, a.N, a.C, UP + 2, F::SC, 1, F::PW)) return false;
         if (!make_map4(&tmY, y, a.S, 1, a.N, a.C, F::SC, 1, 1, F::PW)) return false;
     } else {
@@ -452,6 +501,24 @@ bool launch_fused_dl(const LaunchCtx& L, int UP, const float2* Hd, const float2*
         case 4: return launch_fz_t<4, 2>(L, Hd, nullptr, a);
         case 8: return launch_fz_t<8, 2>(L, Hd, nullptr, a);
         case 16: return launch_fz_t<16, 2>(L, Hd, nullptr, a);
+        default: return false;
+    }
+}
+
+// Centralized baselines (Table I rows MMSE-UL / ZF-DL): cluster-summed Gram + exact solve.
+bool launch_fused_central(const LaunchCtx& L, int UP, bool dl, const float2* H, const float2* ys, int C, int N, int S,
+                          int U, float reg, Modem md, float2* out, uint8_t* hard) {
+    if (!fused_ok(UP, C, N, 1, S, U)) return false;
+    FuArgs a{};
+    a.S = S; a.U = U; a.N = N; a.C = C; a.T = 1;
+    a.rho = reg; a.gamma = 1.f; a.delta = 0.f;
+    a.md = md; a.flag = L.flag;
+    if (dl) { a.s = ys; a.x = out; } else { a.s_hat = out; a.hard = hard; }
+    fz_shape(UP, C, a);
+    switch (UP) {
+        case 4: return dl ? launch_fz_t<4, 4>(L, H, nullptr, a) : launch_fz_t<4, 3>(L, H, ys, a);
+        case 8: return dl ? launch_fz_t<8, 4>(L, H, nullptr, a) : launch_fz_t<8, 3>(L, H, ys, a);
+        case 16: return dl ? launch_fz_t<16, 4>(L, H, nullptr, a) : launch_fz_t<16, 3>(L, H, ys, a);
         default: return false;
     }
 }

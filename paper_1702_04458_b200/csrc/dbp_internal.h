@@ -55,6 +55,8 @@ bool fused_ok(int UP, int C, int N, int J, int S, int U);
 bool launch_fused_ul(const LaunchCtx& L, int UP, bool cg, const float2* H, const float2* y, int C, int N, int S, int U,
                      int T, float rho, float gamma, float N0, float Es, Prox px, Modem md, float2* s_hat,
                      uint8_t* hard);
+bool launch_fused_central(const LaunchCtx& L, int UP, bool dl, const float2* H, const float2* ys, int C, int N, int S,
+                          int U, float reg, Modem md, float2* out, uint8_t* hard);
 bool launch_fused_dl(const LaunchCtx& L, int UP, const float2* Hd, const float2* s, int C, int N, int S, int U, int T,
                      float rho, float gamma, float a0, float2* x);
 size_t prelr_smem(int UP, int S, int U, int J, bool ul);
@@ -111,6 +113,10 @@ void split_cfg(int UP, int C_loc, int N, int J, int* NT, int* CCH);
 cudaError_t launch_admm_gj(const LaunchCtx& L, int UP, UlArgs a);
 cudaError_t launch_admm_it(const LaunchCtx& L, int UP, UlArgs a, int CCH);
 cudaError_t launch_bf_gj(const LaunchCtx& L, int UP, DlArgs a);
+cudaError_t launch_central_solve(const LaunchCtx& L, int UP, bool dl, const float2* Gloc, const float2* rhs, float delta,
+                                 int N, int J, int U, float2* out, uint8_t* hard, Modem md);
+cudaError_t launch_zf_out(const LaunchCtx& L, int UP, const float2* Hd, const float2* r, int N, int J, int U, int S,
+                          long npairs, float2* x);
 cudaError_t launch_bf_it(const LaunchCtx& L, int UP, DlArgs a, int CCH);
 
 }  // namespace dbp

@@ -288,6 +288,58 @@ __global__ void __launch_bounds__(512) k_bf_it(DlArgs a, int CCH) {
         if (n0 + e / (J * UP) < a.N) a.wbuf[(size_t)n0 * J * UP + e] = Acc[e];
 }
 
+// ============================================================ centralized baselines
+
+// Per subcarrier n: (G_n + delta I) v = rhs_nj for every symbol j by a lane-row
+// Gauss-Jordan inverse (UP lanes per subcarrier).  UL (MMSE/ZF detection):
+// rhs = wbuf [N][J][UP] (allreduced y^MRC), writes x_hat/hard [N][J][U].
+// DL (ZF precoding): rhs = s [N][J][U], writes r [N][J][UP] for k_zf_out.
+template <int UP, bool DL>
+__global__ void __launch_bounds__(256) k_central_solve(const float2* __restrict__ Gloc, const float2* __restrict__ rhs,
+                                                       float delta, int N, int J, int U, float2* __restrict__ out,
+                                                       uint8_t* __restrict__ hard, Modem md, int* flag) {
+    __shared__ __align__(16) float2 sbuf[256 / UP][UP];
+    const int g = threadIdx.x / UP, i = threadIdx.x % UP;
+    const long n = (long)blockIdx.x * (256 / UP) + g;
+    const bool valid = n < N;
+    const long nn = valid ? n : N - 1;
+    float2 R[UP];
+    load_herm_row<UP>(Gloc + (size_t)nn * tri(UP), i, R);
+#pragma unroll
+    for (int jc = 0; jc < UP; ++jc)              // + delta I, + 1 on padded users (exact, decoupled)
+        R[jc].x += ((1u << jc) >> i) & 1u ? delta + (i >= U ? 1.f : 0.f) : 0.f;
+    const bool ok = gj_invert<UP>(R, sbuf[g], i);
+    if (!ok && valid) atomicOr(flag, 1);
+    for (int jj = 0; jj < J; ++jj) {
+        float2 b;
+        if (DL) b = i < U ? rhs[((size_t)nn * J + jj) * U + i] : make_float2(0.f, 0.f);
+        else b = rhs[((size_t)nn * J + jj) * UP + i];
+        const float2 v = row_apply<UP>(R, sbuf[g], i, b);
+        if (!valid) continue;
+        if (DL) {
+            out[((size_t)n * J + jj) * UP + i] = v;
+        } else if (i < U) {
+            out[((size_t)n * J + jj) * U + i] = v;
+            if (hard) hard[((size_t)n * J + jj) * U + i] = slice_bits(v, md);
+        }
+    }
+}
+
+// ZF-DL output per pair: x_c = H_c^H r_n (P431), r from k_central_solve.
+template <int UP>
+__global__ void __launch_bounds__(256) k_zf_out(const float2* __restrict__ Hd, const float2* __restrict__ r, int N,
+                                                int J, int U, int S, long npairs, float2* __restrict__ x) {
+    __shared__ __align__(16) float2 sbuf[256 / UP][UP];
+    const int g = threadIdx.x / UP, i = threadIdx.x % UP;
+    const long p = (long)blockIdx.x * (256 / UP) + g;
+    const bool valid = p < npairs;
+    const long pp = valid ? p : npairs - 1;
+    const long n = pp % N;
+    for (int jj = 0; jj < J; ++jj)
+        bf_output<UP>(Hd + (size_t)pp * U * S, sbuf[g], i, r[((size_t)n * J + jj) * UP + i], U, S,
+                      x + ((size_t)pp * J + jj) * S, valid);
+}
+
 // ============================================================ launchers
 static int cdiv_i(long x, long y) { return (int)((x + y - 1) / y); }
 
@@ -340,6 +392,24 @@ cudaError_t launch_bf_gj(const LaunchCtx& L, int UP, DlArgs a) {
     const size_t smem = iter_smem(UP, a.NT, a.C_loc);
     DBP_DISPATCH_UP(UP, big_smem(k_bf_gj<UPc>, smem);
                     k_bf_gj<UPc><<<cdiv_i(a.N, a.NT), a.NT * a.C_loc * UPc, smem, L.stream>>>(a));
+    L.count(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_central_solve(const LaunchCtx& L, int UP, bool dl, const float2* Gloc, const float2* rhs, float delta,
+                                 int N, int J, int U, float2* out, uint8_t* hard, Modem md) {
+    DBP_DISPATCH_UP(UP,
+        if (dl) k_central_solve<UPc, true><<<cdiv_i(N, 256 / UPc), 256, 0, L.stream>>>(Gloc, rhs, delta, N, J, U, out,
+                                                                                    hard, md, L.flag);
+        else k_central_solve<UPc, false><<<cdiv_i(N, 256 / UPc), 256, 0, L.stream>>>(Gloc, rhs, delta, N, J, U, out,
+                                                                                   hard, md, L.flag));
+    L.count(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_zf_out(const LaunchCtx& L, int UP, const float2* Hd, const float2* r, int N, int J, int U, int S,
+                          long npairs, float2* x) {
+    DBP_DISPATCH_UP(UP, k_zf_out<UPc><<<cdiv_i(npairs, 256 / UPc), 256, 0, L.stream>>>(Hd, r, N, J, U, S, npairs, x));
     L.count(1);
     return cudaGetLastError();
 }

@@ -151,8 +151,10 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
         if constexpr (!INV) {
             if (valid) {
                 fold_store<UP>(a.Gout + (size_t)p * P::TRI, A, row);
+                if (MF) {
 #pragma unroll
-                for (int m = 0; m < R; ++m) a.vout[(size_t)p * UP + row[m]] = upk2(E[m]);
+                    for (int m = 0; m < R; ++m) a.vout[(size_t)p * UP + row[m]] = upk2(E[m]);
+                }
             }
             continue;
         }
@@ -218,13 +220,14 @@ size_t prefold_smem(int UP, bool dl, int mode) {
 // uses the lane-row kernel (dbp_prelr.cu).
 bool launch_prefold(const LaunchCtx& L, int UP, int mode, const float2* H, const float2* y, int S, int U, int J,
                     long npairs, float delta, float2* Gout, float2* vout) {
-    if (UP > 16 || (mode != 2 && J != 1) || npairs <= 0 || npairs > (1L << 30)) return false;
+    if (UP > 16 || (mode <= 1 && J != 1) || npairs <= 0 || npairs > (1L << 30)) return false;
     PfArgs a{S, U, npairs, delta, Gout, vout, L.flag};
     switch (UP) {
 #define DBP_PF_CASE(UPc)                                                  \
     case UPc:                                                             \
         if (mode == 0) return launch_pf_t<UPc, false, 0>(L, H, y, a);     \
         if (mode == 1) return launch_pf_t<UPc, false, 1>(L, H, y, a);     \
+        if (mode == 3) return launch_pf_t<UPc, true, 0>(L, H, y, a);      \
         return launch_pf_t<UPc, true, 2>(L, H, y, a);
         DBP_PF_CASE(4)
         DBP_PF_CASE(8)

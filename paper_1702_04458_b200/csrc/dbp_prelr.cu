@@ -183,7 +183,7 @@ k_prelr(const __grid_constant__ CUtensorMap tmH, LrArgs a) {
             }
         }
         // N_sym > 1: the matched filters of all symbols, before the stage is released
-        if (MODE != 2 && J > 1) {
+        if (UL && MODE != 2 && J > 1) {
             for (int jj = 0; jj < J; ++jj) {
                 float2 m = make_float2(0.f, 0.f);
                 if (FULL || i < U)
@@ -210,7 +210,7 @@ k_prelr(const __grid_constant__ CUtensorMap tmH, LrArgs a) {
         if (MODE == 0) {
             if (valid) {
                 store_herm_row<UP>(a.Gout + (size_t)p * TRI, i, g);
-                if (J == 1) a.vout[(size_t)p * UP + i] = mf;
+                if (UL && J == 1) a.vout[(size_t)p * UP + i] = mf;
             }
             continue;
         }
@@ -261,7 +261,8 @@ size_t prelr_smem(int UP, int S, int U, int J, bool ul) {
     return r;
 }
 
-// mode: 0 = Gram + H^H y (CG), 1 = inverse + y^reg (ADMM-UL), 2 = inverse (ADMM-DL, H = H^d)
+// mode: 0 = Gram + H^H y (CG), 1 = inverse + y^reg (ADMM-UL), 2 = inverse (ADMM-DL, H = H^d),
+//       3 = Gram only (ZF-DL, H = H^d)
 cudaError_t launch_prelr(const LaunchCtx& L, int UP, int mode, const float2* H, const float2* y, int S, int U, int J,
                          long npairs, float delta, float2* Gout, float2* vout) {
     if (npairs <= 0) return cudaSuccess;
@@ -271,6 +272,7 @@ cudaError_t launch_prelr(const LaunchCtx& L, int UP, int mode, const float2* H, 
     DBP_DISPATCH_UP(UP,
         if (mode == 0) e = (launch_lr_t<UPc, false, 0>(L, a));
         else if (mode == 1) e = (launch_lr_t<UPc, false, 1>(L, a));
+        else if (mode == 3) e = (launch_lr_t<UPc, true, 0>(L, a));
         else e = (launch_lr_t<UPc, true, 2>(L, a)));
     return e;
 }

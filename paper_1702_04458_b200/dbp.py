@@ -20,14 +20,15 @@ STATUS = {0: "DBP_OK", 1: "DBP_ERR_INVALID_ARG", 2: "DBP_ERR_UNSUPPORTED", 3: "D
           4: "DBP_ERR_CUDA", 5: "DBP_ERR_NCCL", 6: "DBP_ERR_WORKSPACE"}
 REG = {"mmse": 0, "zf": 1, "box": 2}
 MOD = {"bpsk": 1, "qpsk": 2, "qam16": 4, "qam64": 6}
-ALGO = {"admm_ul": 0, "cg_ul": 1, "admm_dl": 2}
+ALGO = {"admm_ul": 0, "cg_ul": 1, "admm_dl": 2, "mmse_ul": 3, "zf_dl": 4}
 OPT_FORCE_SPLIT = 1
 OPT_KERNEL_TIMING = 2
 OPT_NO_FUSED = 3
 
 EXPORTS = ["dbp_get_unique_id", "dbp_ctx_create", "dbp_ctx_destroy", "dbp_set_option", "dbp_get_stats",
            "dbp_last_error", "dbp_workspace_bytes", "dbp_detect_admm", "dbp_detect_cg",
-           "dbp_beamform_admm", "dbp_slice", "dbp_sync", "dbp_get_kernel_times", "dbp_complexity"]
+           "dbp_beamform_admm", "dbp_slice", "dbp_sync", "dbp_get_kernel_times", "dbp_complexity",
+           "dbp_detect_mmse", "dbp_precode_zf"]
 CPLX_ALGO = {"admm_dl": 0, "admm_ul": 1, "cg_ul": 2, "zf_dl": 3, "mmse_ul": 4}
 CPLX_MODE = {"SxS": 0, "UxU": 1, None: 1}
 CPLX_METRIC = {"TM": 0, "AR": 1}
@@ -80,6 +81,8 @@ def load() -> ctypes.CDLL:
         "dbp_sync": [P, P],
         "dbp_get_kernel_times": [P, P, I, P, I],
         "dbp_complexity": [I, I, I, I64, I64, I64, I64, P],
+        "dbp_detect_mmse": [P, P, P, P, F, F, I, P, P, P, S, P],
+        "dbp_precode_zf": [P, P, P, P, P, P, S, P],
     }
     for name, args in sigs.items():
         fn = getattr(lib, name)
@@ -247,6 +250,37 @@ def beamform_admm(ctx: Context, Hd, s, *, rho=1.0, gamma=1.0, eps=0.0, T=5, x=No
     wsb = 0 if ws is None else (ws.numel() * ws.element_size() if _is_torch(ws) else ws.nbytes)
     _check(load().dbp_beamform_admm(ctx._h, ctypes.byref(d), _ptr(Hd), _ptr(s), rho, gamma, eps, T, _ptr(x),
                                     _ptr(ws), wsb, _stream(stream, Hd)))
+    return x
+
+
+def detect_mmse(ctx: Context, H, y, *, N0=0.0, Es=1.0, mod="qam64", x_hat=None, hard=None, want_hard=True,
+                ws=None, stream=None):
+    """Centralized MMSE-UL detection (N0 = 0: ZF) over all clusters.  -> (x_hat [N][N_sym][U], hard)."""
+    C_loc, N, S, U = H.shape
+    J = y.shape[2]
+    if x_hat is None:
+        x_hat = _empty_like_io(H, (N, J, U), "c")
+    if hard is None and want_hard:
+        hard = _empty_like_io(H, (N, J, U), "u")
+    _need_contig(H, y, x_hat, hard)
+    d = Dims(C_loc * ctx.world, S, U, N, J)
+    wsb = 0 if ws is None else (ws.numel() * ws.element_size() if _is_torch(ws) else ws.nbytes)
+    _check(load().dbp_detect_mmse(ctx._h, ctypes.byref(d), _ptr(H), _ptr(y), N0, Es, MOD[mod], _ptr(x_hat),
+                                  _ptr(hard), _ptr(ws), wsb, _stream(stream, H)))
+    return x_hat, hard
+
+
+def precode_zf(ctx: Context, Hd, s, *, x=None, ws=None, stream=None):
+    """Centralized ZF-DL precoding x_c = H_c^H (sum_c H_c H_c^H)^{-1} s -> x [C_loc][N][N_sym][S]."""
+    C_loc, N, U, S = Hd.shape
+    J = s.shape[1]
+    if x is None:
+        x = _empty_like_io(Hd, (C_loc, N, J, S), "c")
+    _need_contig(Hd, s, x)
+    d = Dims(C_loc * ctx.world, S, U, N, J)
+    wsb = 0 if ws is None else (ws.numel() * ws.element_size() if _is_torch(ws) else ws.nbytes)
+    _check(load().dbp_precode_zf(ctx._h, ctypes.byref(d), _ptr(Hd), _ptr(s), _ptr(x), _ptr(ws), wsb,
+                                 _stream(stream, Hd)))
     return x
 
 

@@ -354,3 +354,84 @@ def test_deterministic(env, path):
     c1 = run_cg(env, synth.CONFIGS["C"].scaled(N=16), path)[0]
     c2 = run_cg(env, synth.CONFIGS["C"].scaled(N=16), path)[0]
     assert np.array_equal(c1, c2)
+
+
+# ------------------------------------------------------- centralized baselines (NEXT-3)
+CENTRAL_UL = [
+    synth.CONFIGS["C"].scaled(N=40),
+    synth.CONFIGS["B"].scaled(N=21),
+    synth.CONFIGS["A"],
+    synth.CONFIGS["E"].scaled(N=4, C=8),                      # U = 32: two-kernel path
+    synth.Config("odd", "admm_ul", C=3, S=7, U=5, N=11, mod="qam16", snr_db=20),
+    synth.Config("nsym", "admm_ul", C=2, S=16, U=8, N=10, N_sym=3, mod="qam64", snr_db=30),
+    synth.Config("c20", "admm_ul", C=20, S=12, U=14, N=13, mod="qam16", snr_db=22),
+]
+
+
+@pytest.mark.parametrize("cfg", CENTRAL_UL, ids=lambda c: f"{c.name}-C{c.C}S{c.S}U{c.U}N{c.N}J{c.N_sym}")
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("zf", [False, True], ids=["mmse", "zf"])
+def test_mmse_centralized_parity(env, cfg, path, zf):
+    dbp, ctx, oracle, torch = env
+    H, y, _ = synth.uplink_frame(cfg)
+    N0 = 0.0 if zf else cfg.N0
+    set_path(env, path)
+    x, hard = dbp.detect_mmse(ctx, torch.from_numpy(H).cuda(), torch.from_numpy(y).cuda(), N0=N0, mod=cfg.mod)
+    ctx.sync()
+    set_path(env, "fused")
+    x_ref, hard_ref = oracle.mmse_centralized(H, y, N0=N0, mod=cfg.mod)
+    x = x.cpu().numpy()
+    assert rel(x, x_ref) < TOL
+    check_hard(hard.cpu().numpy(), hard_ref, x_ref, cfg.mod)
+
+
+CENTRAL_DL = [
+    synth.CONFIGS["D"].scaled(N=40),
+    synth.CONFIGS["D"].scaled(N=9, C=4),
+    synth.CONFIGS["E"].scaled(N=4, C=8, algo="admm_dl"),
+    synth.Config("odd", "admm_dl", C=3, S=7, U=5, N=11, mod="qam16"),
+    synth.Config("nsym", "admm_dl", C=2, S=16, U=8, N=10, N_sym=3, mod="qam64"),
+    synth.Config("c5", "admm_dl", C=5, S=8, U=6, N=10, mod="qpsk"),
+]
+
+
+@pytest.mark.parametrize("cfg", CENTRAL_DL, ids=lambda c: f"{c.name}-C{c.C}S{c.S}U{c.U}N{c.N}J{c.N_sym}")
+@pytest.mark.parametrize("path", PATHS)
+def test_zf_precoder_parity(env, cfg, path):
+    dbp, ctx, oracle, torch = env
+    Hd, s = synth.downlink_frame(cfg)
+    set_path(env, path)
+    x = dbp.precode_zf(ctx, torch.from_numpy(Hd).cuda(), torch.from_numpy(s).cuda())
+    ctx.sync()
+    set_path(env, "fused")
+    assert rel(x.cpu().numpy(), oracle.zf_centralized(Hd, s)) < TOL
+
+
+def test_centralized_full_size_sampled(env):
+    """Config C/D shapes at full size (the bench launch configuration), 16 sampled subcarriers."""
+    dbp, ctx, oracle, torch = env
+    rng = np.random.default_rng(11)
+    cfg = synth.CONFIGS["C"]
+    ns = np.sort(rng.choice(cfg.N, 16, replace=False))
+    H, y, _ = synth.uplink_frame(cfg)
+    x, hard = dbp.detect_mmse(ctx, torch.from_numpy(H).cuda(), torch.from_numpy(y).cuda(), N0=cfg.N0, mod=cfg.mod)
+    ctx.sync()
+    x_ref, hard_ref = oracle.mmse_centralized(H[:, ns], y[:, ns], N0=cfg.N0, mod=cfg.mod)
+    assert rel(x.cpu().numpy()[ns], x_ref) < TOL
+    check_hard(hard.cpu().numpy()[ns], hard_ref, x_ref, cfg.mod)
+    dcfg = synth.CONFIGS["D"]
+    Hd, s = synth.downlink_frame(dcfg)
+    xz = dbp.precode_zf(ctx, torch.from_numpy(Hd).cuda(), torch.from_numpy(s).cuda())
+    ctx.sync()
+    assert rel(xz.cpu().numpy()[:, ns], oracle.zf_centralized(Hd[:, ns], s[ns])) < TOL
+
+
+def test_centralized_rank_deficient_flags(env):
+    dbp, ctx, oracle, torch = env
+    H = torch.zeros((2, 3, 4, 8), dtype=torch.complex64, device="cuda")      # S*C = 8 antennas, U = 8: Gram = 0
+    y = torch.zeros((2, 3, 1, 4), dtype=torch.complex64, device="cuda")
+    dbp.detect_mmse(ctx, H, y, N0=0.0, mod="qpsk")
+    with pytest.raises(dbp.DbpError) as ei:
+        ctx.sync()
+    assert ei.value.status == 3
+    ctx.sync()
