@@ -331,6 +331,7 @@ def main():
     K1 = min(args.steps, 200)
     per1 = timed_region(K1, 1, order)
 
+
     def mx(v):
         if world == 1:
             return np.asarray(v, dtype=np.float64)
@@ -340,6 +341,33 @@ def main():
 
     per = mx(per)
     per1 = mx(per1)
+
+    # centralized baselines (Table I rows MMSE-UL / ZF-DL, the paper's comparison P789-792,
+    # P810): same frames, timed alone; context only, not part of the step
+    xb = torch.empty_like(s_hat)
+    hb = torch.empty_like(hard)
+    xz = torch.empty_like(xbf)
+    wsb = {a: torch.empty(max(1, ctx.workspace_bytes(UL.C, UL.S, UL.U, UL.N, UL.N_sym, a)), dtype=torch.uint8,
+                          device=dev) for a in ("mmse_ul", "zf_dl")}
+    base_fns = {"mmse_ul": lambda: dbp.detect_mmse(ctx, Hg, yg, N0=UL.N0, mod=UL.mod, x_hat=xb, hard=hb,
+                                                   ws=wsb["mmse_ul"]),
+                "zf_dl": lambda: dbp.precode_zf(ctx, Hdg, sg, x=xz, ws=wsb["zf_dl"])}
+    baselines = {}
+    for nm, fn in base_fns.items():
+        for _ in range(3):
+            fn()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K1)]
+        barrier()
+        torch.cuda.synchronize()
+        for e0, e1 in evs:
+            flush_l2(0)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        ms = float(mx([sum(e0.elapsed_time(e1) for e0, e1 in evs) / K1])[0])
+        bits = UL.bits_per_frame if nm == "mmse_ul" else DL.bits_per_frame
+        baselines[nm] = {"ms": ms, "gbps": bits / (ms * 1e-3) / 1e9}
     total_ms = float(per.sum())
     ms_step = total_ms / args.steps
     value = BITS_PER_STEP / (ms_step * 1e-3) / 1e9
@@ -416,7 +444,8 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Philox-4x32: i.i.d. Rayleigh "
                 "CN(0,1) channels, uniform Gray QAM, AWGN)", "config": workload_config(world),
-                "solvers": solvers, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "solvers": solvers, "centralized_baselines": baselines,
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "gpu_launches_per_step": launches / args.steps,
                 "consensus_rounds_per_step": (st1["consensus_rounds"] - st0["consensus_rounds"]) / args.steps,
                 "allreduce_calls_per_step": (st1["allreduce_calls"] - st0["allreduce_calls"]) / args.steps,

@@ -92,6 +92,19 @@ def _bf_rank(Hd, s, C, S, rho, T):
     return x
 
 
+def _central_rank(H, y, N0, Hd, s):
+    """Centralized baselines, rank-local Gram sums + ONE allreduce of [Gram | matched filter]."""
+    Hx = H.astype(np.complex128)
+    G = _allreduce(np.einsum("cnsu,cnsv->nuv", Hx.conj(), Hx))
+    b = _allreduce(np.einsum("cnsu,cnjs->nju", Hx.conj(), y.astype(np.complex128)))
+    x = np.linalg.solve(G + N0 * np.eye(G.shape[-1]), b.transpose(0, 2, 1)).transpose(0, 2, 1)
+    Hdx = Hd.astype(np.complex128)
+    B = _allreduce(np.einsum("cnus,cnvs->nuv", Hdx, Hdx.conj()))
+    r = np.linalg.solve(B, s.astype(np.complex128).transpose(0, 2, 1)).transpose(0, 2, 1)
+    xz = np.einsum("cnus,nju->cnjs", Hdx.conj(), r)                       # rank-local x_c
+    return x, xz
+
+
 def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -107,6 +120,7 @@ def _worker(rank, world, port, q):
         Hd, s = synth.downlink_frame(dcfg, d0, d1)
         out["bf"] = _bf_rank(Hd, s, dcfg.C, dcfg.S, dcfg.rho, dcfg.T)
         out["shard"] = (c0, c1)
+        out["mmse"], out["zf"] = _central_rank(H, y, cfg.N0, Hd, s)
         # bench bootstrap: rank 0's id reaches every rank; device time is max over ranks
         obj = [bytes(range(128)) if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -153,3 +167,15 @@ def test_bootstrap_host_logic(two_rank_results):
     assert two_rank_results[0]["shard"] == (0, 2) and two_rank_results[1]["shard"] == (2, 4)
     assert two_rank_results[0]["uid_ok"] and two_rank_results[1]["uid_ok"]
     assert two_rank_results[0]["tmax"] == two_rank_results[1]["tmax"] == 2.0
+
+
+def test_centralized_dataflow_matches_oracle(two_rank_results, oracle_mod):
+    cfg = synth.CONFIGS["C"].scaled(N=6, C=4, N_sym=2)
+    H, y, _ = synth.uplink_frame(cfg)
+    x_ref, _ = oracle_mod.mmse_centralized(H, y, N0=cfg.N0)
+    for r in (0, 1):
+        assert np.allclose(two_rank_results[r]["mmse"], x_ref, atol=1e-10, rtol=0)
+    dcfg = synth.CONFIGS["D"].scaled(N=5, C=4)
+    Hd, s = synth.downlink_frame(dcfg)
+    got = np.concatenate([two_rank_results[0]["zf"], two_rank_results[1]["zf"]], axis=0)
+    assert np.allclose(got, oracle_mod.zf_centralized(Hd, s), atol=1e-10, rtol=0)
