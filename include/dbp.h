@@ -158,8 +158,10 @@ dbp_status dbp_detect_cg(dbp_ctx* ctx, const dbp_dims* dims, const dbp_cf32* H,
                          const dbp_cf32* y, float rho, int mod, int32_t T, dbp_cf32* x_hat,
                          uint8_t* hard, void* ws, size_t ws_bytes, void* stream);
 
-/* Algorithm 3 (P491-527): decentralized ADMM downlink beamforming, eps = 0
- * (Alg. 3 as printed; eps > 0 = Lemma 2 returns DBP_ERR_UNSUPPORTED in v1).
+/* Algorithm 3 (P491-527): decentralized ADMM downlink beamforming.
+ *   eps >= 0: the constraint ||H x - s|| <= eps of (P0); eps = 0 is Alg. 3 as
+ *   printed, eps > 0 applies Lemma 2 (P538) at line 14:
+ *   z_c = w_c + max{0, 1 - eps/||s - w||} (s - w)/C (reading 8).
  *   Hd  [C_loc][N][U][S]     downlink H_c^d = (H_c^u)^T (P174, P181)   (read)
  *   s   [N][N_sym][U]        transmit symbols s^d, replicated (P172)   (read)
  *   rho > 0, gamma > 0 (P457);  T >= 1 (T - 1 consensus collectives: the

@@ -527,7 +527,7 @@ extern "C" dbp_status dbp_beamform_admm(dbp_ctx* c, const dbp_dims* d, const dbp
     if (!(rho > 0.f) || !std::isfinite(rho)) return fail(DBP_ERR_INVALID_ARG, "rho must be > 0");
     if (!(gamma > 0.f) || !std::isfinite(gamma)) return fail(DBP_ERR_INVALID_ARG, "gamma must be > 0");
     if (!(eps >= 0.f)) return fail(DBP_ERR_INVALID_ARG, "eps must be >= 0");
-    if (eps > 0.f) return fail(DBP_ERR_UNSUPPORTED, "eps > 0 (Lemma 2 shrink) is not in v1");
+    if (!std::isfinite(eps)) return fail(DBP_ERR_INVALID_ARG, "eps must be finite");
     if (T < 1) return fail(DBP_ERR_INVALID_ARG, "T must be >= 1");
     if (prelr_smem(sh.UP, sh.S, sh.U, sh.J, false) > (size_t)c->max_smem) return fail(DBP_ERR_UNSUPPORTED, "S too large for the preprocessing tile");
     CU(cudaSetDevice(c->device));
@@ -555,12 +555,13 @@ extern "C" dbp_status dbp_beamform_admm(dbp_ctx* c, const dbp_dims* d, const dbp
     a.gamma = gamma;
     a.a0 = (float)std::max((double)sh.U / ((double)sh.C * sh.S), 1.0 / sh.C);   // Alg. 3 line 8 (P507)
     a.inv_c = (float)(1.0 / sh.C);
+    a.eps = eps;
 
     if (c->world == 1 && !c->force_split && !c->no_fused && fused_ok(sh.UP, sh.C, sh.N, sh.J, sh.S, sh.U)) {
         // c1-c4 in one per-subcarrier kernel (world == 1, supported shape)
         bool launched = false;
         KT("fused_dl", (launched = launch_fused_dl(L, sh.UP, a.Hd, a.s, sh.C, sh.N, sh.S, sh.U, T, rho, gamma,
-                                                   a.a0, a.x), cudaGetLastError()));
+                                                   a.a0, eps, a.x), cudaGetLastError()));
         if (launched) {
             c->consensus_rounds += T - 1;
             return end_call(c, k, s);

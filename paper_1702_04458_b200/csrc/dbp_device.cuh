@@ -202,6 +202,16 @@ __device__ __forceinline__ float2 herm_mv_row(const float2* G, const float2* v, 
     return acc;
 }
 
+// ---------------------------------------------------------------- BF (Alg. 3)
+// Line 14 with Lemma 2 (P538, proof P873-890, reading 8):
+// z_c = w_c + max{0, 1 - eps/||s - w||} (s - w)/C; eps = 0 is Alg. 3 as
+// printed.  Returns the factor multiplying (s - w).
+__device__ __forceinline__ float lemma2_scale(float nrm2, float eps, float inv_c) {
+    if (!(eps > 0.f)) return inv_c;
+    const float nrm = sqrtf(nrm2);
+    return nrm > 0.f ? fmaxf(0.f, 1.f - eps / nrm) * inv_c : 0.f;
+}
+
 // ---------------------------------------------------------------- CG (Alg. 2)
 // sum over the UP-lane group (xor butterfly, the paper's shuffle allreduce P715)
 template <int UP>

@@ -72,7 +72,7 @@ struct FuArgs {
     // DL (SOLVER 2)
     const float2* s;      // [N][U]
     float2* x;            // [C][N][S]
-    float rho_inv, a0, inv_c;
+    float rho_inv, a0, inv_c, eps;
     int* flag;
 };
 
@@ -399,9 +399,19 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                     w[m] = c_sub(mm[m], lam[m]);                                   // line 12
                 }
                 consensus(w, false);                                               // line 13
+                float2 dv[R];
+                float nrm2 = 0.f;
 #pragma unroll
                 for (int m = 0; m < R; ++m) {
-                    const float2 z = c_add(w[m], c_scale(c_sub(sv[m], Sv[j * UP + row[m]]), a.inv_c));   // line 14
+                    dv[m] = c_sub(sv[m], Sv[j * UP + row[m]]);
+                    nrm2 += c_norm2(dv[m]);
+                }
+#pragma unroll
+                for (int o = 1; o < L; o <<= 1) nrm2 += __shfl_xor_sync(0xffffffffu, nrm2, o);   // ||s - w|| of the pair
+                const float f = lemma2_scale(nrm2, a.eps, a.inv_c);
+#pragma unroll
+                for (int m = 0; m < R; ++m) {
+                    const float2 z = c_add(w[m], c_scale(dv[m], f));                                    // line 14
                     lam[m] = c_sub(lam[m], c_scale(c_sub(mm[m], z), a.gamma));                          // line 15
                     qv[m] = c_add(z, lam[m]);
                 }
@@ -490,12 +500,12 @@ bool launch_fused_ul(const LaunchCtx& L, int UP, bool cg, const float2* H, const
 }
 
 bool launch_fused_dl(const LaunchCtx& L, int UP, const float2* Hd, const float2* s, int C, int N, int S, int U, int T,
-                     float rho, float gamma, float a0, float2* x) {
+                     float rho, float gamma, float a0, float eps, float2* x) {
     if (!fused_ok(UP, C, N, 1, S, U)) return false;
     FuArgs a{};
     a.S = S; a.U = U; a.N = N; a.C = C; a.T = T;
     a.rho = rho; a.gamma = gamma; a.delta = 1.f / rho;
-    a.s = s; a.x = x; a.rho_inv = 1.f / rho; a.a0 = a0; a.inv_c = 1.f / (float)C; a.flag = L.flag;
+    a.s = s; a.x = x; a.rho_inv = 1.f / rho; a.a0 = a0; a.inv_c = 1.f / (float)C; a.eps = eps; a.flag = L.flag;
     fz_shape(UP, C, a);
     switch (UP) {
         case 4: return launch_fz_t<4, 2>(L, Hd, nullptr, a);

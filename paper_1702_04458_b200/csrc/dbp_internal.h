@@ -58,7 +58,7 @@ bool launch_fused_ul(const LaunchCtx& L, int UP, bool cg, const float2* H, const
 bool launch_fused_central(const LaunchCtx& L, int UP, bool dl, const float2* H, const float2* ys, int C, int N, int S,
                           int U, float reg, Modem md, float2* out, uint8_t* hard);
 bool launch_fused_dl(const LaunchCtx& L, int UP, const float2* Hd, const float2* s, int C, int N, int S, int U, int T,
-                     float rho, float gamma, float a0, float2* x);
+                     float rho, float gamma, float a0, float eps, float2* x);
 size_t prelr_smem(int UP, int S, int U, int J, bool ul);
 bool launch_prefold(const LaunchCtx& L, int UP, int mode, const float2* H, const float2* y, int S, int U, int J,
                     long npairs, float delta, float2* Gout, float2* vout);
@@ -103,7 +103,7 @@ struct DlArgs {
     float2* x;            // [C_loc][N][J][S]
     int* flag;
     int C_loc, C, N, J, U, S, T, NT, step;
-    float rho_inv, gamma, a0, inv_c;
+    float rho_inv, gamma, a0, inv_c, eps;
 };
 
 size_t iter_smem(int UP, int NT, int C);

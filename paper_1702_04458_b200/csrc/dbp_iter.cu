@@ -209,7 +209,9 @@ __global__ void __launch_bounds__(512) k_bf_gj(DlArgs a) {
             __syncthreads();
             if (tid < NT * UP) Ws[tid] = cluster_sum(W, C, UP, tid / UP, tid % UP);   // line 13
             __syncthreads();
-            const float2 z = c_add(w, c_scale(c_sub(sv, Ws[nl * UP + i]), a.inv_c));  // line 14
+            const float2 d = c_sub(sv, Ws[nl * UP + i]);
+            const float f = lemma2_scale(group_sum<UP>(c_norm2(d)), a.eps, a.inv_c);
+            const float2 z = c_add(w, c_scale(d, f));                                // line 14 (Lemma 2)
             lam = c_sub(lam, c_scale(c_sub(m, z), a.gamma));                         // line 15
             qv = c_add(z, lam);
             __syncthreads();
@@ -262,7 +264,9 @@ __global__ void __launch_bounds__(512) k_bf_it(DlArgs a, int CCH) {
             } else {                                                     // lines 14-15 of t-1
                 const float2 mo = a.m[o], lo = a.lam[o];
                 const float2 w = c_sub(mo, lo);
-                const float2 z = c_add(w, c_scale(c_sub(sv, Wv[((size_t)nl * J + jj) * UP + i]), a.inv_c));
+                const float2 d = c_sub(sv, Wv[((size_t)nl * J + jj) * UP + i]);
+                const float f = lemma2_scale(group_sum<UP>(c_norm2(d)), a.eps, a.inv_c);
+                const float2 z = c_add(w, c_scale(d, f));                    // line 14 (Lemma 2)
                 lam = c_sub(lo, c_scale(c_sub(mo, z), a.gamma));
                 qv = c_add(z, lam);
             }

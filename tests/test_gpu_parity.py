@@ -179,15 +179,15 @@ def test_cg_zero_input(env):
     assert torch.all(x == 0)
 
 
-def run_bf(env, cfg, split=False, T=None):
+def run_bf(env, cfg, split=False, T=None, eps=0.0):
     dbp, ctx, oracle, torch = env
     T = cfg.T if T is None else T
     Hd, s = synth.downlink_frame(cfg)
     set_path(env, split if isinstance(split, str) else ("split" if split else "fused"))
-    x = dbp.beamform_admm(ctx, torch.from_numpy(Hd).cuda(), torch.from_numpy(s).cuda(), rho=cfg.rho, T=T)
+    x = dbp.beamform_admm(ctx, torch.from_numpy(Hd).cuda(), torch.from_numpy(s).cuda(), rho=cfg.rho, T=T, eps=eps)
     ctx.sync()
     set_path(env, "fused")
-    x_ref = oracle.beamform_admm(Hd, s, rho=cfg.rho, T=T)
+    x_ref = oracle.beamform_admm(Hd, s, rho=cfg.rho, T=T, eps=eps)
     return x.cpu().numpy(), x_ref
 
 
@@ -208,6 +208,19 @@ SMALL_DL = [
 @pytest.mark.parametrize("split", PATHS)
 def test_bf_parity(env, cfg, split):
     x, x_ref = run_bf(env, cfg, split)
+    assert rel(x, x_ref) < TOL
+
+
+@pytest.mark.parametrize("cfg", [synth.CONFIGS["D"].scaled(N=24), synth.CONFIGS["D"].scaled(N=9, C=4),
+                                 synth.CONFIGS["E"].scaled(N=4, C=8, algo="admm_dl"),
+                                 synth.Config("odd", "admm_dl", C=3, S=7, U=5, N=11, mod="qam16"),
+                                 synth.Config("nsym", "admm_dl", C=2, S=16, U=8, N=10, N_sym=3, mod="qam64")],
+                         ids=lambda c: f"{c.name}-C{c.C}S{c.S}U{c.U}N{c.N}J{c.N_sym}")
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("eps", [0.05, 0.5, 100.0])
+def test_bf_lemma2_eps(env, cfg, path, eps):
+    """eps > 0 (Lemma 2, P538): small eps ~ Alg. 3, eps beyond ||s - w|| freezes the consensus pull."""
+    x, x_ref = run_bf(env, cfg, path, T=6, eps=eps)
     assert rel(x, x_ref) < TOL
 
 
@@ -278,9 +291,10 @@ def test_invalid_arguments(env):
         dbp.detect_cg(ctx, Hg, yg, rho=-0.5, mod="qpsk")
     assert ei.value.status == 1
     Hd, s = synth.downlink_frame(cfg)
-    with pytest.raises(dbp.DbpError) as ei:
-        dbp.beamform_admm(ctx, torch.from_numpy(Hd).cuda(), torch.from_numpy(s).cuda(), eps=0.1)
-    assert ei.value.status == 2
+    for bad in (-0.1, float("nan")):
+        with pytest.raises(dbp.DbpError) as ei:
+            dbp.beamform_admm(ctx, torch.from_numpy(Hd).cuda(), torch.from_numpy(s).cuda(), eps=bad)
+        assert ei.value.status == 1
     big = torch.zeros((1, 2, 4, 33), dtype=torch.complex64, device="cuda")
     with pytest.raises(dbp.DbpError) as ei:
         dbp.detect_admm(ctx, big, torch.zeros((1, 2, 1, 4), dtype=torch.complex64, device="cuda"))
