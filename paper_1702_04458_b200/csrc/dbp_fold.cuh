@@ -250,6 +250,11 @@ __device__ __forceinline__ void fold_store(float2* G, const f2x (&A)[Fold<UP>::N
     }
 }
 
+// Per-pair stride of the mat-vec partial-sum block: L lanes x (UP + 2) float2,
+// + 2 so consecutive pairs start 80 B apart modulo 128 (distinct bank groups).
+template <int UP>
+__host__ __device__ constexpr int fold_ybuf_pair() { return (UP / 4) * (UP + 2) + 2; }
+
 // Mat-vec form of a Hermitian matrix in folded slots: junk slots zeroed and
 // the diagonal halved, so y = M v is  y_r = sum_slots(r) S_rt v_t  +
 // sum_lanes sum_slots(t, r) conj(S_tr) v_t  with no validity predicates.
@@ -269,7 +274,9 @@ __device__ __forceinline__ void fold_mv_prep(f2x (&A)[Fold<UP>::NSLOT], const in
 }
 
 // y_{r_m} = (M v)_{r_m} for the pair's 4 rows per lane.  vline: the pair's
-// UP-line; ybuf: the pair's L x UP partial-sum block.  Both in shared memory.
+// UP-line; ybuf: the pair's L x YLS partial-sum block (fold_ybuf_pair() float2 per
+// pair; the padded lane and pair strides put the 32 lanes of a warp on distinct
+// 16-B bank groups).  Both in shared memory.
 template <int UP>
 __device__ __forceinline__ void fold_mv(const f2x (&A)[Fold<UP>::NSLOT], const float2 (&v)[4], float2 (&y)[4],
                                         float2* vline, float2* ybuf, const int (&row)[4], int l) {
@@ -298,7 +305,8 @@ __device__ __forceinline__ void fold_mv(const f2x (&A)[Fold<UP>::NSLOT], const f
         }
         y[m] = upk2(acc);
     }
-    float4* yb = reinterpret_cast<float4*>(ybuf + l * UP);
+    constexpr int YLS = UP + 2;                            // lane stride (float2): +16 B per lane
+    float4* yb = reinterpret_cast<float4*>(ybuf + l * YLS);
 #pragma unroll
     for (int t2 = 0; t2 < UP; t2 += 2) {
         const float2 c0 = upk2(col[t2]), c1 = upk2(col[t2 + 1]);
@@ -308,7 +316,7 @@ __device__ __forceinline__ void fold_mv(const f2x (&A)[Fold<UP>::NSLOT], const f
 #pragma unroll
     for (int m = 0; m < 4; ++m)
 #pragma unroll
-        for (int ll = 0; ll < F::L; ++ll) y[m] = c_add(y[m], ybuf[ll * UP + row[m]]);
+        for (int ll = 0; ll < F::L; ++ll) y[m] = c_add(y[m], ybuf[ll * YLS + row[m]]);
 }
 
 }  // namespace dbp

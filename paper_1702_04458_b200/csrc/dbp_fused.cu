@@ -35,6 +35,9 @@
 #include "dbp_internal.h"
 
 #pragma nv_diag_suppress 128   // SOLVER 0 continues before the inverse: "loop is not reachable"
+#ifndef DBP_FZ_1BAR
+#define DBP_FZ_1BAR 0
+#endif
 
 namespace dbp {
 
@@ -52,11 +55,11 @@ struct FZ {
     static constexpr int NST = DBP_FZ_NST;
     static constexpr int PWL = F::PW * (UP + 2);          // pivot / vector lines (float2)
     static constexpr int DLN = F::PW * UP;                // Jacobi scales (float)
-    static constexpr int YB = F::PW * F::L * UP;          // mat-vec partials (float2)
+    static constexpr int YB = F::PW * fold_ybuf_pair<UP>(); // mat-vec partials (float2), padded
     static constexpr int WREG = (NST * G::STG + PWL * 8 + DLN * 4 + YB * 8 + 127) / 128 * 128;
     // CTA-shared: per-warp consensus partials [WARPS][UP] + per-subcarrier sums [4][UP];
     // CG: per-warp Gram partials [WARPS][TRI] + per-subcarrier Gram [4][TRI]
-    static constexpr int CBUF = WARPS * UP * 8 + WARPS * UP * 8;
+    static constexpr int CBUF = 2 * WARPS * UP * 8 + WARPS * UP * 8;   // Wp (x2: round parity) + Sv
     static constexpr int GBUF = SUMS ? 2 * WARPS * F::TRI * 8 : 0;
     static constexpr size_t SMEM = 128 + (size_t)WARPS * WREG + CBUF + GBUF;
 };
@@ -91,9 +94,9 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     const int q = lane / L, l = lane % L;
     float2* pl = reinterpret_cast<float2*>(wbase + NST * G::STG) + q * (UP + 2);           // pivots / vectors
     float* dline = reinterpret_cast<float*>(wbase + NST * G::STG + Z::PWL * 8) + q * UP;
-    float2* ybuf = reinterpret_cast<float2*>(wbase + NST * G::STG + Z::PWL * 8 + Z::DLN * 4) + q * L * UP;
+    float2* ybuf = reinterpret_cast<float2*>(wbase + NST * G::STG + Z::PWL * 8 + Z::DLN * 4) + q * fold_ybuf_pair<UP>();
     float2* Wp = reinterpret_cast<float2*>(smem_raw + 128 + (size_t)Z::WARPS * Z::WREG);   // [4 warps][UP]
-    float2* Sv = Wp + Z::WARPS * UP;                                                       // [4 subc.][UP]
+    float2* Sv = Wp + 2 * Z::WARPS * UP;                                                   // [4 subc.][UP]
     float2* Gp = Sv + Z::WARPS * UP;                                                       // CG: [4 warps][TRI]
     float2* Gs = Gp + (Z::SUMS ? Z::WARPS * TRI : 0);                                      // queue: [4][TRI]
 
@@ -133,7 +136,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     if (lane == 0)
         for (int s = 0; s < NST && s < nseq; ++s) issue(s, s);
 
-    int sq = 0, st = 0, qn = 0;
+    int sq = 0, st = 0, qn = 0, rnd = 0;
     uint32_t phase = 0;
     static_assert(Z::WARPS * NST * 8 <= 96, "mbarriers overlap the CG queue indices");
     int* qsub = reinterpret_cast<int*>(smem_raw + 96);     // CG queue: subcarrier of each slot
@@ -321,7 +324,11 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
 
         // consensus over the subcarrier's clusters, Sv[j] <- f(sum_c w_c): xor butterfly over the
         // warp's pairs, then the WPS warp partials in fixed order (deterministic)
-        auto consensus = [&](const float2 (&w)[R], bool do_prox) {
+        // Returns, for the lane's rows, f(sum_c w_c) with f = prox (UL) or identity (DL).
+        // DBP_FZ_1BAR: one CTA barrier per round -- warp partials go to a double-buffered Wp
+        // (round parity) and every lane sums the WPS partials of its own rows; otherwise 16
+        // threads form the sums into Sv between two barriers.
+        auto consensus = [&](const float2 (&w)[R], bool do_prox, float2 (&out)[R]) {
             float2 ps[R];
 #pragma unroll
             for (int m = 0; m < R; ++m) {
@@ -332,18 +339,39 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                     ps[m].y += __shfl_xor_sync(0xffffffffu, ps[m].y, o);
                 }
             }
+            float2* Wr = Wp + (DBP_FZ_1BAR ? (rnd & 1) * Z::WARPS * UP : 0);
+            ++rnd;
             if (lane < L) {
 #pragma unroll
-                for (int m = 0; m < R; ++m) Wp[warp * UP + row[m]] = ps[m];
+                for (int m = 0; m < R; ++m) Wr[warp * UP + row[m]] = ps[m];
             }
             __syncthreads();
-            if (tid < NPC * UP) {
-                const int jj = tid / UP, u = tid - jj * UP;
-                float2 acc = make_float2(0.f, 0.f);
-                for (int w2 = 0; w2 < WPS; ++w2) acc = c_add(acc, Wp[(jj * WPS + w2) * UP + u]);
-                Sv[tid] = do_prox ? prox(acc, a.px) : acc;
+            if (DBP_FZ_1BAR) {
+#pragma unroll
+                for (int m = 0; m < R; ++m) {
+                    float2 acc = make_float2(0.f, 0.f);
+                    for (int w2 = 0; w2 < WPS; ++w2) acc = c_add(acc, Wr[(j * WPS + w2) * UP + row[m]]);
+                    out[m] = do_prox ? prox(acc, a.px) : acc;
+                }
+            } else {
+                if (tid < NPC * UP) {
+                    const int jj = tid / UP, u = tid - jj * UP;
+                    float2 acc = make_float2(0.f, 0.f);
+                    for (int w2 = 0; w2 < WPS; ++w2) acc = c_add(acc, Wr[(jj * WPS + w2) * UP + u]);
+                    Sv[tid] = do_prox ? prox(acc, a.px) : acc;
+                }
+                __syncthreads();
+#pragma unroll
+                for (int m = 0; m < R; ++m) out[m] = Sv[j * UP + row[m]];
             }
-            __syncthreads();
+        };
+        // entry u of the last round's f(sum) (output lanes)
+        auto last_out = [&](int u, bool do_prox) {
+            if (!DBP_FZ_1BAR) return Sv[j * UP + u];
+            const float2* Wr = Wp + ((rnd - 1) & 1) * Z::WARPS * UP;
+            float2 acc = make_float2(0.f, 0.f);
+            for (int w2 = 0; w2 < WPS; ++w2) acc = c_add(acc, Wr[(j * WPS + w2) * UP + u]);
+            return do_prox ? prox(acc, a.px) : acc;
         };
 
         if constexpr (SOLVER == 1) {
@@ -356,14 +384,14 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                 z[m] = yreg[m];
                 w[m] = yreg[m];
             }
-            consensus(w, true);
+            float2 sc[R];
+            consensus(w, true, sc);
             for (int t = 2; t <= a.T; ++t) {
                 float2 v[R], bv[R];
 #pragma unroll
                 for (int m = 0; m < R; ++m) {
-                    const float2 s = Sv[j * UP + row[m]];
-                    lam[m] = c_add(lam[m], c_scale(c_sub(z[m], s), a.gamma));    // line 12
-                    v[m] = c_sub(s, lam[m]);
+                    lam[m] = c_add(lam[m], c_scale(c_sub(z[m], sc[m]), a.gamma));  // line 12
+                    v[m] = c_sub(sc[m], lam[m]);
                 }
                 fold_mv<UP>(A, v, bv, pl, ybuf, row, l);                          // rho B^{-1} (s - lambda)
 #pragma unroll
@@ -371,12 +399,12 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                     z[m] = c_add(yreg[m], bv[m]);                                 // line 15
                     w[m] = c_add(z[m], lam[m]);                                   // line 17
                 }
-                consensus(w, true);                                               // lines 18-19
+                consensus(w, true, sc);                                           // lines 18-19
             }
             if (warp == j * WPS && lane < UP) {
                 const int u = lane;
                 if (u < a.U && n < a.N) {
-                    const float2 s = Sv[j * UP + u];
+                    const float2 s = last_out(u, true);
                     a.s_hat[(size_t)n * a.U + u] = s;
                     if (a.hard) a.hard[(size_t)n * a.U + u] = slice_bits(s, a.md);
                 }
@@ -398,12 +426,13 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                     mm[m] = c_sub(qv[m], c_scale(bq[m], a.rho_inv));               // line 11
                     w[m] = c_sub(mm[m], lam[m]);                                   // line 12
                 }
-                consensus(w, false);                                               // line 13
+                float2 W[R];
+                consensus(w, false, W);                                            // line 13
                 float2 dv[R];
                 float nrm2 = 0.f;
 #pragma unroll
                 for (int m = 0; m < R; ++m) {
-                    dv[m] = c_sub(sv[m], Sv[j * UP + row[m]]);
+                    dv[m] = c_sub(sv[m], W[m]);
                     nrm2 += c_norm2(dv[m]);
                 }
 #pragma unroll
