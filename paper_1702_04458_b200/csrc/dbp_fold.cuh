@@ -57,7 +57,10 @@ struct FoldStage {
 
 // ---------------------------------------------------------------- Gram
 // UL: G_rt += conj(h_sr) h_st (and b_r += conj(h_sr) y_s) over one stage.
-// Pair q reads antenna (s + q/2) mod 4: the 8 pairs' LDS.128 hit distinct bank groups.
+// Pair q reads antenna (s + P[q/2]) mod 4 with P = {0, 2, 1, 3}: line (q, s) starts
+// at 16-B unit 4(q & 1) + s_q (mod 8), so the 8 pairs' broadcast LDS.128 hit 8
+// distinct bank groups, and within each half-warp the 4 pairs' own-row LDS.64
+// (2 units per pair) start 2 units apart -- both conflict-free.
 template <int UP, bool MF>
 __device__ __forceinline__ void fold_gram_ul(f2x (&A)[Fold<UP>::NSLOT], f2x (&E)[4], const float2* stage, int q,
                                              const int (&row)[4]) {
@@ -67,7 +70,7 @@ __device__ __forceinline__ void fold_gram_ul(f2x (&A)[Fold<UP>::NSLOT], f2x (&E)
     const float2* yq = stage + G::HSZ + q * F::SC;
 #pragma unroll PF_UNROLL
     for (int s = 0; s < F::SC; ++s) {
-        const int sr = (s + (q >> 1)) & (F::SC - 1);
+        const int sr = (s + ((((q >> 1) & 1) << 1) | ((q >> 2) & 1))) & (F::SC - 1);
         const float2* hrow = hq + sr * G::HL;
         float2 h[UP];
         read_vec<UP>(hrow, h);
@@ -86,7 +89,9 @@ __device__ __forceinline__ void fold_gram_ul(f2x (&A)[Fold<UP>::NSLOT], f2x (&E)
     }
 }
 
-// DL: B_rt += H_rs conj(H_ts); pair q reads antenna pair (s/2 + q/4) mod 2.
+// DL: B_rt += H_rs conj(H_ts); pair q reads antenna pair (s/2 + q) mod 2: line
+// units 2q + 2t + c_q with c_q alternating between adjacent pairs, so the own-row
+// LDS.128 of the two pairs sharing a quarter-warp phase never collide.
 template <int UP>
 __device__ __forceinline__ void fold_gram_dl(f2x (&A)[Fold<UP>::NSLOT], const float2* stage, int q, const int (&row)[4]) {
     using F = Fold<UP>;
@@ -94,7 +99,7 @@ __device__ __forceinline__ void fold_gram_dl(f2x (&A)[Fold<UP>::NSLOT], const fl
     const float2* hq = stage + q * G::NL * G::HL;
 #pragma unroll 1
     for (int s0 = 0; s0 < F::SC; s0 += 2) {
-        const int s = (s0 + 2 * (q >> 2)) & (F::SC - 1);
+        const int s = (s0 + 2 * (q & 1)) & (F::SC - 1);
         float4 o[4];
 #pragma unroll
         for (int m = 0; m < 4; ++m) o[m] = *reinterpret_cast<const float4*>(hq + row[m] * G::HL + s);
@@ -250,10 +255,11 @@ __device__ __forceinline__ void fold_store(float2* G, const f2x (&A)[Fold<UP>::N
     }
 }
 
-// Per-pair stride of the mat-vec partial-sum block: L lanes x (UP + 2) float2,
-// + 2 so consecutive pairs start 80 B apart modulo 128 (distinct bank groups).
+// Per-pair stride of the mat-vec partial-sum block: L lanes x (UP + 2) float2.
+// Lane stride 9 16-B units (= 1 mod 8), pair stride 36 units (= 4 mod 8 at UP = 16):
+// the 8 lanes of each quarter-warp phase of an STS.128 hit 8 distinct bank groups.
 template <int UP>
-__host__ __device__ constexpr int fold_ybuf_pair() { return (UP / 4) * (UP + 2) + 2; }
+__host__ __device__ constexpr int fold_ybuf_pair() { return (UP / 4) * (UP + 2); }
 
 // Mat-vec form of a Hermitian matrix in folded slots: junk slots zeroed and
 // the diagonal halved, so y = M v is  y_r = sum_slots(r) S_rt v_t  +
