@@ -114,11 +114,12 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     const int per_item = DL ? 2 * nch : nch;           // DL: Gram pass + output pass
     const int nseq = nitems * per_item;
 
-    auto issue = [&](int sqn, int st) {
-        const int item = sqn / per_item;
-        int ch = sqn - item * per_item;
-        if (ch >= nch) ch -= nch;
-        const int n = (blockIdx.x + item * gridDim.x) * NPC + j;
+    // TMA issue cursor (lane 0): the (item, chunk) of the next stage to load, advanced by one
+    // per issue -- no division on the per-stage path
+    int is_item = 0, is_ch = 0;
+    auto issue = [&](int st) {
+        const int ch = is_ch >= nch ? is_ch - nch : is_ch;
+        const int n = (blockIdx.x + is_item * gridDim.x) * NPC + j;
         unsigned char* dst = wbase + st * G::STG;
         mbar_arrive_expect_tx(&bar[st], (uint32_t)G::BYTES);
         if (DL) {
@@ -127,6 +128,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
             tma_load4(dst, &tmH, 0, ch * SC, n, cb * PW, &bar[st]);
             tma_load4(dst + G::HSZ * 8, &tmY, ch * SC, 0, n, cb * PW, &bar[st]);
         }
+        if (++is_ch == per_item) { is_ch = 0; ++is_item; }
     };
     if (lane == 0) {
         for (int s = 0; s < NST; ++s) mbar_init(&bar[s], 1);
@@ -134,7 +136,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     }
     __syncwarp();
     if (lane == 0)
-        for (int s = 0; s < NST && s < nseq; ++s) issue(s, s);
+        for (int s = 0; s < NST && s < nseq; ++s) issue(s);
 
     int sq = 0, st = 0, qn = 0, rnd = 0;
     uint32_t phase = 0;
@@ -144,7 +146,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
         __syncwarp();
         if (lane == 0 && sq + NST < nseq) {
             fence_proxy_async();
-            issue(sq + NST, st);
+            issue(st);
         }
         ++sq;
         if (++st == NST) { st = 0; phase ^= 1u; }

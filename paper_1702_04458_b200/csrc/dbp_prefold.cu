@@ -99,10 +99,12 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
     const int nch = (a.S + SC - 1) / SC;
     const int nseq = nitems * nch;
 
-    // sequence number sq -> (item, chunk) in stage st; issued NST ahead of consumption
-    auto issue = [&](int sq, int st) {
-        const int item = sq / nch, ch = sq - item * nch;
-        const int p0 = (gw + item * W) * PW;
+    // TMA issue cursor (lane 0): the (item, chunk) of the next stage to load, advanced by one
+    // per issue (stages are issued in sequence order, NST ahead of consumption)
+    int is_item = 0, is_ch = 0;
+    auto issue = [&](int st) {
+        const int p0 = (gw + is_item * W) * PW;
+        const int ch = is_ch;
         unsigned char* dst = wbase + st * G::STG;
         mbar_arrive_expect_tx(&bar[st], (uint32_t)G::BYTES);
         if (DL) {
@@ -111,6 +113,7 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
             tma_load3(dst, &tmH, 0, ch * SC, p0, &bar[st]);
             if (MF) tma_load3(dst + G::HSZ * 8, &tmY, ch * SC, 0, p0, &bar[st]);
         }
+        if (++is_ch == nch) { is_ch = 0; ++is_item; }
     };
     if (lane == 0) {
         for (int s = 0; s < NST; ++s) mbar_init(&bar[s], 1);
@@ -118,7 +121,7 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
     }
     __syncwarp();
     if (lane == 0)
-        for (int s = 0; s < NST && s < nseq; ++s) issue(s, s);
+        for (int s = 0; s < NST && s < nseq; ++s) issue(s);
 
     int sq = 0, st = 0;
     uint32_t phase = 0;
@@ -141,7 +144,7 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
             __syncwarp();
             if (lane == 0 && sq + NST < nseq) {
                 fence_proxy_async();
-                issue(sq + NST, st);
+                issue(st);
             }
             ++sq;
             if (++st == NST) { st = 0; phase ^= 1u; }
