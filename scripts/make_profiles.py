@@ -19,7 +19,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PROF = os.path.join(ROOT, "profiles")
 
 # libdbp kernel symbol -> bench kernel-timer name
-NAMES = [(r"k_fused<\d+, 0>", "fused_cg"), (r"k_fused<\d+, 1>", "fused_ul"), (r"k_fused<\d+, 2>", "fused_dl"),
+NAMES = [(r"k_fused<\d+, 3>", "fused_mmse"), (r"k_fused<\d+, 4>", "fused_zf"), (r"k_fused<\d+, 0>", "fused_cg"), (r"k_fused<\d+, 1>", "fused_ul"), (r"k_fused<\d+, 2>", "fused_dl"),
          (r"k_prefold<\d+, 0, 0", "pre_cg"), (r"k_prefold<\d+, 0, 1", "pre_ul"), (r"k_prefold<\d+, 1, 2", "pre_dl"),
          (r"k_prelr<\d+, 0, 0", "pre_cg"), (r"k_prelr<\d+, 0, 1", "pre_ul"), (r"k_prelr<\d+, 1, 2", "pre_dl"),
          (r"k_gram<\d+, 0, 1", "gram_ul"), (r"k_gram<\d+, 1,", "gram_dl"), (r"k_inv_ul", "inv_ul"),
@@ -49,13 +49,16 @@ def launches(tag, path):
         v = v / 1e3 if r[ui] in ("nsecond", "ns") else v * 1e3 if r[ui] in ("msecond", "ms") else v
         agg.setdefault(r[ki], []).append(v)
     ours = {k: v for k, v in agg.items() if "dbp::" in k}
-    tot = sum(sum(v) for v in ours.values())
+    # shares over the timed step's kernels; the centralized baselines bench.py times afterwards are listed apart
+    BASE = ("fused_mmse", "fused_zf", "central_solve", "zf_out")
+    tot = sum(sum(v) for k, v in ours.items() if short(k) not in BASE) or 1.0
     lines = [f"# {tag}: ncu launch list (gpu__time_duration.sum, --clock-control none)", "",
              "Serialised, cold-cache per-launch times of `bench.py --steps 3 --warmup 3` (all launches of the",
              "process, libdbp kernels only below).  Compare SHARES with bench.py's live event timing, not",
-             "absolute times.", "", "| kernel | launches | mean us | share of libdbp time |", "|---|---|---|---|"]
+             "absolute times.", "", "| kernel | launches | mean us | share of the step's libdbp time |", "|---|---|---|---|"]
     for k, v in sorted(ours.items(), key=lambda kv: -sum(kv[1])):
-        lines.append(f"| {short(k)} (`{k.split('(')[0]}`) | {len(v)} | {sum(v)/len(v):.1f} | {sum(v)/tot:.3f} |")
+        sh = "baseline (not in the step)" if short(k) in BASE else f"{sum(v)/tot:.3f}"
+        lines.append(f"| {short(k)} (`{k.split('(')[0]}`) | {len(v)} | {sum(v)/len(v):.1f} | {sh} |")
     others = {k: v for k, v in agg.items() if "dbp::" not in k}
     lines += ["", "Non-libdbp launches in the same process (torch flush / setup): " +
               ", ".join(f"{k.split('(')[0][:40]} x{len(v)}" for k, v in others.items())]
