@@ -242,6 +242,15 @@ __global__ void __launch_bounds__(512) k_bf_it(DlArgs a, int CCH) {
     float2* buf = pbuf + (size_t)q * UP;
     const bool fin = a.step > a.T;
     const bool first = a.step == 2;
+    if (fin && i == 0) {
+        // the output pass reads H_c of every pair of this CTA: pull them into L2 up front
+        const size_t bytes = (size_t)a.U * a.S * 8;
+        if ((bytes & 15) == 0 && bytes < (1u << 20))
+            for (int c = cl; c < C; c += CCH)
+                if (n < a.N)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                                 ::"l"(a.Hd + ((size_t)c * a.N + n) * a.U * a.S), "r"((uint32_t)bytes) : "memory");
+    }
     for (int e = tid; e < NT * J * UP; e += blockDim.x) {
         const int el = e / (J * UP);
         Wv[e] = (n0 + el < a.N && !first) ? a.wbuf[(size_t)n0 * J * UP + e] : make_float2(0.f, 0.f);
