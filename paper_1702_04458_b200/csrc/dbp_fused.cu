@@ -35,9 +35,6 @@
 #include "dbp_internal.h"
 
 #pragma nv_diag_suppress 128   // SOLVER 0 continues before the inverse: "loop is not reachable"
-#ifndef DBP_FZ_1BAR
-#define DBP_FZ_1BAR 0
-#endif
 
 namespace dbp {
 
@@ -59,7 +56,7 @@ struct FZ {
     static constexpr int WREG = (NST * G::STG + PWL * 8 + DLN * 4 + YB * 8 + 127) / 128 * 128;
     // CTA-shared: per-warp consensus partials [WARPS][UP] + per-subcarrier sums [4][UP];
     // CG: per-warp Gram partials [WARPS][TRI] + per-subcarrier Gram [4][TRI]
-    static constexpr int CBUF = 2 * WARPS * UP * 8 + WARPS * UP * 8;   // Wp (x2: round parity) + Sv
+    static constexpr int CBUF = WARPS * UP * 8 + WARPS * UP * 8;       // Wp + Sv
     static constexpr int GBUF = SUMS ? 2 * WARPS * F::TRI * 8 : 0;
     static constexpr size_t SMEM = 128 + (size_t)WARPS * WREG + CBUF + GBUF;
 };
@@ -96,7 +93,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     float* dline = reinterpret_cast<float*>(wbase + NST * G::STG + Z::PWL * 8) + q * UP;
     float2* ybuf = reinterpret_cast<float2*>(wbase + NST * G::STG + Z::PWL * 8 + Z::DLN * 4) + q * fold_ybuf_pair<UP>();
     float2* Wp = reinterpret_cast<float2*>(smem_raw + 128 + (size_t)Z::WARPS * Z::WREG);   // [4 warps][UP]
-    float2* Sv = Wp + 2 * Z::WARPS * UP;                                                   // [4 subc.][UP]
+    float2* Sv = Wp + Z::WARPS * UP;                                                       // [4 subc.][UP]
     float2* Gp = Sv + Z::WARPS * UP;                                                       // CG: [4 warps][TRI]
     float2* Gs = Gp + (Z::SUMS ? Z::WARPS * TRI : 0);                                      // queue: [4][TRI]
 
@@ -138,7 +135,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     if (lane == 0)
         for (int s = 0; s < NST && s < nseq; ++s) issue(s);
 
-    int sq = 0, st = 0, qn = 0, rnd = 0;
+    int sq = 0, st = 0, qn = 0;
     uint32_t phase = 0;
     static_assert(Z::WARPS * NST * 8 <= 96, "mbarriers overlap the CG queue indices");
     int* qsub = reinterpret_cast<int*>(smem_raw + 96);     // CG queue: subcarrier of each slot
@@ -326,10 +323,10 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
 
         // consensus over the subcarrier's clusters, Sv[j] <- f(sum_c w_c): xor butterfly over the
         // warp's pairs, then the WPS warp partials in fixed order (deterministic)
-        // Returns, for the lane's rows, f(sum_c w_c) with f = prox (UL) or identity (DL).
-        // DBP_FZ_1BAR: one CTA barrier per round -- warp partials go to a double-buffered Wp
-        // (round parity) and every lane sums the WPS partials of its own rows; otherwise 16
-        // threads form the sums into Sv between two barriers.
+        // consensus over the subcarrier's clusters: xor butterfly over the warp's pairs, the WPS
+        // warp partials summed in fixed order by UP threads per subcarrier (deterministic) into
+        // Sv; returns f(sum_c w_c) for the lane's rows, f = prox (UL) or identity (DL).  (A
+        // one-barrier variant, every lane summing its own rows, measured slower.)
         auto consensus = [&](const float2 (&w)[R], bool do_prox, float2 (&out)[R]) {
             float2 ps[R];
 #pragma unroll
@@ -341,40 +338,22 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                     ps[m].y += __shfl_xor_sync(0xffffffffu, ps[m].y, o);
                 }
             }
-            float2* Wr = Wp + (DBP_FZ_1BAR ? (rnd & 1) * Z::WARPS * UP : 0);
-            ++rnd;
             if (lane < L) {
 #pragma unroll
-                for (int m = 0; m < R; ++m) Wr[warp * UP + row[m]] = ps[m];
+                for (int m = 0; m < R; ++m) Wp[warp * UP + row[m]] = ps[m];
             }
             __syncthreads();
-            if (DBP_FZ_1BAR) {
-#pragma unroll
-                for (int m = 0; m < R; ++m) {
-                    float2 acc = make_float2(0.f, 0.f);
-                    for (int w2 = 0; w2 < WPS; ++w2) acc = c_add(acc, Wr[(j * WPS + w2) * UP + row[m]]);
-                    out[m] = do_prox ? prox(acc, a.px) : acc;
-                }
-            } else {
-                if (tid < NPC * UP) {
-                    const int jj = tid / UP, u = tid - jj * UP;
-                    float2 acc = make_float2(0.f, 0.f);
-                    for (int w2 = 0; w2 < WPS; ++w2) acc = c_add(acc, Wr[(jj * WPS + w2) * UP + u]);
-                    Sv[tid] = do_prox ? prox(acc, a.px) : acc;
-                }
-                __syncthreads();
-#pragma unroll
-                for (int m = 0; m < R; ++m) out[m] = Sv[j * UP + row[m]];
+            if (tid < NPC * UP) {
+                const int jj = tid / UP, u = tid - jj * UP;
+                float2 acc = make_float2(0.f, 0.f);
+                for (int w2 = 0; w2 < WPS; ++w2) acc = c_add(acc, Wp[(jj * WPS + w2) * UP + u]);
+                Sv[tid] = do_prox ? prox(acc, a.px) : acc;
             }
+            __syncthreads();
+#pragma unroll
+            for (int m = 0; m < R; ++m) out[m] = Sv[j * UP + row[m]];
         };
-        // entry u of the last round's f(sum) (output lanes)
-        auto last_out = [&](int u, bool do_prox) {
-            if (!DBP_FZ_1BAR) return Sv[j * UP + u];
-            const float2* Wr = Wp + ((rnd - 1) & 1) * Z::WARPS * UP;
-            float2 acc = make_float2(0.f, 0.f);
-            for (int w2 = 0; w2 < WPS; ++w2) acc = c_add(acc, Wr[(j * WPS + w2) * UP + u]);
-            return do_prox ? prox(acc, a.px) : acc;
-        };
+        auto last_out = [&](int u) { return Sv[j * UP + u]; };   // entry u of the last round (output lanes)
 
         if constexpr (SOLVER == 1) {
             // ---------------------------------------------- ADMM-UL iterations (Alg. 1 lines 10-19)
@@ -406,7 +385,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
             if (warp == j * WPS && lane < UP) {
                 const int u = lane;
                 if (u < a.U && n < a.N) {
-                    const float2 s = last_out(u, true);
+                    const float2 s = last_out(u);
                     a.s_hat[(size_t)n * a.U + u] = s;
                     if (a.hard) a.hard[(size_t)n * a.U + u] = slice_bits(s, a.md);
                 }
