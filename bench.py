@@ -227,6 +227,7 @@ def main():
     ap.add_argument("--impl", default="dbp", choices=["dbp", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-table2", action="store_true")
     ap.add_argument("--ref-subcarriers", type=int, default=60)
     args = ap.parse_args()
 
@@ -267,7 +268,7 @@ def main():
     ws = {a: torch.empty(max(1, ctx.workspace_bytes(UL.C, UL.S, UL.U, UL.N, UL.N_sym, a)), dtype=torch.uint8,
                          device=dev) for a in ("admm_ul", "cg_ul", "admm_dl")}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    flush_sink = torch.empty(1, dtype=torch.int64, device=dev)
+    flush_sink = torch.empty((), dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def flush_l2(k):
@@ -368,6 +369,42 @@ def main():
         ms = float(mx([sum(e0.elapsed_time(e1) for e0, e1 in evs) / K1])[0])
         bits = UL.bits_per_frame if nm == "mmse_ul" else DL.bits_per_frame
         baselines[nm] = {"ms": ms, "gbps": bits / (ms * 1e-3) / 1e9}
+
+    # the paper's own Table II workload (P803-804: U=16, 64-QAM, N=1200, N_sym=7 per coherence
+    # interval, T=5, B=1024 = 32 x 32) next to its printed K40-cluster cells -- context only
+    table2 = None
+    if not args.no_table2:
+        t2 = UL.scaled(N_sym=7)
+        H7, y7, _ = synth.uplink_frame(t2, c0, c1)
+        Hd7, s7 = synth.downlink_frame(t2.scaled(algo="admm_dl"), c0, c1)
+        H7g, y7g = torch.from_numpy(H7).to(dev), torch.from_numpy(y7).to(dev)
+        Hd7g, s7g = torch.from_numpy(Hd7).to(dev), torch.from_numpy(s7).to(dev)
+        bits7 = t2.U * t2.N * t2.N_sym * 6
+        paper = {"admm_ul": (21.53, 39.95, "P771"), "cg_ul": (13.61, 59.25, "P779"), "admm_dl": (11.11, 77.40, "P787")}
+        fns = {"admm_ul": lambda: dbp.detect_admm(ctx, H7g, y7g, rho=t2.rho, N0=t2.N0, mod="qam64", T=t2.T),
+               "cg_ul": lambda: dbp.detect_cg(ctx, H7g, y7g, rho=t2.N0, mod="qam64", T=t2.T),
+               "admm_dl": lambda: dbp.beamform_admm(ctx, Hd7g, s7g, rho=t2.rho, T=t2.T)}
+        table2 = {"workload": "B=1024 (C=32 x S=32), U=16, 64-QAM, N=1200, N_sym=7, T=5 (PAPER.md P803-804); "
+                              "two-kernel path (the fused kernel takes N_sym = 1)",
+                  "paper_hw": "32 x Tesla K40 + Cray Aries MPI (P685, P799), CPU wall clock"}
+        K2 = 20
+        for nm, fn in fns.items():
+            for _ in range(2):
+                fn()
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K2)]
+            barrier()
+            torch.cuda.synchronize()
+            for e0, e1 in evs:
+                flush_l2(1)
+                e0.record(stream)
+                fn()
+                e1.record(stream)
+            torch.cuda.synchronize()
+            ms = float(mx([sum(e0.elapsed_time(e1) for e0, e1 in evs) / K2])[0])
+            pl, pt, cite = paper[nm]
+            table2[nm] = {"ms": ms, "mbps": bits7 / (ms * 1e-3) / 1e6, "paper_ms": pl, "paper_mbps": pt,
+                          "paper_cite": cite}
+        del H7g, y7g, Hd7g, s7g
     total_ms = float(per.sum())
     ms_step = total_ms / args.steps
     value = BITS_PER_STEP / (ms_step * 1e-3) / 1e9
@@ -444,7 +481,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Philox-4x32: i.i.d. Rayleigh "
                 "CN(0,1) channels, uniform Gray QAM, AWGN)", "config": workload_config(world),
-                "solvers": solvers, "centralized_baselines": baselines,
+                "solvers": solvers, "centralized_baselines": baselines, "paper_table2_context": table2,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "gpu_launches_per_step": launches / args.steps,
                 "consensus_rounds_per_step": (st1["consensus_rounds"] - st0["consensus_rounds"]) / args.steps,

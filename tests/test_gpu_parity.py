@@ -449,3 +449,19 @@ def test_centralized_rank_deficient_flags(env):
         ctx.sync()
     assert ei.value.status == 3
     ctx.sync()
+
+
+def test_centralized_host_pointers_match_device(env):
+    """Host-buffer calls (library-staged H2D/D2H) give the device results bit for bit."""
+    dbp, ctx, oracle, torch = env
+    cfg = synth.CONFIGS["C"].scaled(N=12)
+    H, y, _ = synth.uplink_frame(cfg)
+    xh, hh = dbp.detect_mmse(ctx, H, y, N0=cfg.N0, mod=cfg.mod)
+    xd, hd = dbp.detect_mmse(ctx, torch.from_numpy(H).cuda(), torch.from_numpy(y).cuda(), N0=cfg.N0, mod=cfg.mod)
+    ctx.sync()
+    assert np.array_equal(xh, xd.cpu().numpy()) and np.array_equal(hh, hd.cpu().numpy())
+    Hd, s = synth.downlink_frame(synth.CONFIGS["D"].scaled(N=12))
+    zh = dbp.precode_zf(ctx, Hd, s)
+    zd = dbp.precode_zf(ctx, torch.from_numpy(Hd).cuda(), torch.from_numpy(s).cuda())
+    ctx.sync()
+    assert np.array_equal(zh, zd.cpu().numpy())
