@@ -242,6 +242,26 @@ __device__ __forceinline__ void fold_unscale(f2x (&A)[Fold<UP>::NSLOT], f2x (&E)
     }
 }
 
+// fold_unscale followed by fold_mv_prep in one pass over the slots: the mat-vec form
+// of scale * M^{-1} (junk slots 0, diagonal halved) and (M^{-1} b)_r = d_r E_r.
+template <int UP, bool BORDER>
+__device__ __forceinline__ void fold_unscale_mv(f2x (&A)[Fold<UP>::NSLOT], f2x (&E)[4], const float (&dr)[4],
+                                                const float* dline, float scale, const int (&row)[4]) {
+    using F = Fold<UP>;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        const unsigned vmask = (2u << row[m]) - 1u, dmask = 1u << row[m];
+        const float base = -scale * dr[m];
+#pragma unroll
+        for (int t = 0; t < (m + 1) * F::L; ++t) {
+            const bool v = (vmask >> t) & 1u, d = (dmask >> t) & 1u;
+            const float sc = v ? (d ? 0.5f * base : base) * dline[t] : 0.f;
+            A[F::off(m) + t] = pk2(c_scale(upk2(A[F::off(m) + t]), sc));
+        }
+        if (BORDER) E[m] = pk2(c_scale(upk2(E[m]), dr[m]));
+    }
+}
+
 // Packed lower-triangle store of the valid slots.
 template <int UP>
 __device__ __forceinline__ void fold_store(float2* G, const f2x (&A)[Fold<UP>::NSLOT], const int (&row)[4]) {

@@ -323,8 +323,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
         fold_jacobi<UP, !DL>(A, E, dg, dr, dline, row);
         const bool ok = fold_sweep<UP, !DL>(A, E, pl, row, l);
         if (!ok && valid) atomicOr(a.flag, 1);
-        fold_unscale<UP, !DL>(A, E, dr, dline, DL ? 1.f : a.rho);   // UL: rho B^{-1} (eq. (3))
-        fold_mv_prep<UP>(A, row);
+        fold_unscale_mv<UP, !DL>(A, E, dr, dline, DL ? 1.f : a.rho, row);   // UL: rho B^{-1} (eq. (3))
 
         // consensus over the subcarrier's clusters, Sv[j] <- f(sum_c w_c): xor butterfly over the
         // warp's pairs, then the WPS warp partials in fixed order (deterministic)
