@@ -402,7 +402,7 @@ extern "C" dbp_status dbp_detect_admm(dbp_ctx* c, const dbp_dims* d, const dbp_c
         // a1-a8 in one per-subcarrier kernel (world == 1, supported shape)
         bool launched = false;
         KT("fused_ul", (launched = launch_fused_ul(L, sh.UP, false, dH, dy, sh.C, sh.N, sh.S, sh.U, T, rho, gamma,
-                                                   N0, Es, make_prox(reg, mod, sh.C, rho, N0, Es), modem_of(mod),
+                                                   make_prox(reg, mod, sh.C, rho, N0, Es), modem_of(mod),
                                                    static_cast<float2*>(k.io[2].dev),
                                                    static_cast<uint8_t*>(k.io[3].dev)), cudaGetLastError()));
         if (launched) {
@@ -489,7 +489,7 @@ extern "C" dbp_status dbp_detect_cg(dbp_ctx* c, const dbp_dims* d, const dbp_cf3
         bool launched = false;
         KT("fused_cg", (launched = launch_fused_ul(L, sh.UP, true, static_cast<const float2*>(k.io[0].dev),
                                                    static_cast<const float2*>(k.io[1].dev), sh.C, sh.N, sh.S, sh.U,
-                                                   T, rho, 1.f, 0.f, 1.f, Prox{}, modem_of(mod), a.x_hat, a.hard),
+                                                   T, rho, 1.f, Prox{}, modem_of(mod), a.x_hat, a.hard),
                         cudaGetLastError()));
         if (launched) {
             c->consensus_rounds += T + 1;

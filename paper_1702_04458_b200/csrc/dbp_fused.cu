@@ -496,14 +496,12 @@ static void fz_shape(int UP, int C, FuArgs& a) {
 }
 
 bool launch_fused_ul(const LaunchCtx& L, int UP, bool cg, const float2* H, const float2* y, int C, int N, int S, int U,
-                     int T, float rho, float gamma, float N0, float Es, Prox px, Modem md, float2* s_hat,
-                     uint8_t* hard) {
+                     int T, float rho, float gamma, Prox px, Modem md, float2* s_hat, uint8_t* hard) {
     if (!fused_ok(UP, C, N, 1, S, U)) return false;
     FuArgs a{};
     a.S = S; a.U = U; a.N = N; a.C = C; a.T = T;
     a.rho = rho; a.gamma = gamma; a.delta = cg ? 0.f : rho;
     a.s_hat = s_hat; a.hard = hard; a.px = px; a.md = md; a.flag = L.flag;
-    (void)N0; (void)Es;
     fz_shape(UP, C, a);
     switch (UP) {
         case 4: return cg ? launch_fz_t<4, 0>(L, H, y, a) : launch_fz_t<4, 1>(L, H, y, a);

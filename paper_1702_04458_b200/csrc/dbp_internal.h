@@ -53,8 +53,7 @@ bool make_map4(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint6
 // single-kernel per-subcarrier solvers (dbp_fused.cu), world == 1
 bool fused_ok(int UP, int C, int N, int J, int S, int U);
 bool launch_fused_ul(const LaunchCtx& L, int UP, bool cg, const float2* H, const float2* y, int C, int N, int S, int U,
-                     int T, float rho, float gamma, float N0, float Es, Prox px, Modem md, float2* s_hat,
-                     uint8_t* hard);
+                     int T, float rho, float gamma, Prox px, Modem md, float2* s_hat, uint8_t* hard);
 bool launch_fused_central(const LaunchCtx& L, int UP, bool dl, const float2* H, const float2* ys, int C, int N, int S,
                           int U, float reg, Modem md, float2* out, uint8_t* hard);
 bool launch_fused_dl(const LaunchCtx& L, int UP, const float2* Hd, const float2* s, int C, int N, int S, int U, int T,
