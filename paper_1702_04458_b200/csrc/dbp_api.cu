@@ -26,6 +26,12 @@ struct dbp_ctx {
     int64_t allreduce_calls = 0, allreduce_bytes = 0, consensus_rounds = 0;
     int force_split = 0;
     int no_fused = 0;
+    // device-side consensus (DBP_OPT_DEVICE_CONSENSUS): symmetric buffer, peer mappings
+    int xcons = 0;
+    void* xbuf = nullptr;
+    void* xpeer[8] = {nullptr};
+    int xcap = 0;
+    unsigned xround = 1;
     void* stage = nullptr;       // host-I/O staging (device)
     size_t stage_bytes = 0;
     void* iws = nullptr;         // internal workspace when ws == NULL
@@ -133,6 +139,9 @@ extern "C" dbp_status dbp_ctx_create(dbp_ctx** out, int device, int rank, int wo
 extern "C" dbp_status dbp_ctx_destroy(dbp_ctx* c) {
     if (!c) return DBP_OK;
     cudaSetDevice(c->device);
+    for (int r = 0; r < 8; ++r)
+        if (c->xpeer[r] && c->xpeer[r] != c->xbuf) cudaIpcCloseMemHandle(c->xpeer[r]);
+    if (c->xbuf) cudaFree(c->xbuf);
     if (c->comm) ncclCommDestroy(c->comm);
     cudaFree(c->d_flag);
     if (c->stage) cudaFree(c->stage);
@@ -148,6 +157,12 @@ extern "C" dbp_status dbp_set_option(dbp_ctx* c, int option, int64_t value) {
     if (option == DBP_OPT_FORCE_SPLIT) { c->force_split = value ? 1 : 0; return DBP_OK; }
     if (option == DBP_OPT_KERNEL_TIMING) { c->timing = value ? 1 : 0; return DBP_OK; }
     if (option == DBP_OPT_NO_FUSED) { c->no_fused = value ? 1 : 0; return DBP_OK; }
+    if (option == DBP_OPT_DEVICE_CONSENSUS) {
+        if (value < 0 || value > 2) return fail(DBP_ERR_INVALID_ARG, "device consensus mode %lld", (long long)value);
+        if (value && c->world > 8) return fail(DBP_ERR_UNSUPPORTED, "device consensus supports world <= 8");
+        c->xcons = (int)value;
+        return DBP_OK;
+    }
     return fail(DBP_ERR_INVALID_ARG, "unknown option %d", option);
 }
 
@@ -367,6 +382,65 @@ static Prox make_prox(int reg, int mod, int C, float rho, float N0, float Es) {
 
 static bool mod_ok(int mod) { return mod == DBP_BPSK || mod == DBP_QPSK || mod == DBP_QAM16 || mod == DBP_QAM64; }
 
+// ------------------------------------------------ device-side consensus (NEXT-1)
+// Symmetric per-rank buffer: part [2][8][cap][16] float2 + flag [8][cap] u32 (layout in dbp_internal.h).
+static size_t xbuf_bytes(int cap) { return (size_t)2 * 8 * cap * 16 * 8 + (size_t)8 * cap * 4; }
+
+// Collective when world > 1 (every rank calls it with the same N): allocate the buffer and map
+// every rank's buffer through CUDA IPC handles exchanged by one ncclAllGather.
+static dbp_status xbuf_ensure(dbp_ctx* c, int N, cudaStream_t s) {
+    if (c->xbuf && c->xcap >= N) return DBP_OK;
+    CU(cudaStreamSynchronize(s));
+    for (int r = 0; r < 8; ++r) {
+        if (c->xpeer[r] && c->xpeer[r] != c->xbuf) cudaIpcCloseMemHandle(c->xpeer[r]);
+        c->xpeer[r] = nullptr;
+    }
+    if (c->xbuf) cudaFree(c->xbuf);
+    c->xbuf = nullptr;
+    const int cap = std::max(N, 64);
+    CU(cudaMalloc(&c->xbuf, xbuf_bytes(cap)));
+    CU(cudaMemset(c->xbuf, 0, xbuf_bytes(cap)));
+    c->xcap = cap;
+    c->xround = 1;
+    c->xpeer[c->rank] = c->xbuf;
+    if (c->world > 1) {
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+        cudaIpcMemHandle_t h;
+        CU(cudaIpcGetMemHandle(&h, c->xbuf));
+        uint8_t* dh = nullptr;
+        CU(cudaMalloc(&dh, (size_t)64 * (c->world + 1)));
+        CU(cudaMemcpyAsync(dh + (size_t)64 * c->world, &h, 64, cudaMemcpyHostToDevice, s));
+        NC(ncclAllGather(dh + (size_t)64 * c->world, dh, 64, ncclUint8, c->comm, s));
+        std::vector<cudaIpcMemHandle_t> all(c->world);
+        CU(cudaMemcpyAsync(all.data(), dh, (size_t)64 * c->world, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        cudaFree(dh);
+        for (int r = 0; r < c->world; ++r) {
+            if (r == c->rank) continue;
+            CU(cudaIpcOpenMemHandle(&c->xpeer[r], all[r], cudaIpcMemLazyEnablePeerAccess));
+        }
+    }
+    return DBP_OK;
+}
+
+// Consensus-exchange arguments for one call with `rounds` rounds (nullptr: not in use).
+static bool xcons_active(const dbp_ctx* c) { return c->xcons == 2 || (c->xcons == 1 && c->world > 1); }
+
+static XArgs xargs_for(dbp_ctx* c, int rounds) {
+    XArgs x{};
+    x.on = 1;
+    x.world = c->world;
+    x.rank = c->rank;
+    x.cap = c->xcap;
+    for (int r = 0; r < c->world; ++r) {
+        x.part[r] = static_cast<float2*>(c->xpeer[r]);
+        x.flag[r] = reinterpret_cast<unsigned*>(static_cast<char*>(c->xpeer[r]) + (size_t)2 * 8 * c->xcap * 16 * 8);
+    }
+    x.base = c->xround;
+    c->xround += (unsigned)rounds + 2;      // round ids of different calls never overlap
+    return x;
+}
+
 // ============================================================ Algorithm 1
 extern "C" dbp_status dbp_detect_admm(dbp_ctx* c, const dbp_dims* d, const dbp_cf32* H, const dbp_cf32* y,
                                       float rho, float gamma, float N0, float Es, int reg, int mod, int32_t T,
@@ -398,13 +472,21 @@ extern "C" dbp_status dbp_detect_admm(dbp_ctx* c, const dbp_dims* d, const dbp_c
     float2* mf = reinterpret_cast<float2*>(k.ws + Lw.off[1]);
     LaunchCtx L{s, c->d_flag, &c->launches};
 
-    if (c->world == 1 && !c->force_split && !c->no_fused && fused_ok(sh.UP, sh.C, sh.N, sh.J, sh.S, sh.U)) {
-        // a1-a8 in one per-subcarrier kernel (world == 1, supported shape)
+    const bool xc_on = xcons_active(c) && T < 250;
+    if ((c->world == 1 || xc_on) && !c->force_split && !c->no_fused &&
+        fused_ok(sh.UP, sh.C_loc, sh.N, sh.J, sh.S, sh.U)) {
+        // a1-a8 in one per-subcarrier kernel (world == 1, or world > 1 with device-side consensus)
+        XArgs xa{};
+        if (xc_on) {
+            if ((st = xbuf_ensure(c, sh.N, s))) return st;
+            xa = xargs_for(c, T);
+        }
         bool launched = false;
-        KT("fused_ul", (launched = launch_fused_ul(L, sh.UP, false, dH, dy, sh.C, sh.N, sh.S, sh.U, T, rho, gamma,
+        KT("fused_ul", (launched = launch_fused_ul(L, sh.UP, false, dH, dy, sh.C_loc, sh.N, sh.S, sh.U, T, rho, gamma,
                                                    make_prox(reg, mod, sh.C, rho, N0, Es), modem_of(mod),
                                                    static_cast<float2*>(k.io[2].dev),
-                                                   static_cast<uint8_t*>(k.io[3].dev)), cudaGetLastError()));
+                                                   static_cast<uint8_t*>(k.io[3].dev), xc_on ? &xa : nullptr),
+                        cudaGetLastError()));
         if (launched) {
             c->consensus_rounds += T;
             return end_call(c, k, s);
@@ -557,11 +639,19 @@ extern "C" dbp_status dbp_beamform_admm(dbp_ctx* c, const dbp_dims* d, const dbp
     a.inv_c = (float)(1.0 / sh.C);
     a.eps = eps;
 
-    if (c->world == 1 && !c->force_split && !c->no_fused && fused_ok(sh.UP, sh.C, sh.N, sh.J, sh.S, sh.U)) {
-        // c1-c4 in one per-subcarrier kernel (world == 1, supported shape)
+    const bool xc_on = xcons_active(c) && T < 250;
+    if ((c->world == 1 || xc_on) && !c->force_split && !c->no_fused &&
+        fused_ok(sh.UP, sh.C_loc, sh.N, sh.J, sh.S, sh.U)) {
+        // c1-c4 in one per-subcarrier kernel (world == 1, or world > 1 with device-side consensus)
+        XArgs xa{};
+        if (xc_on) {
+            if ((st = xbuf_ensure(c, sh.N, s))) return st;
+            xa = xargs_for(c, T);
+        }
         bool launched = false;
-        KT("fused_dl", (launched = launch_fused_dl(L, sh.UP, a.Hd, a.s, sh.C, sh.N, sh.S, sh.U, T, rho, gamma,
-                                                   a.a0, eps, a.x), cudaGetLastError()));
+        KT("fused_dl", (launched = launch_fused_dl(L, sh.UP, a.Hd, a.s, sh.C_loc, sh.C, sh.N, sh.S, sh.U, T, rho,
+                                                   gamma, a.a0, eps, a.x, xc_on ? &xa : nullptr),
+                        cudaGetLastError()));
         if (launched) {
             c->consensus_rounds += T - 1;
             return end_call(c, k, s);

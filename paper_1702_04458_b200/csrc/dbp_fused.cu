@@ -62,6 +62,7 @@ struct FZ {
 };
 
 struct FuArgs {
+    XArgs xc;
     int S, U, N, C, T, WPS, NPC;
     float rho, gamma, delta;
     // UL outputs (SOLVER 0, 1)
@@ -331,7 +332,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
         // warp partials summed in fixed order by UP threads per subcarrier (deterministic) into
         // Sv; returns f(sum_c w_c) for the lane's rows, f = prox (UL) or identity (DL).  (A
         // one-barrier variant, every lane summing its own rows, measured slower.)
-        auto consensus = [&](const float2 (&w)[R], bool do_prox, float2 (&out)[R]) {
+        auto consensus = [&](int t, const float2 (&w)[R], bool do_prox, float2 (&out)[R]) {
             float2 ps[R];
 #pragma unroll
             for (int m = 0; m < R; ++m) {
@@ -347,11 +348,47 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                 for (int m = 0; m < R; ++m) Wp[warp * UP + row[m]] = ps[m];
             }
             __syncthreads();
-            if (tid < NPC * UP) {
-                const int jj = tid / UP, u = tid - jj * UP;
-                float2 acc = make_float2(0.f, 0.f);
-                for (int w2 = 0; w2 < WPS; ++w2) acc = c_add(acc, Wp[(jj * WPS + w2) * UP + u]);
-                Sv[tid] = do_prox ? prox(acc, a.px) : acc;
+            if (!a.xc.on) {
+                if (tid < NPC * UP) {
+                    const int jj = tid / UP, u = tid - jj * UP;
+                    float2 acc = make_float2(0.f, 0.f);
+                    for (int w2 = 0; w2 < WPS; ++w2) acc = c_add(acc, Wp[(jj * WPS + w2) * UP + u]);
+                    Sv[tid] = do_prox ? prox(acc, a.px) : acc;
+                }
+            } else {
+                // rank-local partial -> every rank's buffer, then the sum over ranks (NEXT-1)
+                const unsigned rid = a.xc.base + (unsigned)t;
+                const int par = rid & 1u;
+                const int n0 = (blockIdx.x + it * gridDim.x) * NPC;
+                if (tid < NPC * UP) {
+                    const int jj = tid / UP, u = tid - jj * UP;
+                    float2 acc = make_float2(0.f, 0.f);
+                    for (int w2 = 0; w2 < WPS; ++w2) acc = c_add(acc, Wp[(jj * WPS + w2) * UP + u]);
+                    if (n0 + jj < a.N) {
+                        const size_t o = ((size_t)(par * 8 + a.xc.rank) * a.xc.cap + n0 + jj) * UP + u;
+                        for (int r = 0; r < a.xc.world; ++r) st_relaxed_sys(a.xc.part[r] + o, acc);
+                    }
+                }
+                __threadfence_system();
+                __syncthreads();
+                if (tid < NPC && n0 + tid < a.N) {
+                    const size_t fo = (size_t)a.xc.rank * a.xc.cap + n0 + tid;
+                    for (int r = 0; r < a.xc.world; ++r) st_release_sys(a.xc.flag[r] + fo, rid);
+                    for (int p = 0; p < a.xc.world; ++p) {
+                        const unsigned* f = a.xc.flag[a.xc.rank] + (size_t)p * a.xc.cap + n0 + tid;
+                        while ((int)(ld_acquire_sys(f) - rid) < 0) {}
+                    }
+                }
+                __syncthreads();
+                if (tid < NPC * UP) {
+                    const int jj = tid / UP, u = tid - jj * UP;
+                    float2 acc = make_float2(0.f, 0.f);
+                    if (n0 + jj < a.N)
+                        for (int p = 0; p < a.xc.world; ++p)
+                            acc = c_add(acc, ld_relaxed_sys(a.xc.part[a.xc.rank] +
+                                                            ((size_t)(par * 8 + p) * a.xc.cap + n0 + jj) * UP + u));
+                    Sv[tid] = do_prox ? prox(acc, a.px) : acc;
+                }
             }
             __syncthreads();
 #pragma unroll
@@ -370,7 +407,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                 w[m] = yreg[m];
             }
             float2 sc[R];
-            consensus(w, true, sc);
+            consensus(1, w, true, sc);
             for (int t = 2; t <= a.T; ++t) {
                 float2 v[R], bv[R];
 #pragma unroll
@@ -384,7 +421,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                     z[m] = c_add(yreg[m], bv[m]);                                 // line 15
                     w[m] = c_add(z[m], lam[m]);                                   // line 17
                 }
-                consensus(w, true, sc);                                           // lines 18-19
+                consensus(t, w, true, sc);                                        // lines 18-19
             }
             if (warp == j * WPS && lane < UP) {
                 const int u = lane;
@@ -412,7 +449,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                     w[m] = c_sub(mm[m], lam[m]);                                   // line 12
                 }
                 float2 W[R];
-                consensus(w, false, W);                                            // line 13
+                consensus(t, w, false, W);                                         // line 13
                 float2 dv[R];
                 float nrm2 = 0.f;
 #pragma unroll
@@ -496,9 +533,10 @@ static void fz_shape(int UP, int C, FuArgs& a) {
 }
 
 bool launch_fused_ul(const LaunchCtx& L, int UP, bool cg, const float2* H, const float2* y, int C, int N, int S, int U,
-                     int T, float rho, float gamma, Prox px, Modem md, float2* s_hat, uint8_t* hard) {
+                     int T, float rho, float gamma, Prox px, Modem md, float2* s_hat, uint8_t* hard, const XArgs* xc) {
     if (!fused_ok(UP, C, N, 1, S, U)) return false;
     FuArgs a{};
+    if (xc && !cg) a.xc = *xc;
     a.S = S; a.U = U; a.N = N; a.C = C; a.T = T;
     a.rho = rho; a.gamma = gamma; a.delta = cg ? 0.f : rho;
     a.s_hat = s_hat; a.hard = hard; a.px = px; a.md = md; a.flag = L.flag;
@@ -511,13 +549,14 @@ bool launch_fused_ul(const LaunchCtx& L, int UP, bool cg, const float2* H, const
     }
 }
 
-bool launch_fused_dl(const LaunchCtx& L, int UP, const float2* Hd, const float2* s, int C, int N, int S, int U, int T,
-                     float rho, float gamma, float a0, float eps, float2* x) {
+bool launch_fused_dl(const LaunchCtx& L, int UP, const float2* Hd, const float2* s, int C, int C_glob, int N, int S,
+                     int U, int T, float rho, float gamma, float a0, float eps, float2* x, const XArgs* xc) {
     if (!fused_ok(UP, C, N, 1, S, U)) return false;
     FuArgs a{};
+    if (xc) a.xc = *xc;
     a.S = S; a.U = U; a.N = N; a.C = C; a.T = T;
     a.rho = rho; a.gamma = gamma; a.delta = 1.f / rho;
-    a.s = s; a.x = x; a.rho_inv = 1.f / rho; a.a0 = a0; a.inv_c = 1.f / (float)C; a.eps = eps; a.flag = L.flag;
+    a.s = s; a.x = x; a.rho_inv = 1.f / rho; a.a0 = a0; a.inv_c = 1.f / (float)C_glob; a.eps = eps; a.flag = L.flag;
     fz_shape(UP, C, a);
     switch (UP) {
         case 4: return launch_fz_t<4, 2>(L, Hd, nullptr, a);

@@ -50,14 +50,30 @@ bool make_map3(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint6
                uint32_t b2);
 bool make_map4(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3, uint32_t b0,
                uint32_t b1, uint32_t b2, uint32_t b3);
-// single-kernel per-subcarrier solvers (dbp_fused.cu), world == 1
+// Device-side consensus over ranks (NEXT-1, DBP_OPT_DEVICE_CONSENSUS): every rank owns one
+// symmetric buffer, mapped into all ranks (CUDA IPC over NVLink):
+//   part [2 round parity][8 ranks][xcap subcarriers][UP] float2,  flag [8 ranks][xcap] u32.
+// A round publishes the CTA's local partial into every rank's part[par][my_rank][n], fences,
+// raises flag[my_rank][n] = round id in every rank, waits on its own flag[p][n] for all p and sums
+// part[par][p][n] in rank order (deterministic, identical on every rank).  Round ids grow
+// monotonically across calls (host counter), so nothing is ever reset.
+struct XArgs {
+    float2* part[8];
+    unsigned* flag[8];
+    int world, rank, cap, on;
+    unsigned base;                       // round id of this call's round t is base + t
+};
+
+// single-kernel per-subcarrier solvers (dbp_fused.cu): world == 1, or world > 1 with the
+// device-side consensus (xc != nullptr, xc->on)
 bool fused_ok(int UP, int C, int N, int J, int S, int U);
 bool launch_fused_ul(const LaunchCtx& L, int UP, bool cg, const float2* H, const float2* y, int C, int N, int S, int U,
-                     int T, float rho, float gamma, Prox px, Modem md, float2* s_hat, uint8_t* hard);
+                     int T, float rho, float gamma, Prox px, Modem md, float2* s_hat, uint8_t* hard,
+                     const XArgs* xc = nullptr);
 bool launch_fused_central(const LaunchCtx& L, int UP, bool dl, const float2* H, const float2* ys, int C, int N, int S,
                           int U, float reg, Modem md, float2* out, uint8_t* hard);
-bool launch_fused_dl(const LaunchCtx& L, int UP, const float2* Hd, const float2* s, int C, int N, int S, int U, int T,
-                     float rho, float gamma, float a0, float eps, float2* x);
+bool launch_fused_dl(const LaunchCtx& L, int UP, const float2* Hd, const float2* s, int C, int C_glob, int N, int S,
+                     int U, int T, float rho, float gamma, float a0, float eps, float2* x, const XArgs* xc = nullptr);
 size_t prelr_smem(int UP, int S, int U, int J, bool ul);
 bool launch_prefold(const LaunchCtx& L, int UP, int mode, const float2* H, const float2* y, int S, int U, int J,
                     long npairs, float delta, float2* Gout, float2* vout);

@@ -465,3 +465,34 @@ def test_centralized_host_pointers_match_device(env):
     zd = dbp.precode_zf(ctx, torch.from_numpy(Hd).cuda(), torch.from_numpy(s).cuda())
     ctx.sync()
     assert np.array_equal(zh, zd.cpu().numpy())
+
+
+# ------------------------------------------------------- device-side consensus (NEXT-1)
+def test_device_consensus_self_peer(env):
+    """DBP_OPT_DEVICE_CONSENSUS = 2 at world 1: the fused kernels publish each round's partial
+    into the rank's symmetric buffer, raise and wait on the flags and sum over the (single) rank
+    -- the device protocol of the multi-GPU consensus without inter-process waiting.  Results
+    are bitwise those of the plain fused path; repeated calls keep the round ids monotonic and
+    a larger N regrows the buffer."""
+    dbp, ctx, oracle, torch = env
+    cfgs = [synth.CONFIGS["C"].scaled(N=30), synth.CONFIGS["C"].scaled(N=75), synth.CONFIGS["A"]]
+    for cfg in cfgs:
+        H, y, _ = synth.uplink_frame(cfg)
+        Hd, s = synth.downlink_frame(cfg.scaled(algo="admm_dl"))
+        Hg, yg = torch.from_numpy(H).cuda(), torch.from_numpy(y).cuda()
+        Hdg, sg = torch.from_numpy(Hd).cuda(), torch.from_numpy(s).cuda()
+        ref_s, ref_h = dbp.detect_admm(ctx, Hg, yg, N0=cfg.N0, mod=cfg.mod, T=cfg.T)
+        ref_x = dbp.beamform_admm(ctx, Hdg, sg, T=cfg.T, eps=0.2)
+        ctx.sync()
+        ctx.set_option(dbp.OPT_DEVICE_CONSENSUS, 2)
+        try:
+            for _ in range(3):
+                s1, h1 = dbp.detect_admm(ctx, Hg, yg, N0=cfg.N0, mod=cfg.mod, T=cfg.T)
+                x1 = dbp.beamform_admm(ctx, Hdg, sg, T=cfg.T, eps=0.2)
+                ctx.sync()
+                assert torch.equal(s1, ref_s) and torch.equal(h1, ref_h)
+                assert torch.equal(x1, ref_x)
+        finally:
+            ctx.set_option(dbp.OPT_DEVICE_CONSENSUS, 0)
+        s_or, _ = oracle.detect_admm(H, y, N0=cfg.N0, mod=cfg.mod, T=cfg.T)
+        assert rel(s1.cpu().numpy(), s_or) < TOL
