@@ -383,8 +383,8 @@ static Prox make_prox(int reg, int mod, int C, float rho, float N0, float Es) {
 static bool mod_ok(int mod) { return mod == DBP_BPSK || mod == DBP_QPSK || mod == DBP_QAM16 || mod == DBP_QAM64; }
 
 // ------------------------------------------------ device-side consensus (NEXT-1)
-// Symmetric per-rank buffer: part [2][8][cap][16] float2 + flag [8][cap] u32 (layout in dbp_internal.h).
-static size_t xbuf_bytes(int cap) { return (size_t)2 * 8 * cap * 16 * 8 + (size_t)8 * cap * 4; }
+// Symmetric per-rank buffer: part [2][8][cap][16] uint4 (layout in dbp_internal.h).
+static size_t xbuf_bytes(int cap) { return (size_t)2 * 8 * cap * 16 * 16; }
 
 // Collective when world > 1 (every rank calls it with the same N): allocate the buffer and map
 // every rank's buffer through CUDA IPC handles exchanged by one ncclAllGather.
@@ -432,10 +432,7 @@ static XArgs xargs_for(dbp_ctx* c, int rounds) {
     x.world = c->world;
     x.rank = c->rank;
     x.cap = c->xcap;
-    for (int r = 0; r < c->world; ++r) {
-        x.part[r] = static_cast<float2*>(c->xpeer[r]);
-        x.flag[r] = reinterpret_cast<unsigned*>(static_cast<char*>(c->xpeer[r]) + (size_t)2 * 8 * c->xcap * 16 * 8);
-    }
+    for (int r = 0; r < c->world; ++r) x.part[r] = static_cast<uint4*>(c->xpeer[r]);
     x.base = c->xround;
     c->xround += (unsigned)rounds + 2;      // round ids of different calls never overlap
     return x;

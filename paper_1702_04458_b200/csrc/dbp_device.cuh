@@ -144,22 +144,20 @@ __device__ __forceinline__ void tma_load4(void* dst, const void* map, int c0, in
           "r"(smem_u32(bar))
         : "memory");
 }
-// System-scope loads/stores for the cross-GPU consensus (peer memory over NVLink).
-__device__ __forceinline__ void st_relaxed_sys(float2* p, float2 v) {
-    asm volatile("st.relaxed.sys.global.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
+// Cross-GPU consensus words (peer memory over NVLink), NCCL-LL style: a complex value travels
+// as two 8-byte words {re, id} {im, id}; 8-byte stores are single-copy atomic, so a reader that
+// sees both ids equal to the round id it waits for has that round's value.
+__device__ __forceinline__ void st_ll_sys(uint4* p, float2 v, unsigned id) {
+    asm volatile("st.relaxed.sys.global.v4.u32 [%0], {%1, %2, %3, %4};"
+                 ::"l"(p), "r"(__float_as_uint(v.x)), "r"(id), "r"(__float_as_uint(v.y)), "r"(id) : "memory");
 }
-__device__ __forceinline__ float2 ld_relaxed_sys(const float2* p) {
-    float2 v;
-    asm volatile("ld.relaxed.sys.global.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
+__device__ __forceinline__ float2 ld_ll_sys(const uint4* p, unsigned id) {
+    unsigned a, b, c, d;
+    do {
+        asm volatile("ld.relaxed.sys.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(p) : "memory");
+    } while (b != id || d != id);
+    return make_float2(__uint_as_float(a), __uint_as_float(c));
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 

@@ -356,7 +356,9 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                     Sv[tid] = do_prox ? prox(acc, a.px) : acc;
                 }
             } else {
-                // rank-local partial -> every rank's buffer, then the sum over ranks (NEXT-1)
+                // rank-local partial -> every rank's buffer, then the sum over ranks (NEXT-1).
+                // LL protocol: each 8-byte word carries its own round id ({re, rid}, {im, rid}), so
+                // a reader polls its entry until both ids match -- no fence, no separate flag.
                 const unsigned rid = a.xc.base + (unsigned)t;
                 const int par = rid & 1u;
                 const int n0 = (blockIdx.x + it * gridDim.x) * NPC;
@@ -364,30 +366,15 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                     const int jj = tid / UP, u = tid - jj * UP;
                     float2 acc = make_float2(0.f, 0.f);
                     for (int w2 = 0; w2 < WPS; ++w2) acc = c_add(acc, Wp[(jj * WPS + w2) * UP + u]);
+                    float2 sum = make_float2(0.f, 0.f);
                     if (n0 + jj < a.N) {
                         const size_t o = ((size_t)(par * 8 + a.xc.rank) * a.xc.cap + n0 + jj) * UP + u;
-                        for (int r = 0; r < a.xc.world; ++r) st_relaxed_sys(a.xc.part[r] + o, acc);
+                        for (int r = 0; r < a.xc.world; ++r) st_ll_sys(a.xc.part[r] + o, acc, rid);
+                        for (int p = 0; p < a.xc.world; ++p)        // rank order: identical sums everywhere
+                            sum = c_add(sum, ld_ll_sys(a.xc.part[a.xc.rank] +
+                                                       ((size_t)(par * 8 + p) * a.xc.cap + n0 + jj) * UP + u, rid));
                     }
-                }
-                __threadfence_system();
-                __syncthreads();
-                if (tid < NPC && n0 + tid < a.N) {
-                    const size_t fo = (size_t)a.xc.rank * a.xc.cap + n0 + tid;
-                    for (int r = 0; r < a.xc.world; ++r) st_release_sys(a.xc.flag[r] + fo, rid);
-                    for (int p = 0; p < a.xc.world; ++p) {
-                        const unsigned* f = a.xc.flag[a.xc.rank] + (size_t)p * a.xc.cap + n0 + tid;
-                        while ((int)(ld_acquire_sys(f) - rid) < 0) {}
-                    }
-                }
-                __syncthreads();
-                if (tid < NPC * UP) {
-                    const int jj = tid / UP, u = tid - jj * UP;
-                    float2 acc = make_float2(0.f, 0.f);
-                    if (n0 + jj < a.N)
-                        for (int p = 0; p < a.xc.world; ++p)
-                            acc = c_add(acc, ld_relaxed_sys(a.xc.part[a.xc.rank] +
-                                                            ((size_t)(par * 8 + p) * a.xc.cap + n0 + jj) * UP + u));
-                    Sv[tid] = do_prox ? prox(acc, a.px) : acc;
+                    Sv[tid] = do_prox ? prox(sum, a.px) : sum;
                 }
             }
             __syncthreads();

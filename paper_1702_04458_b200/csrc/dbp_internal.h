@@ -52,14 +52,14 @@ bool make_map4(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint6
                uint32_t b1, uint32_t b2, uint32_t b3);
 // Device-side consensus over ranks (NEXT-1, DBP_OPT_DEVICE_CONSENSUS): every rank owns one
 // symmetric buffer, mapped into all ranks (CUDA IPC over NVLink):
-//   part [2 round parity][8 ranks][xcap subcarriers][UP] float2,  flag [8 ranks][xcap] u32.
-// A round publishes the CTA's local partial into every rank's part[par][my_rank][n], fences,
-// raises flag[my_rank][n] = round id in every rank, waits on its own flag[p][n] for all p and sums
-// part[par][p][n] in rank order (deterministic, identical on every rank).  Round ids grow
-// monotonically across calls (host counter), so nothing is ever reset.
+//   part [2 round parity][8 ranks][cap subcarriers][16 users] uint4 = {re, id, im, id}.
+// A round stores the CTA's local partial into every rank's part[par][my_rank][n] with the round
+// id in both 8-byte halves (LL protocol), then polls its own part[par][p][n] for every p until
+// both ids match and sums in rank order (deterministic, identical on every rank).  Round ids
+// grow monotonically across calls (host counter), so nothing is ever reset; parity double
+// buffering keeps a fast rank's round r + 2 from overwriting round r before it is read.
 struct XArgs {
-    float2* part[8];
-    unsigned* flag[8];
+    uint4* part[8];
     int world, rank, cap, on;
     unsigned base;                       // round id of this call's round t is base + t
 };

@@ -1,8 +1,9 @@
 """CPU model of the device-side consensus protocol of k_fused (NEXT-1,
 DBP_OPT_DEVICE_CONSENSUS; dbp_internal.h XArgs): W ranks x several subcarriers, each
-rank's round r publishes its partial into EVERY rank's part[r & 1][my_rank][n], raises
-flag[my_rank][n] = r in every rank, waits until its own flag[p][n] >= r for all p, then sums
-part[r & 1][p][n] in rank order.  Round ids grow across calls (base += rounds + 2).
+rank's round r publishes its partial into EVERY rank's part[r & 1][my_rank][n] tagged with
+the round id (on the GPU the id rides in each 8-byte word, NCCL-LL style; here a flag array
+models the tag), waits until its own part[r & 1][p][n] carries id r for all p, then sums in
+rank order.  Round ids grow across calls (base += rounds + 2).
 
 Threads with random delays stand in for the GPUs' CTAs; the test checks that every read
 sees exactly the partials of the round it waited for (no overwrite by a faster rank's round
