@@ -228,6 +228,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-table2", action="store_true")
+    ap.add_argument("--device-consensus", action="store_true",
+                    help="world > 1: consensus inside the fused kernels over NVLink (DBP_OPT_DEVICE_CONSENSUS)")
     ap.add_argument("--ref-subcarriers", type=int, default=60)
     args = ap.parse_args()
 
@@ -253,6 +255,8 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     ctx = dbp.Context(device=local, rank=rank, world=world, unique_id=uid)
+    if args.device_consensus:
+        ctx.set_option(dbp.OPT_DEVICE_CONSENSUS, 1)
 
     c0, c1 = synth.cluster_range(UL.C, rank, world)
     H, y, _ = synth.uplink_frame(UL, c0, c1)

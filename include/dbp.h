@@ -100,11 +100,11 @@ typedef enum {
      * inverse, every consensus round and the output on chip); 1: use the
      * preprocessing + iteration kernels instead (same results up to rounding). */
     DBP_OPT_NO_FUSED = 3,
-    /* Device-side consensus (NEXT-1; ADMM-UL and ADMM-DL).  0 (default): world > 1 uses the split
+    /* Device-side consensus (NEXT-1; ADMM-UL, CG-UL, ADMM-DL).  0 (default): world > 1 uses the split
      * path, one ncclAllReduce per round.  1: at world > 1 each rank runs the fused per-subcarrier
      * kernel on its own clusters and the rounds' partial sums cross GPUs inside that kernel, by
-     * peer stores into a symmetric buffer (CUDA IPC over NVLink) and per-(rank, subcarrier)
-     * flags; no collective per round.  Needs peer access between all ranks' GPUs (creating the
+     * peer stores of round-tagged words into a symmetric buffer (CUDA IPC over NVLink, LL
+     * protocol); no collective per round.  Needs peer access between all ranks' GPUs (creating the
      * buffer is collective: every rank must make the same call).  2: as 1, and also at world == 1
      * against the rank's own buffer (a self-peer exercise of the device protocol for testing).
      * Unverified across GPUs in round 1 (single-GPU environment). */

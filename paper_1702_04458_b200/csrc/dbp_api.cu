@@ -563,12 +563,20 @@ extern "C" dbp_status dbp_detect_cg(dbp_ctx* c, const dbp_dims* d, const dbp_cf3
     a.N = sh.N; a.J = sh.J; a.U = sh.U; a.T = T; a.rho = rho;
     a.md = modem_of(mod);
 
-    if (c->world == 1 && !c->force_split && !c->no_fused && fused_ok(sh.UP, sh.C, sh.N, sh.J, sh.S, sh.U)) {
-        // b1-b5 in one per-subcarrier kernel (world == 1, supported shape)
+    const bool xc_on = xcons_active(c) && T < 250;
+    if ((c->world == 1 || xc_on) && !c->force_split && !c->no_fused &&
+        fused_ok(sh.UP, sh.C_loc, sh.N, sh.J, sh.S, sh.U)) {
+        // b1-b5 in one per-subcarrier kernel (world == 1, or world > 1 with device-side consensus)
+        XArgs xa{};
+        if (xc_on) {
+            if ((st = xbuf_ensure(c, sh.N, s))) return st;
+            xa = xargs_for(c, T + 1);
+        }
         bool launched = false;
         KT("fused_cg", (launched = launch_fused_ul(L, sh.UP, true, static_cast<const float2*>(k.io[0].dev),
-                                                   static_cast<const float2*>(k.io[1].dev), sh.C, sh.N, sh.S, sh.U,
-                                                   T, rho, 1.f, Prox{}, modem_of(mod), a.x_hat, a.hard),
+                                                   static_cast<const float2*>(k.io[1].dev), sh.C_loc, sh.N, sh.S,
+                                                   sh.U, T, rho, 1.f, Prox{}, modem_of(mod), a.x_hat, a.hard,
+                                                   xc_on ? &xa : nullptr),
                         cudaGetLastError()));
         if (launched) {
             c->consensus_rounds += T + 1;

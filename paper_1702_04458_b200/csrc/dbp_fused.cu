@@ -292,7 +292,20 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                         for (int jc = 0; jc < UP; ++jc)
                             grow[jc] = jc <= u ? Gj[(u * (u + 1)) / 2 + jc] : c_conj(Gj[(jc * (jc + 1)) / 2 + u]);
                         float2* P = pl - q * (UP + 2) + (lane / UP) * (UP + 2);       // a per-group line
-                        float2 r = Sv[warp * UP + u];           // line 6: r = y^MRC, p = r, x = 0
+                        // device-side consensus (NEXT-1): sum of v over ranks for round t (LL words)
+                        auto xsum = [&](int t, float2 v) {
+                            if (!a.xc.on || nn >= a.N) return v;
+                            const unsigned rid = a.xc.base + (unsigned)t;
+                            const int par = rid & 1u;
+                            const size_t o = ((size_t)(par * 8 + a.xc.rank) * a.xc.cap + nn) * UP + u;
+                            for (int rk = 0; rk < a.xc.world; ++rk) st_ll_sys(a.xc.part[rk] + o, v, rid);
+                            float2 sum = make_float2(0.f, 0.f);
+                            for (int pk = 0; pk < a.xc.world; ++pk)
+                                sum = c_add(sum, ld_ll_sys(a.xc.part[a.xc.rank] +
+                                                           ((size_t)(par * 8 + pk) * a.xc.cap + nn) * UP + u, rid));
+                            return sum;
+                        };
+                        float2 r = xsum(1, Sv[warp * UP + u]);  // line 6: r = y^MRC (consensus), p = r, x = 0
                         float2 p = r;
                         x = make_float2(0.f, 0.f);
                         float rr = group_sum<UP>(c_norm2(r));
@@ -305,6 +318,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                             float2 w = make_float2(0.f, 0.f);                            // lines 9-11: w = G p
 #pragma unroll
                             for (int jc = 0; jc < UP; ++jc) c_fma(w, grow[jc], pv[jc]);
+                            w = xsum(2 + t, w);                                          // line 11 consensus
                             cg_update<UP>(x, r, p, rr, w, a.rho);                        // lines 13-18
                         }
                     }
@@ -523,7 +537,7 @@ bool launch_fused_ul(const LaunchCtx& L, int UP, bool cg, const float2* H, const
                      int T, float rho, float gamma, Prox px, Modem md, float2* s_hat, uint8_t* hard, const XArgs* xc) {
     if (!fused_ok(UP, C, N, 1, S, U)) return false;
     FuArgs a{};
-    if (xc && !cg) a.xc = *xc;
+    if (xc) a.xc = *xc;
     a.S = S; a.U = U; a.N = N; a.C = C; a.T = T;
     a.rho = rho; a.gamma = gamma; a.delta = cg ? 0.f : rho;
     a.s_hat = s_hat; a.hard = hard; a.px = px; a.md = md; a.flag = L.flag;

@@ -483,15 +483,18 @@ def test_device_consensus_self_peer(env):
         Hdg, sg = torch.from_numpy(Hd).cuda(), torch.from_numpy(s).cuda()
         ref_s, ref_h = dbp.detect_admm(ctx, Hg, yg, N0=cfg.N0, mod=cfg.mod, T=cfg.T)
         ref_x = dbp.beamform_admm(ctx, Hdg, sg, T=cfg.T, eps=0.2)
+        ref_c, ref_ch = dbp.detect_cg(ctx, Hg, yg, rho=cfg.N0, mod=cfg.mod, T=cfg.T)
         ctx.sync()
         ctx.set_option(dbp.OPT_DEVICE_CONSENSUS, 2)
         try:
             for _ in range(3):
                 s1, h1 = dbp.detect_admm(ctx, Hg, yg, N0=cfg.N0, mod=cfg.mod, T=cfg.T)
                 x1 = dbp.beamform_admm(ctx, Hdg, sg, T=cfg.T, eps=0.2)
+                c1, ch1 = dbp.detect_cg(ctx, Hg, yg, rho=cfg.N0, mod=cfg.mod, T=cfg.T)
                 ctx.sync()
                 assert torch.equal(s1, ref_s) and torch.equal(h1, ref_h)
                 assert torch.equal(x1, ref_x)
+                assert torch.equal(c1, ref_c) and torch.equal(ch1, ref_ch)
         finally:
             ctx.set_option(dbp.OPT_DEVICE_CONSENSUS, 0)
         s_or, _ = oracle.detect_admm(H, y, N0=cfg.N0, mod=cfg.mod, T=cfg.T)
