@@ -217,8 +217,30 @@ __global__ void __launch_bounds__(512) k_bf_gj(DlArgs a) {
             __syncthreads();
         }
         const float2 r = row_apply<UP>(R, buf, i, qv);                  // B^{-1} q
-        bf_output<UP>(a.Hd + pair * (size_t)a.U * a.S, buf, i, r, a.U, a.S,
-                      a.x + (pair * a.J + jj) * a.S, valid);            // line 20 / output
+        if (a.J == 1) {
+            bf_output<UP>(a.Hd + pair * (size_t)a.U * a.S, buf, i, r, a.U, a.S,
+                          a.x + (pair * a.J + jj) * a.S, valid);        // line 20 / output
+        } else {
+            a.m[(pair * a.J + jj) * UP + i] = r;                        // all symbols' r, then one H_c pass
+        }
+    }
+    if (a.J > 1) {
+        // x_c[j] = H_c^H r_j for every symbol j from ONE pass over H_c: lane i takes antennas
+        // i, i+UP, ..., loads the antenna's column of H_c once and reuses it for all J symbols
+        __syncwarp();
+        const float2* Hp = a.Hd + pair * (size_t)a.U * a.S;
+        const float2* rp = a.m + pair * a.J * UP;
+        for (int s = i; s < a.S; s += UP) {
+            float2 h[UP];
+#pragma unroll
+            for (int u = 0; u < UP; ++u) h[u] = u < a.U ? __ldg(Hp + (size_t)u * a.S + s) : make_float2(0.f, 0.f);
+            for (int jj = 0; jj < a.J; ++jj) {
+                float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int u = 0; u < UP; ++u) c_fmac(acc, h[u], rp[jj * UP + u]);
+                if (valid) a.x[(pair * a.J + jj) * a.S + s] = acc;
+            }
+        }
     }
 }
 

@@ -57,7 +57,7 @@ struct PF : Fold<UP> {
 template <int UP, bool DL, int MODE>
 struct PFL {
     using P = PF<UP>;
-    using G = FoldStage<UP, DL, !DL && MODE != 2>;
+    using G = FoldStage<UP, DL, !DL && (MODE == 0 || MODE == 1)>;
     static constexpr int PLN = P::PW * (UP + 2);                // pivot lines (float2)
     static constexpr int WREG = (P::NST * G::STG + PLN * 8 + P::PW * UP * 4 + 127) / 128 * 128;
     static constexpr size_t SMEM = 128 + (size_t)P::WARPS * WREG;
@@ -79,7 +79,8 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
     using Q = PFL<UP, DL, MODE>;
     using G = typename Q::G;
     constexpr int L = P::L, PW = P::PW, SC = P::SC, NST = P::NST, R = P::R;
-    constexpr bool MF = !DL && MODE != 2, INV = MODE != 0;
+    // MODE 0 Gram + b, 1 inverse + y^reg, 2 inverse (DL), 4 Gram only (UL, N_sym > 1), 5 inverse only (UL)
+    constexpr bool MF = !DL && (MODE == 0 || MODE == 1), INV = MODE == 1 || MODE == 2 || MODE == 5;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw) + warp * NST;
@@ -185,7 +186,7 @@ static bool launch_pf_t(const LaunchCtx& L, const float2* H, const float2* y, Pf
     CUtensorMap tmH{}, tmY{};
     if (!DL) {
         if (!make_map3(&tmH, H, a.U, a.S, a.npairs, UP + 2, P::SC, P::PW)) return false;
-        if (MODE != 2 && !make_map3(&tmY, y, a.S, 1, a.npairs, P::SC, 1, P::PW)) return false;
+        if ((MODE == 0 || MODE == 1) && !make_map3(&tmY, y, a.S, 1, a.npairs, P::SC, 1, P::PW)) return false;
     } else {
         if (!make_map3(&tmH, H, a.S, a.U, a.npairs, P::SC, UP + 1, P::PW)) return false;
     }
@@ -231,6 +232,8 @@ bool launch_prefold(const LaunchCtx& L, int UP, int mode, const float2* H, const
         if (mode == 0) return launch_pf_t<UPc, false, 0>(L, H, y, a);     \
         if (mode == 1) return launch_pf_t<UPc, false, 1>(L, H, y, a);     \
         if (mode == 3) return launch_pf_t<UPc, true, 0>(L, H, y, a);      \
+        if (mode == 4) return launch_pf_t<UPc, false, 4>(L, H, y, a);     \
+        if (mode == 5) return launch_pf_t<UPc, false, 5>(L, H, y, a);     \
         return launch_pf_t<UPc, true, 2>(L, H, y, a);
         DBP_PF_CASE(4)
         DBP_PF_CASE(8)

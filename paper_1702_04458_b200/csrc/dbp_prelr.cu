@@ -261,12 +261,61 @@ size_t prelr_smem(int UP, int S, int U, int J, bool ul) {
     return r;
 }
 
+// N_sym > 1 companion of k_prefold modes 4 / 5: b_j = H_c^H y_cj for every symbol j (lane u of a
+// UP-lane group takes column u of H_c), and with YREG y^reg_j = G^{-1} b_j (Alg. 1 line 8) by a
+// lane-row mat-vec with row u of the packed inverse k_prefold wrote.
+template <int UP, bool YREG>
+__global__ void __launch_bounds__(256) k_mf_yreg(const float2* __restrict__ H, const float2* __restrict__ y,
+                                                 const float2* __restrict__ Ginv, int S, int U, int J, long npairs,
+                                                 float2* __restrict__ out) {
+    __shared__ __align__(16) float2 sbuf[256 / UP][UP];
+    const int g = threadIdx.x / UP, i = threadIdx.x % UP;
+    const long p = (long)blockIdx.x * (256 / UP) + g;
+    const bool valid = p < npairs;
+    const long pp = valid ? p : npairs - 1;
+    float2 R[UP];
+    if (YREG) load_herm_row<UP>(Ginv + (size_t)pp * tri(UP), i, R);
+    const float2* Hp = H + (size_t)pp * S * U;
+    const float2* yp = y + (size_t)pp * J * S;
+    constexpr int JB = 8;                         // symbols per pass: H_c is read once per JB symbols
+    for (int j0 = 0; j0 < J; j0 += JB) {
+        float2 b[JB];
+#pragma unroll
+        for (int k = 0; k < JB; ++k) b[k] = make_float2(0.f, 0.f);
+        if (i < U) {
+#pragma unroll 4
+            for (int s = 0; s < S; ++s) {
+                const float2 h = __ldg(Hp + (size_t)s * U + i);
+#pragma unroll
+                for (int k = 0; k < JB; ++k)
+                    if (j0 + k < J) c_fmac(b[k], h, __ldg(yp + (size_t)(j0 + k) * S + s));
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < JB; ++k) {
+            if (j0 + k >= J) break;
+            const float2 v = YREG ? row_apply<UP>(R, sbuf[g], i, b[k]) : b[k];
+            if (valid) out[((size_t)p * J + j0 + k) * UP + i] = v;
+        }
+    }
+}
+
 // mode: 0 = Gram + H^H y (CG), 1 = inverse + y^reg (ADMM-UL), 2 = inverse (ADMM-DL, H = H^d),
 //       3 = Gram only (ZF-DL, H = H^d)
 cudaError_t launch_prelr(const LaunchCtx& L, int UP, int mode, const float2* H, const float2* y, int S, int U, int J,
                          long npairs, float delta, float2* Gout, float2* vout) {
     if (npairs <= 0) return cudaSuccess;
     if (launch_prefold(L, UP, mode, H, y, S, U, J, npairs, delta, Gout, vout)) return cudaGetLastError();
+    if (J > 1 && (mode == 0 || mode == 1) &&
+        launch_prefold(L, UP, mode == 0 ? 4 : 5, H, y, S, U, J, npairs, delta, Gout, vout)) {
+        // N_sym > 1: folded Gram (+ sweep) without the matched filter, then b_j (+ y^reg_j) per symbol
+        const int grid = (int)((npairs + 256 / UP - 1) / (256 / UP));
+        DBP_DISPATCH_UP(UP,
+            if (mode == 1) k_mf_yreg<UPc, true><<<grid, 256, 0, L.stream>>>(H, y, Gout, S, U, J, npairs, vout);
+            else k_mf_yreg<UPc, false><<<grid, 256, 0, L.stream>>>(H, y, Gout, S, U, J, npairs, vout));
+        L.count(1);
+        return cudaGetLastError();
+    }
     LrArgs a{H, y, S, U, J, 0, npairs, delta, Gout, vout, L.flag};
     cudaError_t e = cudaSuccess;
     DBP_DISPATCH_UP(UP,
