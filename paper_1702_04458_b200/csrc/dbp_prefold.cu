@@ -73,7 +73,7 @@ struct PfArgs {
 };
 
 template <int UP, bool DL, int MODE>
-__global__ void __launch_bounds__(128, 3)
+__global__ void __launch_bounds__(128, UP >= 32 ? 2 : 3)
 k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmY, PfArgs a) {
     using P = PF<UP>;
     using Q = PFL<UP, DL, MODE>;
@@ -213,6 +213,7 @@ size_t prefold_smem(int UP, bool dl, int mode) {
         case 4: r = dl ? PFL<4, true, 2>::SMEM : PFL<4, false, 1>::SMEM; break;
         case 8: r = dl ? PFL<8, true, 2>::SMEM : PFL<8, false, 1>::SMEM; break;
         case 16: r = dl ? PFL<16, true, 2>::SMEM : PFL<16, false, 1>::SMEM; break;
+        case 32: r = dl ? PFL<32, true, 2>::SMEM : PFL<32, false, 1>::SMEM; break;
         default: r = 0;
     }
     (void)mode;
@@ -224,7 +225,7 @@ size_t prefold_smem(int UP, bool dl, int mode) {
 // uses the lane-row kernel (dbp_prelr.cu).
 bool launch_prefold(const LaunchCtx& L, int UP, int mode, const float2* H, const float2* y, int S, int U, int J,
                     long npairs, float delta, float2* Gout, float2* vout) {
-    if (UP > 16 || (mode <= 1 && J != 1) || npairs <= 0 || npairs > (1L << 30)) return false;
+    if (UP > 32 || (mode <= 1 && J != 1) || npairs <= 0 || npairs > (1L << 30)) return false;
     PfArgs a{S, U, npairs, delta, Gout, vout, L.flag};
     switch (UP) {
 #define DBP_PF_CASE(UPc)                                                  \
@@ -238,6 +239,7 @@ bool launch_prefold(const LaunchCtx& L, int UP, int mode, const float2* H, const
         DBP_PF_CASE(4)
         DBP_PF_CASE(8)
         DBP_PF_CASE(16)
+        DBP_PF_CASE(32)
 #undef DBP_PF_CASE
         default: return false;
     }
