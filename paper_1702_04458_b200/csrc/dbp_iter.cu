@@ -82,17 +82,65 @@ __global__ void __launch_bounds__(512) k_admm_gj(UlArgs a) {
     }
 }
 
+// Per-warp staging of the packed triangles for the split kernels.  A warp
+// holds the 32/UP consecutive pair slots q0.. of one subcarrier row; it copies
+// their chunk-c0 triangles into its own shared buffer with coalesced 16-B
+// cp.async (tri(UP) * 8 B is a multiple of 16 for every UP), so lane-row reads
+// come from shared memory: read straight from HBM, lane i's row (a contiguous
+// piece plus a strided column) makes every warp load touch 32 sectors, and the
+// L1 wavefront rate, not HBM, set the time.  Double-buffered per warp: chunk
+// k+1's copies are in flight while chunk k computes; no CTA barrier.  Used at
+// UP = 32 (E: 705 vs 942 us per ADMM-UL round); at UP <= 16 half-warp rows
+// gather fewer sectors and the direct loads measured faster (C split: 22.6 vs
+// 25.3 us), so there the rows come straight from HBM.
+constexpr int split_staged(int UP) { return UP >= 32; }
+template <int UP>
+__device__ __forceinline__ void warp_tri_copy(float2* dst, const float2* __restrict__ Gp, int C, int N, int c0,
+                                              int n0, int q0, int CCH, int lane) {
+    constexpr int TV = tri(UP) / 2, PWQ = 32 / UP;
+    // the last warp may be partial when UP < 32 (UP = 32: every warp is one full pair)
+    const int nlanes = UP == 32 ? 32 : min(32, (int)blockDim.x - (int)(threadIdx.x & ~31u));
+    for (int e = lane; e < PWQ * TV; e += nlanes) {
+        const int pj = e / TV, k = e - pj * TV;
+        const int qq = q0 + pj, nl = qq / CCH, c = c0 + qq % CCH, n = n0 + nl;
+        if (c < C && n < N) cp_async16(dst + pj * tri(UP) + 2 * k, Gp + ((size_t)c * N + n) * tri(UP) + 2 * k);
+    }
+    cp_async_commit();
+}
+
+// Row i of this lane's pair for chunk c0 (buffers tb[2] of 32/UP triangles each).
+template <int UP>
+__device__ __forceinline__ void warp_tri_row(float2* tb, const float2* __restrict__ Gp, int C, int N, int c0, int n0,
+                                             int q0, int CCH, int lane, int qi, int i, float2 (&R)[UP]) {
+    constexpr int WB = 32 / UP * tri(UP);
+    const int k = c0 / CCH;
+    __syncwarp();                                        // the buffer about to be refilled was read a chunk ago
+    if (c0 + CCH < C) {
+        warp_tri_copy<UP>(tb + ((k + 1) & 1) * WB, Gp, C, N, c0 + CCH, n0, q0, CCH, lane);
+        cp_async_wait_1();
+    } else {
+        cp_async_wait_all();
+    }
+    __syncwarp();
+    load_herm_row_s<UP>(tb + (k & 1) * WB + qi * tri(UP), i, R);
+}
+
 // Split path: one iteration (or the init t = 1) for all local clusters of NT
 // subcarriers, clusters visited in chunks of CCH (any C_loc); writes the
-// local partial consensus sum (fixed cluster order) into wbuf.
+// local partial consensus sum into wbuf.  No barrier inside the chunk loop:
+// every (subcarrier, cluster-slot) pair accumulates its clusters' w_c in its
+// own shared-memory slot (chunk order), and one fixed-order sum over the slots
+// at the end forms the partial sum (deterministic).  Each warp therefore
+// streams its pairs' G^{-1} rows independently, and the load latency of one
+// chunk is hidden by the other warps instead of serialising the CTA.
 template <int UP>
 __global__ void __launch_bounds__(512) k_admm_it(UlArgs a, int CCH) {
     extern __shared__ __align__(16) float2 sm[];
     const int C = a.C_loc, NT = a.NT, J = a.J;
     float2* pbuf = sm;                                  // [NT*CCH][UP]
-    float2* W = pbuf + (size_t)NT * CCH * UP;           // [NT][CCH][UP]
-    float2* Sv = W + (size_t)NT * CCH * UP;             // [NT][J][UP]
-    float2* Acc = Sv + (size_t)NT * J * UP;             // [NT][J][UP]
+    float2* Wp = pbuf + (size_t)NT * CCH * UP;          // [NT][J][CCH][UP] per-slot partial sums
+    float2* Sv = Wp + (size_t)NT * J * CCH * UP;        // [NT][J][UP]
+    float2* Tb = Sv + (size_t)NT * J * UP;              // [warps][2][32/UP][tri(UP)] staged G^{-1}
     const int tid = threadIdx.x;
     const int q = tid / UP, i = tid % UP;
     const int nl = q / CCH, cl = q % CCH;
@@ -100,12 +148,16 @@ __global__ void __launch_bounds__(512) k_admm_it(UlArgs a, int CCH) {
     const int n = n0 + nl;
     const int nn = n < a.N ? n : a.N - 1;
     float2* buf = pbuf + (size_t)q * UP;
+    const int lane = tid & 31, q0 = (tid >> 5) * (32 / UP);
+    float2* tb = Tb + (size_t)(tid >> 5) * 2 * (32 / UP) * tri(UP);
+    if (split_staged(UP) && !a.init) warp_tri_copy<UP>(tb, a.Ginv, C, a.N, 0, n0, q0, CCH, lane);
     for (int e = tid; e < NT * J * UP; e += blockDim.x) {
         const int el = e / (J * UP);
         const bool ok = n0 + el < a.N && !a.init;
         Sv[e] = prox(ok ? a.wbuf[(size_t)n0 * J * UP + e] : make_float2(0.f, 0.f), a.px);
-        Acc[e] = make_float2(0.f, 0.f);
     }
+    float2* wp = Wp + ((size_t)nl * J * CCH + cl) * UP + i;   // this lane's slot, symbol stride CCH * UP
+    for (int jj = 0; jj < J; ++jj) wp[(size_t)jj * CCH * UP] = make_float2(0.f, 0.f);
     __syncthreads();
     for (int c0 = 0; c0 < C; c0 += CCH) {
         const int c = c0 + cl;
@@ -113,7 +165,8 @@ __global__ void __launch_bounds__(512) k_admm_it(UlArgs a, int CCH) {
         const size_t pair = (size_t)(c < C ? c : C - 1) * a.N + nn;
         float2 R[UP];
         if (!a.init) {
-            load_herm_row<UP>(a.Ginv + pair * tri(UP), i, R);
+            if (split_staged(UP)) warp_tri_row<UP>(tb, a.Ginv, C, a.N, c0, n0, q0, CCH, lane, q - q0, i, R);
+            else load_herm_row<UP>(a.Ginv + pair * tri(UP), i, R);
 #pragma unroll
             for (int j = 0; j < UP; ++j) R[j] = c_scale(R[j], a.rho);
         }
@@ -131,19 +184,16 @@ __global__ void __launch_bounds__(512) k_admm_it(UlArgs a, int CCH) {
                 z = c_add(yreg, row_apply<UP>(R, buf, i, c_sub(s, lam)));    // line 15
                 w = c_add(z, lam);                                           // line 17
             }
-            if (valid) { a.lam[o] = lam; a.z[o] = z; }
-            W[((size_t)nl * CCH + cl) * UP + i] = valid ? w : make_float2(0.f, 0.f);
-            __syncthreads();
-            if (tid < NT * UP) {
-                const int el = tid / UP, uu = tid % UP;
-                float2* ac = Acc + ((size_t)el * J + jj) * UP + uu;
-                *ac = c_add(*ac, cluster_sum(W, CCH, UP, el, uu));
+            if (valid) {
+                a.lam[o] = lam;
+                a.z[o] = z;
+                wp[(size_t)jj * CCH * UP] = c_add(wp[(size_t)jj * CCH * UP], w);
             }
-            __syncthreads();
         }
     }
-    for (int e = tid; e < NT * J * UP; e += blockDim.x)
-        if (n0 + e / (J * UP) < a.N) a.wbuf[(size_t)n0 * J * UP + e] = Acc[e];
+    __syncthreads();
+    for (int e = tid; e < NT * J * UP; e += blockDim.x)      // e = (el J + jj) UP + u
+        if (n0 + e / (J * UP) < a.N) a.wbuf[(size_t)n0 * J * UP + e] = cluster_sum(Wp, CCH, UP, e / UP, e % UP);
 }
 
 // ============================================================ ADMM-DL
@@ -252,9 +302,9 @@ __global__ void __launch_bounds__(512) k_bf_it(DlArgs a, int CCH) {
     extern __shared__ __align__(16) float2 sm[];
     const int C = a.C_loc, NT = a.NT, J = a.J;
     float2* pbuf = sm;                                  // [NT*CCH][UP]
-    float2* W = pbuf + (size_t)NT * CCH * UP;           // [NT][CCH][UP]
-    float2* Wv = W + (size_t)NT * CCH * UP;             // [NT][J][UP]  allreduced w^(t-1)
-    float2* Acc = Wv + (size_t)NT * J * UP;             // [NT][J][UP]
+    float2* Wp = pbuf + (size_t)NT * CCH * UP;          // [NT][J][CCH][UP] per-slot partial sums
+    float2* Wv = Wp + (size_t)NT * J * CCH * UP;        // [NT][J][UP]  allreduced w^(t-1)
+    float2* Tb = Wv + (size_t)NT * J * UP;              // [warps][2][32/UP][tri(UP)] staged B^{-1}
     const int tid = threadIdx.x;
     const int q = tid / UP, i = tid % UP;
     const int nl = q / CCH, cl = q % CCH;
@@ -262,6 +312,9 @@ __global__ void __launch_bounds__(512) k_bf_it(DlArgs a, int CCH) {
     const int n = n0 + nl;
     const int nn = n < a.N ? n : a.N - 1;
     float2* buf = pbuf + (size_t)q * UP;
+    const int lane = tid & 31, q0 = (tid >> 5) * (32 / UP);
+    float2* tb = Tb + (size_t)(tid >> 5) * 2 * (32 / UP) * tri(UP);
+    if (split_staged(UP)) warp_tri_copy<UP>(tb, a.Binv, C, a.N, 0, n0, q0, CCH, lane);
     const bool fin = a.step > a.T;
     const bool first = a.step == 2;
     if (fin && i == 0) {
@@ -276,15 +329,17 @@ __global__ void __launch_bounds__(512) k_bf_it(DlArgs a, int CCH) {
     for (int e = tid; e < NT * J * UP; e += blockDim.x) {
         const int el = e / (J * UP);
         Wv[e] = (n0 + el < a.N && !first) ? a.wbuf[(size_t)n0 * J * UP + e] : make_float2(0.f, 0.f);
-        Acc[e] = make_float2(0.f, 0.f);
     }
+    float2* wp = Wp + ((size_t)nl * J * CCH + cl) * UP + i;   // this lane's slot, symbol stride CCH * UP
+    for (int jj = 0; jj < J; ++jj) wp[(size_t)jj * CCH * UP] = make_float2(0.f, 0.f);
     __syncthreads();
     for (int c0 = 0; c0 < C; c0 += CCH) {
         const int c = c0 + cl;
         const bool valid = n < a.N && c < C;
         const size_t pair = (size_t)(c < C ? c : C - 1) * a.N + nn;
         float2 R[UP];
-        load_herm_row<UP>(a.Binv + pair * tri(UP), i, R);
+        if (split_staged(UP)) warp_tri_row<UP>(tb, a.Binv, C, a.N, c0, n0, q0, CCH, lane, q - q0, i, R);
+        else load_herm_row<UP>(a.Binv + pair * tri(UP), i, R);
         for (int jj = 0; jj < J; ++jj) {
             const size_t o = (pair * J + jj) * UP + i;
             const float2 sv = i < a.U ? a.s[((size_t)nn * J + jj) * a.U + i] : make_float2(0.f, 0.f);
@@ -307,20 +362,17 @@ __global__ void __launch_bounds__(512) k_bf_it(DlArgs a, int CCH) {
                 continue;
             }
             const float2 m = c_sub(qv, c_scale(bq, a.rho_inv));          // line 11
-            if (valid) { a.m[o] = m; a.lam[o] = lam; }
-            W[((size_t)nl * CCH + cl) * UP + i] = valid ? c_sub(m, lam) : make_float2(0.f, 0.f);   // line 12
-            __syncthreads();
-            if (tid < NT * UP) {
-                const int el = tid / UP, uu = tid % UP;
-                float2* ac = Acc + ((size_t)el * J + jj) * UP + uu;
-                *ac = c_add(*ac, cluster_sum(W, CCH, UP, el, uu));
+            if (valid) {
+                a.m[o] = m;
+                a.lam[o] = lam;
+                wp[(size_t)jj * CCH * UP] = c_add(wp[(size_t)jj * CCH * UP], c_sub(m, lam));   // line 12
             }
-            __syncthreads();
         }
     }
     if (fin) return;
-    for (int e = tid; e < NT * J * UP; e += blockDim.x)
-        if (n0 + e / (J * UP) < a.N) a.wbuf[(size_t)n0 * J * UP + e] = Acc[e];
+    __syncthreads();
+    for (int e = tid; e < NT * J * UP; e += blockDim.x)      // e = (el J + jj) UP + u
+        if (n0 + e / (J * UP) < a.N) a.wbuf[(size_t)n0 * J * UP + e] = cluster_sum(Wp, CCH, UP, e / UP, e % UP);
 }
 
 // ============================================================ centralized baselines
@@ -405,7 +457,12 @@ cudaError_t launch_admm_gj(const LaunchCtx& L, int UP, UlArgs a) {
     return cudaGetLastError();
 }
 
-size_t split_smem(int UP, int NT, int CCH, int J) { return ((size_t)2 * NT * CCH * UP + (size_t)2 * NT * J * UP) * 8; }
+// pbuf [NT*CCH][UP], per-slot partial sums [NT][J][CCH][UP], [NT][J][UP] consensus vector,
+size_t split_smem(int UP, int NT, int CCH, int J) {
+    // + per-warp double-buffered triangles: 2 x tri(UP) per pair slot of every (possibly partial) warp
+    const size_t slots = split_staged(UP) ? (size_t)(NT * CCH * UP + 31) / 32 * (32 / UP) : 0;
+    return ((size_t)NT * CCH * UP * (1 + J) + (size_t)NT * J * UP + 2 * slots * tri(UP)) * 8;
+}
 
 // Split CTA shape: CCH clusters per chunk, NT subcarriers, ~512 threads.
 void split_cfg(int UP, int C_loc, int N, int J, int* NT, int* CCH) {

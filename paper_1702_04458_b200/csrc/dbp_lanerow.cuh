@@ -18,6 +18,17 @@ __device__ __forceinline__ void load_herm_row(const float2* __restrict__ Gp, int
     }
 }
 
+// Same, from a packed triangle staged in shared memory.
+template <int UP>
+__device__ __forceinline__ void load_herm_row_s(const float2* Gp, int i, float2 (&r)[UP]) {
+    const int base = (i * (i + 1)) / 2;
+#pragma unroll
+    for (int j = 0; j < UP; ++j) {
+        if (j <= i) r[j] = Gp[base + j];
+        else { const float2 v = Gp[(j * (j + 1)) / 2 + i]; r[j] = make_float2(v.x, -v.y); }
+    }
+}
+
 template <int UP>
 __device__ __forceinline__ void store_herm_row(float2* __restrict__ Gp, int i, const float2 (&r)[UP]) {
     const int base = (i * (i + 1)) / 2;
