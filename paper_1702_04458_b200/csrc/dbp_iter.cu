@@ -205,13 +205,14 @@ __device__ __forceinline__ void bf_output(const float2* __restrict__ Hd, float2*
                                           float2* __restrict__ xo, bool valid) {
     buf[i] = ri;
     __syncwarp();
-    float2 r[UP];
-    read_vec<UP>(buf, r);
+    // UP = 32: r_u by broadcast LDS (a register copy of r next to the caller's row spills)
+    float2 r[UP <= 16 ? UP : 1];
+    if constexpr (UP <= 16) read_vec<UP>(buf, r);
     for (int s = i; s < S; s += UP) {
         float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
         for (int u = 0; u < UP; ++u)
-            if (u < U) c_fmac(acc, __ldg(Hd + (size_t)u * S + s), r[u]);
+            if (u < U) c_fmac(acc, __ldg(Hd + (size_t)u * S + s), UP <= 16 ? r[UP <= 16 ? u : 0] : buf[u]);
         if (valid) xo[s] = acc;
     }
     __syncwarp();
@@ -317,15 +318,16 @@ __global__ void __launch_bounds__(512) k_bf_it(DlArgs a, int CCH) {
     if (split_staged(UP)) warp_tri_copy<UP>(tb, a.Binv, C, a.N, 0, n0, q0, CCH, lane);
     const bool fin = a.step > a.T;
     const bool first = a.step == 2;
-    if (fin && i == 0) {
-        // the output pass reads H_c of every pair of this CTA: pull them into L2 up front
-        const size_t bytes = (size_t)a.U * a.S * 8;
-        if ((bytes & 15) == 0 && bytes < (1u << 20))
-            for (int c = cl; c < C; c += CCH)
-                if (n < a.N)
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
-                                 ::"l"(a.Hd + ((size_t)c * a.N + n) * a.U * a.S), "r"((uint32_t)bytes) : "memory");
-    }
+    // the output pass reads H_c of every pair: pull the pair's tile into L2 one
+    // chunk ahead (all chunks up front overflows L2 at C_loc = 128: 8x slower)
+    const size_t hbytes = (size_t)a.U * a.S * 8;
+    const bool pf = fin && i == 0 && n < a.N && (hbytes & 15) == 0 && hbytes < (1u << 20);
+    auto prefetch_h = [&](int c) {
+        if (pf && c < C)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                         ::"l"(a.Hd + ((size_t)c * a.N + n) * a.U * a.S), "r"((uint32_t)hbytes) : "memory");
+    };
+    prefetch_h(cl);
     for (int e = tid; e < NT * J * UP; e += blockDim.x) {
         const int el = e / (J * UP);
         Wv[e] = (n0 + el < a.N && !first) ? a.wbuf[(size_t)n0 * J * UP + e] : make_float2(0.f, 0.f);
@@ -338,6 +340,7 @@ __global__ void __launch_bounds__(512) k_bf_it(DlArgs a, int CCH) {
         const bool valid = n < a.N && c < C;
         const size_t pair = (size_t)(c < C ? c : C - 1) * a.N + nn;
         float2 R[UP];
+        prefetch_h(c0 + CCH + cl);
         if (split_staged(UP)) warp_tri_row<UP>(tb, a.Binv, C, a.N, c0, n0, q0, CCH, lane, q - q0, i, R);
         else load_herm_row<UP>(a.Binv + pair * tri(UP), i, R);
         for (int jj = 0; jj < J; ++jj) {

@@ -91,6 +91,10 @@ SMALL_UL = [
     synth.Config("u20", "admm_ul", C=2, S=24, U=20, N=7, mod="qam16", snr_db=25),
     synth.Config("c20", "admm_ul", C=20, S=12, U=14, N=13, mod="qam16", snr_db=22),  # partial cluster blocks
     synth.Config("c5", "admm_ul", C=5, S=8, U=6, N=10, mod="qpsk", snr_db=12),       # 4 subcarriers per CTA
+    # U = 32 with C > 16: split kernels visit 3 cluster chunks (last partial) through the
+    # per-warp staged inverse; N_sym = 2 runs the chunk loop with J > 1
+    synth.Config("u32c40", "admm_ul", C=40, S=32, U=32, N=3, mod="qam64", snr_db=30),
+    synth.Config("u32j2", "admm_ul", C=20, S=32, U=29, N=2, N_sym=2, mod="qam16", snr_db=25),
 ]
 
 
@@ -201,6 +205,8 @@ SMALL_DL = [
     synth.Config("nsym", "admm_dl", C=2, S=16, U=8, N=10, N_sym=3, mod="qam64"),
     synth.Config("c20", "admm_dl", C=20, S=12, U=14, N=13, mod="qam16"),
     synth.Config("c5", "admm_dl", C=5, S=8, U=6, N=10, mod="qpsk"),
+    synth.Config("u32c40", "admm_dl", C=40, S=32, U=32, N=3, mod="qam64"),
+    synth.Config("u32j2", "admm_dl", C=20, S=32, U=29, N=2, N_sym=2, mod="qam16"),
 ]
 
 
