@@ -38,6 +38,11 @@ struct Fold {
     static constexpr int NST = DBP_PF_NST;           // per-warp ring depth
     static constexpr int NSLOT = 10 * L;             // L * R(R+1)/2
     static constexpr int TRI = UP * (UP + 1) / 2;
+    // pitch (float2) of a pair's pivot / vector line in shared memory: = L mod 16, so the
+    // 16/L pairs of a 16-lane LDS.64 / STS.64 phase put their L-row blocks (rows mL..mL+L-1)
+    // on disjoint banks; even (16-B aligned LDS.128 of c_t pairs) and >= UP + 2
+    // (E_k and a dump entry follow the UP column entries)
+    static constexpr int PLP = L >= 8 ? UP + 8 : (L >= 4 ? UP + 4 : UP + 2);
     __host__ __device__ static constexpr int off(int m) { return L * m * (m + 1) / 2; }
     __device__ static __forceinline__ int row(int m, int l) { return (m & 1) ? (m + 1) * L - 1 - l : m * L + l; }
 };
@@ -161,7 +166,7 @@ __device__ __forceinline__ void fold_jacobi(f2x (&A)[Fold<UP>::NSLOT], f2x (&E)[
 
 // Hermitian sweep over pivots k = 0..UP-1 (Goodnight form): afterwards the
 // valid slots hold -M^{-1} of the (scaled) matrix and, with BORDER, E holds
-// M^{-1} E.  pl: the pair's UP+2 line (pivot column, E_k).  Returns false if
+// M^{-1} E.  pl: the pair's PLP line (pivot column, E_k, dump).  Returns false if
 // a pivot was not positive and finite (not HPD).
 template <int UP, bool BORDER>
 __device__ __forceinline__ bool fold_sweep(f2x (&A)[Fold<UP>::NSLOT], f2x (&E)[4], float2* pl, const int (&row)[4],

@@ -50,7 +50,7 @@ struct FZ {
 #define DBP_FZ_NST 2
 #endif
     static constexpr int NST = DBP_FZ_NST;
-    static constexpr int PWL = F::PW * (UP + 2);          // pivot / vector lines (float2)
+    static constexpr int PWL = F::PW * F::PLP;            // pivot / vector lines (float2)
     static constexpr int DLN = F::PW * UP;                // Jacobi scales (float)
     static constexpr int YB = F::PW * fold_ybuf_pair<UP>(); // mat-vec partials (float2), padded
     static constexpr int WREG = (NST * G::STG + PWL * 8 + DLN * 4 + YB * 8 + 127) / 128 * 128;
@@ -90,7 +90,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw) + warp * NST;
     unsigned char* wbase = smem_raw + 128 + (size_t)warp * Z::WREG;
     const int q = lane / L, l = lane % L;
-    float2* pl = reinterpret_cast<float2*>(wbase + NST * G::STG) + q * (UP + 2);           // pivots / vectors
+    float2* pl = reinterpret_cast<float2*>(wbase + NST * G::STG) + q * F::PLP;             // pivots / vectors
     float* dline = reinterpret_cast<float*>(wbase + NST * G::STG + Z::PWL * 8) + q * UP;
     float2* ybuf = reinterpret_cast<float2*>(wbase + NST * G::STG + Z::PWL * 8 + Z::DLN * 4) + q * fold_ybuf_pair<UP>();
     float2* Wp = reinterpret_cast<float2*>(smem_raw + 128 + (size_t)Z::WARPS * Z::WREG);   // [4 warps][UP]
@@ -254,7 +254,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                     // and exact at delta = 0 (ZF); (jc == u) as a bit test, without local memory
                     grow[jc].x += ((1u << jc) >> u) & 1u ? delta + (u >= a.U ? 1.f : 0.f) : 0.f;
                 }
-                float2* P = pl - q * (UP + 2) + (lane / UP) * (UP + 2);       // a per-group line
+                float2* P = pl - q * F::PLP + (lane / UP) * F::PLP;          // a per-group line
                 const bool ok = gj_invert<UP>(grow, P, u);
                 if (!ok && live) atomicOr(a.flag, 1);        // padding subcarriers (n >= N) have G = 0
                 return row_apply<UP>(grow, P, u, rhs_u);
@@ -291,7 +291,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
 #pragma unroll
                         for (int jc = 0; jc < UP; ++jc)
                             grow[jc] = jc <= u ? Gj[(u * (u + 1)) / 2 + jc] : c_conj(Gj[(jc * (jc + 1)) / 2 + u]);
-                        float2* P = pl - q * (UP + 2) + (lane / UP) * (UP + 2);       // a per-group line
+                        float2* P = pl - q * F::PLP + (lane / UP) * F::PLP;          // a per-group line
                         // device-side consensus (NEXT-1): sum of v over ranks for round t (LL words)
                         auto xsum = [&](int t, float2 v) {
                             if (!a.xc.on || nn >= a.N) return v;

@@ -58,7 +58,7 @@ template <int UP, bool DL, int MODE>
 struct PFL {
     using P = PF<UP>;
     using G = FoldStage<UP, DL, !DL && (MODE == 0 || MODE == 1)>;
-    static constexpr int PLN = P::PW * (UP + 2);                // pivot lines (float2)
+    static constexpr int PLN = P::PW * P::PLP;                  // pivot lines (float2)
     static constexpr int WREG = (P::NST * G::STG + PLN * 8 + P::PW * UP * 4 + 127) / 128 * 128;
     static constexpr size_t SMEM = 128 + (size_t)P::WARPS * WREG;
 };
@@ -86,7 +86,7 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw) + warp * NST;
     unsigned char* wbase = smem_raw + 128 + (size_t)warp * Q::WREG;
     const int q = lane / L, l = lane % L;
-    float2* pl = reinterpret_cast<float2*>(wbase + NST * G::STG) + q * (UP + 2);    // pivot column + E_k
+    float2* pl = reinterpret_cast<float2*>(wbase + NST * G::STG) + q * P::PLP;      // pivot column + E_k
     float* dline = reinterpret_cast<float*>(wbase + NST * G::STG + Q::PLN * 8) + q * UP;   // Jacobi scales
 
     int row[R];
