@@ -15,7 +15,13 @@ round -- the only communication (P744-746).
 
 Timing: W untimed warm-up steps; then exactly K steps, each bracketed by CUDA
 events on the launch stream, with an untimed 256 MiB L2-flush write between
-steps; barrier + synchronize on both sides; max over ranks.  The end-to-end
+steps; barrier + synchronize on both sides; max over ranks.  At world = 1
+the step runs the uplink pair (ADMM-UL then CG-UL, one stream) concurrently
+with ADMM-DL (second stream, forked from and joined to the launch stream
+inside the event bracket); a separate sequential region (all three back to
+back on one stream) gives the per-solver times, per-iteration latencies and
+the kernel-timer shares the roofline uses.  At world > 1 the step is the
+sequential schedule (one communicator, one collective order).  The end-to-end
 figure (e2e) calls the same C ABI with pinned HOST buffers, so every step
 includes the host->device copy of its inputs and the device->host copy of
 its outputs.  `--impl reference` times the fp64 oracle (oracle/) on the
@@ -228,6 +234,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-table2", action="store_true")
+    ap.add_argument("--sequential", action="store_true",
+                    help="world = 1: time the step with the three solvers back to back on one stream")
     ap.add_argument("--device-consensus", action="store_true",
                     help="world > 1: consensus inside the fused kernels over NVLink (DBP_OPT_DEVICE_CONSENSUS)")
     ap.add_argument("--ref-subcarriers", type=int, default=60)
@@ -281,14 +289,49 @@ def main():
         flush.fill_(k & 0xFF)
         torch.sum(flush.view(torch.int64), dim=0, out=flush_sink)
 
-    def solver(name, T):
+    def solver(name, T, st=None):
+        sp = None if st is None else st.cuda_stream
         if name == "admm_ul":
             dbp.detect_admm(ctx, Hg, yg, rho=UL.rho, N0=UL.N0, mod=UL.mod, T=T, s_hat=s_hat, hard=hard,
-                            ws=ws["admm_ul"])
+                            ws=ws["admm_ul"], stream=sp)
         elif name == "admm_dl":
-            dbp.beamform_admm(ctx, Hdg, sg, rho=DL.rho, T=T, x=xbf, ws=ws["admm_dl"])
+            dbp.beamform_admm(ctx, Hdg, sg, rho=DL.rho, T=T, x=xbf, ws=ws["admm_dl"], stream=sp)
         else:
-            dbp.detect_cg(ctx, Hg, yg, rho=UL.N0, mod=UL.mod, T=T, x_hat=x_hat, hard=hard2, ws=ws["cg_ul"])
+            dbp.detect_cg(ctx, Hg, yg, rho=UL.N0, mod=UL.mod, T=T, x_hat=x_hat, hard=hard2, ws=ws["cg_ul"],
+                          stream=sp)
+
+    # Step schedule.  world == 1: the uplink solvers (ADMM-UL, then CG-UL: same H, one stream) and
+    # the downlink solver (its own H^d) on two streams, so each kernel's CTAs fill the other's wave
+    # tail.  world > 1: sequential on one stream (every solver issues one NCCL allreduce per round
+    # on the same communicator; two streams could order them differently across ranks).
+    concurrent = world == 1 and not args.sequential
+    side = (torch.cuda.Stream(dev), torch.cuda.Stream(dev)) if concurrent else None
+    join = (torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event())
+
+    def step_concurrent(T, e_start):
+        sa, sb = side
+        sa.wait_event(e_start)
+        sb.wait_event(e_start)
+        solver("admm_ul", T, sa)
+        solver("cg_ul", T, sa)
+        solver("admm_dl", T, sb)
+        join[0].record(sa)
+        join[1].record(sb)
+        stream.wait_event(join[0])
+        stream.wait_event(join[1])
+
+    def timed_concurrent(K, T):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        barrier()
+        torch.cuda.synchronize()
+        for k in range(K):
+            flush_l2(k)
+            ev[k][0].record(stream)
+            step_concurrent(T, ev[k][0])
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        return sum(e0.elapsed_time(e1) for e0, e1 in ev)   # ms over K steps
 
     order = ["admm_ul", "admm_dl", "cg_ul"]   # BF between the two uplink passes: no L2 reuse of H
 
@@ -317,6 +360,9 @@ def main():
     for _ in range(args.warmup):
         for nm in order:
             solver(nm, UL.T)
+        if concurrent:
+            join[2].record(stream)
+            step_concurrent(UL.T, join[2])
     ctx.sync()
 
     clk = ClockSampler(local)
@@ -325,10 +371,15 @@ def main():
     ctx.set_option(dbp.OPT_KERNEL_TIMING, 1)
     ctx.kernel_times(reset=True)
     st0 = ctx.stats()
-    per = timed_region(args.steps, UL.T, order)
+    per = timed_region(args.steps, UL.T, order)        # sequential: per-solver times + kernel timer
     st1 = ctx.stats()
     ktimes = ctx.kernel_times(reset=True)
     ctx.set_option(dbp.OPT_KERNEL_TIMING, 0)
+    conc_ms = None
+    if concurrent:                                     # the step as scheduled (headline)
+        st0 = ctx.stats()
+        conc_ms = timed_concurrent(args.steps, UL.T)
+        st1 = ctx.stats()
     clocks = clk.stop()
     ctx.sync()
 
@@ -410,7 +461,8 @@ def main():
                           "paper_cite": cite}
         del H7g, y7g, Hd7g, s7g
     total_ms = float(per.sum())
-    ms_step = total_ms / args.steps
+    ms_seq = total_ms / args.steps
+    ms_step = float(mx([conc_ms])[0]) / args.steps if concurrent else ms_seq
     value = BITS_PER_STEP / (ms_step * 1e-3) / 1e9
     solvers = {}
     for i, nm in enumerate(order):
@@ -482,7 +534,10 @@ def main():
     if rank == 0:
         launches = st1["kernel_launches"] - st0["kernel_launches"]
         line = {"metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+                "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_step_sequential": ms_seq,
+                "schedule": ("concurrent: ADMM-UL then CG-UL on one stream, ADMM-DL on a second"
+                             if concurrent else "sequential on one stream"),
+                "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Philox-4x32: i.i.d. Rayleigh "
                 "CN(0,1) channels, uniform Gray QAM, AWGN)", "config": workload_config(world),
                 "solvers": solvers, "centralized_baselines": baselines, "paper_table2_context": table2,
