@@ -508,3 +508,30 @@ def test_device_consensus_self_peer(env):
             ctx.set_option(dbp.OPT_DEVICE_CONSENSUS, 0)
         s_or, _ = oracle.detect_admm(H, y, N0=cfg.N0, mod=cfg.mod, T=cfg.T)
         assert rel(s1.cpu().numpy(), s_or) < TOL
+
+
+def test_two_stream_schedule_matches_sequential(env):
+    """bench.py's world-1 schedule: ADMM-UL + CG-UL on one stream, ADMM-DL on another, one
+    context; results bitwise equal to the same calls back to back on one stream."""
+    dbp, ctx, oracle, torch = env
+    ul, dl = synth.CONFIGS["C"].scaled(N=300), synth.CONFIGS["D"].scaled(N=300)
+    H, y, _ = synth.uplink_frame(ul)
+    Hd, s = synth.downlink_frame(dl)
+    Hg, yg, Hdg, sg = (torch.from_numpy(a).cuda() for a in (H, y, Hd, s))
+    set_path(env, "fused")
+
+    def run(sa, sb):
+        out = [dbp.detect_admm(ctx, Hg, yg, rho=ul.rho, N0=ul.N0, mod=ul.mod, T=ul.T, stream=sa.cuda_stream),
+               dbp.detect_cg(ctx, Hg, yg, rho=ul.N0, mod=ul.mod, T=ul.T, stream=sa.cuda_stream),
+               dbp.beamform_admm(ctx, Hdg, sg, rho=dl.rho, T=dl.T, stream=sb.cuda_stream)]
+        torch.cuda.synchronize()
+        return out
+
+    main = torch.cuda.current_stream()
+    seq = run(main, main)
+    conc = run(torch.cuda.Stream(), torch.cuda.Stream())
+    for a, b in zip(seq, conc):
+        for u, v in zip(a if isinstance(a, tuple) else (a,), b if isinstance(b, tuple) else (b,)):
+            assert torch.equal(u, v)
+    x_ref = oracle.beamform_admm(Hd, s, rho=dl.rho, T=dl.T)
+    assert rel(conc[2].cpu().numpy(), x_ref) < TOL
