@@ -467,10 +467,17 @@ size_t split_smem(int UP, int NT, int CCH, int J) {
     return ((size_t)NT * CCH * UP * (1 + J) + (size_t)NT * J * UP + 2 * slots * tri(UP)) * 8;
 }
 
-// Split CTA shape: CCH clusters per chunk, NT subcarriers, ~512 threads.
+// Split CTA shape: CCH clusters per chunk, NT subcarriers, ~TH threads: small CTAs, so
+// several per SM hide each other's load latency (split_scaling_proxy.py, world-8 shares:
+// E ADMM-UL 1725 / 1500 / 1421 us and C ADMM-DL at world 2 195 / 185 / 183 us at
+// TH = 512 / 256 / 128).
+#ifndef DBP_SPLIT_THREADS
+#define DBP_SPLIT_THREADS 0
+#endif
 void split_cfg(int UP, int C_loc, int N, int J, int* NT, int* CCH) {
-    int cch = std::max(1, std::min(C_loc, 512 / UP));
-    int nt = std::max(1, std::min(N, 512 / (cch * UP)));
+    const int TH = DBP_SPLIT_THREADS ? DBP_SPLIT_THREADS : (UP >= 32 ? 128 : 256);
+    int cch = std::max(1, std::min(C_loc, TH / UP));
+    int nt = std::max(1, std::min(N, TH / (cch * UP)));
     *NT = nt;
     *CCH = cch;
 }

@@ -14,10 +14,11 @@ from paper_1702_04458_b200 import dbp, synth  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C")
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--gs", default="1,2,4,8", help="world sizes to model")
 a = ap.parse_args()
 ctx = dbp.Context(0)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-for G in (1, 2, 4, 8):
+for G in (int(g) for g in a.gs.split(",")):
     cfg = synth.CONFIGS[a.config]
     loc = cfg.scaled(C=cfg.C // G)
     H, y, _ = synth.uplink_frame(loc)
