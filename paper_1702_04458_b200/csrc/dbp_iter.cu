@@ -30,7 +30,7 @@ namespace dbp {
 // Fused (world == 1): G^{-1} in registers, all T iterations of Alg. 1 on chip.
 // CTA = NT subcarriers x C clusters x UP lanes.
 template <int UP>
-__global__ void __launch_bounds__(512) k_admm_gj(UlArgs a) {
+__global__ void __launch_bounds__(512, UP <= 16 ? 2 : 1) k_admm_gj(UlArgs a) {   // 2 CTAs/SM at <= 64 registers (no spills)
     extern __shared__ __align__(16) float2 sm[];
     const int C = a.C_loc, NT = a.NT;
     float2* pbuf = sm;                                  // [NT*C][UP] per-pair line
@@ -221,8 +221,11 @@ __device__ __forceinline__ void bf_output(const float2* __restrict__ Hd, float2*
 // Fused (world == 1): B^{-1} in registers; init, T-1 consensus iterations of
 // Alg. 3 in the exact m-form (m_c = q - rho^{-1} B^{-1} q, q = z + lambda;
 // DESIGN.md section 5) and the output pass x_c = H_c^H B^{-1} q.
+#ifndef DBP_BFGJ_2CTA_MAX_UP
+#define DBP_BFGJ_2CTA_MAX_UP 8
+#endif
 template <int UP>
-__global__ void __launch_bounds__(512) k_bf_gj(DlArgs a) {
+__global__ void __launch_bounds__(512, UP <= DBP_BFGJ_2CTA_MAX_UP ? 2 : 1) k_bf_gj(DlArgs a) {
     extern __shared__ __align__(16) float2 sm[];
     const int C = a.C_loc, NT = a.NT;
     float2* pbuf = sm;
