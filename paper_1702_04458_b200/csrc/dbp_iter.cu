@@ -22,6 +22,12 @@
 #include "dbp_internal.h"
 #include "dbp_lanerow.cuh"
 
+// tuning knob (build.py -D...): bf_output keeps r in registers up to this UP, else it
+// reads r_u by broadcast LDS per use (UP = 16: the split output pass 112 -> 99 us, and
+// k_bf_gj fits 64 registers without spills)
+#ifndef DBP_BFOUT_REG_MAX_UP
+#define DBP_BFOUT_REG_MAX_UP 8
+#endif
 namespace dbp {
 
 // ============================================================ ADMM-UL
@@ -206,13 +212,14 @@ __device__ __forceinline__ void bf_output(const float2* __restrict__ Hd, float2*
     buf[i] = ri;
     __syncwarp();
     // UP = 32: r_u by broadcast LDS (a register copy of r next to the caller's row spills)
-    float2 r[UP <= 16 ? UP : 1];
-    if constexpr (UP <= 16) read_vec<UP>(buf, r);
+    constexpr bool RR = UP <= DBP_BFOUT_REG_MAX_UP;
+    float2 r[RR ? UP : 1];
+    if constexpr (RR) read_vec<UP>(buf, r);
     for (int s = i; s < S; s += UP) {
         float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
         for (int u = 0; u < UP; ++u)
-            if (u < U) c_fmac(acc, __ldg(Hd + (size_t)u * S + s), UP <= 16 ? r[UP <= 16 ? u : 0] : buf[u]);
+            if (u < U) c_fmac(acc, __ldg(Hd + (size_t)u * S + s), RR ? r[RR ? u : 0] : buf[u]);
         if (valid) xo[s] = acc;
     }
     __syncwarp();
@@ -221,11 +228,10 @@ __device__ __forceinline__ void bf_output(const float2* __restrict__ Hd, float2*
 // Fused (world == 1): B^{-1} in registers; init, T-1 consensus iterations of
 // Alg. 3 in the exact m-form (m_c = q - rho^{-1} B^{-1} q, q = z + lambda;
 // DESIGN.md section 5) and the output pass x_c = H_c^H B^{-1} q.
-#ifndef DBP_BFGJ_2CTA_MAX_UP
-#define DBP_BFGJ_2CTA_MAX_UP 8
-#endif
-template <int UP>
-__global__ void __launch_bounds__(512, UP <= DBP_BFGJ_2CTA_MAX_UP ? 2 : 1) k_bf_gj(DlArgs a) {
+// MINB = 2 (<= 64 registers, 2 CTAs/SM) pays when N_sym > 1 (N_sym = 7: 277 -> 243 us) but not at
+// N_sym = 1 (89 vs 117 us): launch_bf_gj picks per call.
+template <int UP, int MINB>
+__global__ void __launch_bounds__(512, MINB) k_bf_gj(DlArgs a) {
     extern __shared__ __align__(16) float2 sm[];
     const int C = a.C_loc, NT = a.NT;
     float2* pbuf = sm;
@@ -495,8 +501,20 @@ cudaError_t launch_admm_it(const LaunchCtx& L, int UP, UlArgs a, int CCH) {
 
 cudaError_t launch_bf_gj(const LaunchCtx& L, int UP, DlArgs a) {
     const size_t smem = iter_smem(UP, a.NT, a.C_loc);
-    DBP_DISPATCH_UP(UP, big_smem(k_bf_gj<UPc>, smem);
-                    k_bf_gj<UPc><<<cdiv_i(a.N, a.NT), a.NT * a.C_loc * UPc, smem, L.stream>>>(a));
+    const int grid = cdiv_i(a.N, a.NT), nthr = a.NT * a.C_loc * UP;
+    DBP_DISPATCH_UP(UP,
+        if constexpr (UPc <= 16) {
+            if (a.J > 1) {
+                big_smem(k_bf_gj<UPc, 2>, smem);
+                k_bf_gj<UPc, 2><<<grid, nthr, smem, L.stream>>>(a);
+            } else {
+                big_smem(k_bf_gj<UPc, 1>, smem);
+                k_bf_gj<UPc, 1><<<grid, nthr, smem, L.stream>>>(a);
+            }
+        } else {
+            big_smem(k_bf_gj<UPc, 1>, smem);
+            k_bf_gj<UPc, 1><<<grid, nthr, smem, L.stream>>>(a);
+        });
     L.count(1);
     return cudaGetLastError();
 }
