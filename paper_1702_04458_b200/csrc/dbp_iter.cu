@@ -140,7 +140,7 @@ __device__ __forceinline__ void warp_tri_row(float2* tb, const float2* __restric
 // streams its pairs' G^{-1} rows independently, and the load latency of one
 // chunk is hidden by the other warps instead of serialising the CTA.
 template <int UP>
-__global__ void __launch_bounds__(512) k_admm_it(UlArgs a, int CCH) {
+__global__ void __launch_bounds__(256) k_admm_it(UlArgs a, int CCH) {   // split_cfg: <= 256 threads
     extern __shared__ __align__(16) float2 sm[];
     const int C = a.C_loc, NT = a.NT, J = a.J;
     float2* pbuf = sm;                                  // [NT*CCH][UP]
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(512, MINB) k_bf_gj(DlArgs a) {
 // then m, w_c and the local partial sum.  step == T+1: complete, write x_c.
 // Clusters in chunks of CCH.
 template <int UP>
-__global__ void __launch_bounds__(512) k_bf_it(DlArgs a, int CCH) {
+__global__ void __launch_bounds__(256, UP >= 32 ? 2 : 3) k_bf_it(DlArgs a, int CCH) {   // split_cfg: <= 256 threads
     extern __shared__ __align__(16) float2 sm[];
     const int C = a.C_loc, NT = a.NT, J = a.J;
     float2* pbuf = sm;                                  // [NT*CCH][UP]
@@ -484,7 +484,7 @@ size_t split_smem(int UP, int NT, int CCH, int J) {
 #define DBP_SPLIT_THREADS 0
 #endif
 void split_cfg(int UP, int C_loc, int N, int J, int* NT, int* CCH) {
-    const int TH = DBP_SPLIT_THREADS ? DBP_SPLIT_THREADS : (UP >= 32 ? 128 : 256);
+    const int TH = DBP_SPLIT_THREADS ? std::min(DBP_SPLIT_THREADS, 256) : (UP >= 32 ? 128 : 256);
     int cch = std::max(1, std::min(C_loc, TH / UP));
     int nt = std::max(1, std::min(N, TH / (cch * UP)));
     *NT = nt;
