@@ -95,6 +95,7 @@ SMALL_UL = [
     # per-warp staged inverse; N_sym = 2 runs the chunk loop with J > 1
     synth.Config("u32c40", "admm_ul", C=40, S=32, U=32, N=3, mod="qam64", snr_db=30),
     synth.Config("u32j2", "admm_ul", C=20, S=32, U=29, N=2, N_sym=2, mod="qam16", snr_db=25),
+    synth.CONFIGS["C"].scaled(N=5, N_sym=7, mod="qam64"),   # Table II shape: N_sym = 7 at C = 32, U = 16
     # N_sym = 16 at U = 32: the split kernels' shared memory cap shrinks the chunk (CCH 16 -> 15)
     synth.Config("u32j16", "admm_ul", C=17, S=32, U=32, N=2, N_sym=16, mod="qpsk", snr_db=20),
 ]
@@ -210,6 +211,7 @@ SMALL_DL = [
     synth.Config("u32c40", "admm_dl", C=40, S=32, U=32, N=3, mod="qam64"),
     synth.Config("u32j2", "admm_dl", C=20, S=32, U=29, N=2, N_sym=2, mod="qam16"),
     synth.Config("u32j16", "admm_dl", C=17, S=32, U=32, N=2, N_sym=16, mod="qpsk"),
+    synth.CONFIGS["D"].scaled(N=5, N_sym=7),                  # Table II shape (k_bf_gj's 2-CTA instance)
 ]
 
 
