@@ -36,6 +36,10 @@
  *    thread-local message for the last non-OK status.
  *  * Supported envelope (v1): 1 <= U <= 32 (users are zero-padded to the
  *    next of 4/8/16/32 internally, which is exact), 1 <= S <= 64, N_sym <= 16.
+ *  * Empty frames: N = 0 (no subcarriers) is valid.  After the scalar
+ *    arguments are validated the solvers return DBP_OK with nothing
+ *    enqueued and no consensus round (N is the same on every rank, so all
+ *    ranks skip together); data pointers may then be NULL.
  *  * Threading: a context is not thread-safe; use one per rank and thread.
  */
 #ifndef DBP_H
@@ -72,8 +76,8 @@ typedef enum { DBP_ALGO_ADMM_UL = 0, DBP_ALGO_CG_UL = 1, DBP_ALGO_ADMM_DL = 2, D
                DBP_ALGO_ZF_DL = 4 } dbp_algo;
 
 /* C = total clusters (all ranks), S = B_c antennas per cluster (P150),
- * U users, N subcarriers, N_sym symbols sharing one channel (P706-709).
- * B = C*S. */
+ * U users, N subcarriers (N >= 0), N_sym symbols sharing one channel
+ * (P706-709).  B = C*S. */
 typedef struct { int32_t C, S, U, N, N_sym; } dbp_dims;
 
 typedef struct dbp_ctx dbp_ctx;

@@ -184,8 +184,9 @@ struct Shape {
 static dbp_status check_dims(const dbp_ctx* c, const dbp_dims* d, Shape* sh) {
     if (!c) return fail(DBP_ERR_INVALID_ARG, "ctx is NULL");
     if (!d) return fail(DBP_ERR_INVALID_ARG, "dims is NULL");
-    if (d->C < 1 || d->S < 1 || d->U < 1 || d->N < 1 || d->N_sym < 1)
-        return fail(DBP_ERR_INVALID_ARG, "dims must be >= 1 (C=%d S=%d U=%d N=%d N_sym=%d)", d->C, d->S, d->U, d->N, d->N_sym);
+    // N = 0 is an empty frame (no subcarriers): valid, the solvers return DBP_OK with nothing enqueued.
+    if (d->C < 1 || d->S < 1 || d->U < 1 || d->N < 0 || d->N_sym < 1)
+        return fail(DBP_ERR_INVALID_ARG, "dims must be >= 1, N >= 0 (C=%d S=%d U=%d N=%d N_sym=%d)", d->C, d->S, d->U, d->N, d->N_sym);
     if (d->C % c->world) return fail(DBP_ERR_INVALID_ARG, "C=%d not divisible by world=%d (SPEC S107)", d->C, c->world);
     if (d->U > 32 || d->S > 64 || d->N_sym > 16)
         return fail(DBP_ERR_UNSUPPORTED, "v1 envelope: U<=32, S<=64, N_sym<=16 (got U=%d S=%d N_sym=%d)", d->U, d->S, d->N_sym);
@@ -445,7 +446,7 @@ extern "C" dbp_status dbp_detect_admm(dbp_ctx* c, const dbp_dims* d, const dbp_c
     Shape sh;
     dbp_status st = check_dims(c, d, &sh);
     if (st) return st;
-    if (!H || !y || !s_hat) return fail(DBP_ERR_INVALID_ARG, "H, y and s_hat are required");
+    if (sh.N > 0 && (!H || !y || !s_hat)) return fail(DBP_ERR_INVALID_ARG, "H, y and s_hat are required");
     if (!(rho > 0.f) || !std::isfinite(rho)) return fail(DBP_ERR_INVALID_ARG, "rho must be > 0 (SPEC S54)");
     if (!(gamma > 0.f) || !std::isfinite(gamma)) return fail(DBP_ERR_INVALID_ARG, "gamma must be > 0");
     if (!(Es > 0.f) || !(N0 >= 0.f) || !std::isfinite(N0) || !std::isfinite(Es)) return fail(DBP_ERR_INVALID_ARG, "need N0 >= 0, Es > 0");
@@ -453,6 +454,7 @@ extern "C" dbp_status dbp_detect_admm(dbp_ctx* c, const dbp_dims* d, const dbp_c
     if (!mod_ok(mod)) return fail(DBP_ERR_INVALID_ARG, "mod %d", mod);
     if (T < 1) return fail(DBP_ERR_INVALID_ARG, "T must be >= 1");
     if (prelr_smem(sh.UP, sh.S, sh.U, sh.J, true) > (size_t)c->max_smem) return fail(DBP_ERR_UNSUPPORTED, "S too large for the preprocessing tile");
+    if (sh.N == 0) return DBP_OK;                 // empty frame: nothing to compute or exchange
     CU(cudaSetDevice(c->device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const Layout Lw = layout(sh, DBP_ALGO_ADMM_UL);
@@ -533,11 +535,12 @@ extern "C" dbp_status dbp_detect_cg(dbp_ctx* c, const dbp_dims* d, const dbp_cf3
     Shape sh;
     dbp_status st = check_dims(c, d, &sh);
     if (st) return st;
-    if (!H || !y || !x_hat) return fail(DBP_ERR_INVALID_ARG, "H, y and x_hat are required");
+    if (sh.N > 0 && (!H || !y || !x_hat)) return fail(DBP_ERR_INVALID_ARG, "H, y and x_hat are required");
     if (!(rho >= 0.f) || !std::isfinite(rho)) return fail(DBP_ERR_INVALID_ARG, "rho must be >= 0 (P376)");
     if (!mod_ok(mod)) return fail(DBP_ERR_INVALID_ARG, "mod %d", mod);
     if (T < 1) return fail(DBP_ERR_INVALID_ARG, "T must be >= 1");
     if (prelr_smem(sh.UP, sh.S, sh.U, sh.J, true) > (size_t)c->max_smem) return fail(DBP_ERR_UNSUPPORTED, "S too large for the preprocessing tile");
+    if (sh.N == 0) return DBP_OK;                 // empty frame: nothing to compute or exchange
     CU(cudaSetDevice(c->device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const Layout Lw = layout(sh, DBP_ALGO_CG_UL);
@@ -610,13 +613,14 @@ extern "C" dbp_status dbp_beamform_admm(dbp_ctx* c, const dbp_dims* d, const dbp
     Shape sh;
     dbp_status st = check_dims(c, d, &sh);
     if (st) return st;
-    if (!Hd || !sv || !x) return fail(DBP_ERR_INVALID_ARG, "Hd, s and x are required");
+    if (sh.N > 0 && (!Hd || !sv || !x)) return fail(DBP_ERR_INVALID_ARG, "Hd, s and x are required");
     if (!(rho > 0.f) || !std::isfinite(rho)) return fail(DBP_ERR_INVALID_ARG, "rho must be > 0");
     if (!(gamma > 0.f) || !std::isfinite(gamma)) return fail(DBP_ERR_INVALID_ARG, "gamma must be > 0");
     if (!(eps >= 0.f)) return fail(DBP_ERR_INVALID_ARG, "eps must be >= 0");
     if (!std::isfinite(eps)) return fail(DBP_ERR_INVALID_ARG, "eps must be finite");
     if (T < 1) return fail(DBP_ERR_INVALID_ARG, "T must be >= 1");
     if (prelr_smem(sh.UP, sh.S, sh.U, sh.J, false) > (size_t)c->max_smem) return fail(DBP_ERR_UNSUPPORTED, "S too large for the preprocessing tile");
+    if (sh.N == 0) return DBP_OK;                 // empty frame: nothing to compute or exchange
     CU(cudaSetDevice(c->device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const Layout Lw = layout(sh, DBP_ALGO_ADMM_DL);
@@ -691,11 +695,12 @@ extern "C" dbp_status dbp_detect_mmse(dbp_ctx* c, const dbp_dims* d, const dbp_c
     Shape sh;
     dbp_status st = check_dims(c, d, &sh);
     if (st) return st;
-    if (!H || !y || !x_hat) return fail(DBP_ERR_INVALID_ARG, "H, y and x_hat are required");
+    if (sh.N > 0 && (!H || !y || !x_hat)) return fail(DBP_ERR_INVALID_ARG, "H, y and x_hat are required");
     if (!(N0 >= 0.f) || !std::isfinite(N0) || !(Es > 0.f) || !std::isfinite(Es))
         return fail(DBP_ERR_INVALID_ARG, "need N0 >= 0, Es > 0");
     if (!mod_ok(mod)) return fail(DBP_ERR_INVALID_ARG, "mod %d", mod);
     if (prelr_smem(sh.UP, sh.S, sh.U, sh.J, true) > (size_t)c->max_smem) return fail(DBP_ERR_UNSUPPORTED, "S too large for the preprocessing tile");
+    if (sh.N == 0) return DBP_OK;                 // empty frame: nothing to compute or exchange
     CU(cudaSetDevice(c->device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const Layout Lw = layout(sh, DBP_ALGO_MMSE_UL);
@@ -736,8 +741,9 @@ extern "C" dbp_status dbp_precode_zf(dbp_ctx* c, const dbp_dims* d, const dbp_cf
     Shape sh;
     dbp_status st = check_dims(c, d, &sh);
     if (st) return st;
-    if (!Hd || !sv || !x) return fail(DBP_ERR_INVALID_ARG, "Hd, s and x are required");
+    if (sh.N > 0 && (!Hd || !sv || !x)) return fail(DBP_ERR_INVALID_ARG, "Hd, s and x are required");
     if (prelr_smem(sh.UP, sh.S, sh.U, sh.J, false) > (size_t)c->max_smem) return fail(DBP_ERR_UNSUPPORTED, "S too large for the preprocessing tile");
+    if (sh.N == 0) return DBP_OK;                 // empty frame: nothing to compute or exchange
     CU(cudaSetDevice(c->device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const Layout Lw = layout(sh, DBP_ALGO_ZF_DL);

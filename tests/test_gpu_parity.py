@@ -537,3 +537,31 @@ def test_two_stream_schedule_matches_sequential(env):
             assert torch.equal(u, v)
     x_ref = oracle.beamform_admm(Hd, s, rho=dl.rho, T=dl.T)
     assert rel(conc[2].cpu().numpy(), x_ref) < TOL
+
+
+@pytest.mark.parametrize("host", [False, True])
+def test_empty_frame(env, host):
+    """N = 0 subcarriers (include/dbp.h 'Empty frames'): every solver returns DBP_OK with
+    empty outputs of the right shape and enqueues nothing; invalid scalars are still rejected."""
+    dbp, ctx, oracle, torch = env
+    C, S, U, J = 4, 8, 4, 2
+    def mk(*shape):
+        a = np.zeros(shape, np.complex64)
+        return a if host else torch.from_numpy(a).cuda()
+    H, y, Hd, s = mk(C, 0, S, U), mk(C, 0, J, S), mk(C, 0, U, S), mk(0, J, U)
+    before = ctx.stats()
+    for path in PATHS:
+        set_path(env, path)
+        for out in (dbp.detect_admm(ctx, H, y, N0=0.1, mod="qpsk", T=3),
+                    dbp.detect_cg(ctx, H, y, mod="qpsk", T=3),
+                    dbp.detect_mmse(ctx, H, y, N0=0.1, mod="qpsk")):
+            assert tuple(out[0].shape) == (0, J, U) and tuple(out[1].shape) == (0, J, U)
+        assert tuple(dbp.beamform_admm(ctx, Hd, s, T=3).shape) == (C, 0, J, S)
+        assert tuple(dbp.precode_zf(ctx, Hd, s).shape) == (C, 0, J, S)
+    set_path(env, "fused")
+    ctx.sync()
+    assert ctx.stats() == before
+    assert ctx.workspace_bytes(C, S, U, 0, J, "admm_ul") == 0
+    with pytest.raises(dbp.DbpError) as ei:
+        dbp.detect_admm(ctx, H, y, rho=0.0, mod="qpsk")
+    assert ei.value.status == 1
