@@ -238,6 +238,9 @@ def main():
                     help="world = 1: time the step with the three solvers back to back on one stream")
     ap.add_argument("--device-consensus", action="store_true",
                     help="world > 1: consensus inside the fused kernels over NVLink (DBP_OPT_DEVICE_CONSENSUS)")
+    ap.add_argument("--streams", type=int, default=2, choices=[2, 3],
+                    help="world-1 concurrent schedule: 2 = uplink pair on one stream, ADMM-DL on another; "
+                         "3 = every solver on its own stream")
     ap.add_argument("--ref-subcarriers", type=int, default=60)
     args = ap.parse_args()
 
@@ -305,20 +308,20 @@ def main():
     # tail.  world > 1: sequential on one stream (every solver issues one NCCL allreduce per round
     # on the same communicator; two streams could order them differently across ranks).
     concurrent = world == 1 and not args.sequential
-    side = (torch.cuda.Stream(dev), torch.cuda.Stream(dev)) if concurrent else None
-    join = (torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event())
+    side = tuple(torch.cuda.Stream(dev) for _ in range(args.streams)) if concurrent else None
+    join = (torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event())
 
     def step_concurrent(T, e_start):
-        sa, sb = side
-        sa.wait_event(e_start)
-        sb.wait_event(e_start)
+        sa, sb = side[0], side[1]
+        sc = side[2] if len(side) > 2 else sa
+        for sx in side:
+            sx.wait_event(e_start)
         solver("admm_ul", T, sa)
-        solver("cg_ul", T, sa)
+        solver("cg_ul", T, sc)
         solver("admm_dl", T, sb)
-        join[0].record(sa)
-        join[1].record(sb)
-        stream.wait_event(join[0])
-        stream.wait_event(join[1])
+        for i, sx in enumerate(side):
+            join[i].record(sx)
+            stream.wait_event(join[i])
 
     def timed_concurrent(K, T):
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
@@ -361,8 +364,8 @@ def main():
         for nm in order:
             solver(nm, UL.T)
         if concurrent:
-            join[2].record(stream)
-            step_concurrent(UL.T, join[2])
+            join[3].record(stream)
+            step_concurrent(UL.T, join[3])
     ctx.sync()
 
     clk = ClockSampler(local)
@@ -535,7 +538,8 @@ def main():
         launches = st1["kernel_launches"] - st0["kernel_launches"]
         line = {"metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_step_sequential": ms_seq,
-                "schedule": ("concurrent: ADMM-UL then CG-UL on one stream, ADMM-DL on a second"
+                "schedule": (("concurrent: each solver on its own stream" if args.streams == 3 else
+                              "concurrent: ADMM-UL then CG-UL on one stream, ADMM-DL on a second")
                              if concurrent else "sequential on one stream"),
                 "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Philox-4x32: i.i.d. Rayleigh "
