@@ -239,8 +239,11 @@ def main():
     ap.add_argument("--device-consensus", action="store_true",
                     help="world > 1: consensus inside the fused kernels over NVLink (DBP_OPT_DEVICE_CONSENSUS)")
     ap.add_argument("--streams", type=int, default=2, choices=[2, 3],
-                    help="world-1 concurrent schedule: 2 = uplink pair on one stream, ADMM-DL on another; "
+                    help="world-1 concurrent schedule: 2 = ADMM-UL then ADMM-DL on one stream, CG-UL on another; "
                          "3 = every solver on its own stream")
+    ap.add_argument("--plan", default=None,
+                    help="world-1 concurrent schedule as solver lists per stream, e.g. "
+                         "'admm_ul,cg_ul|admm_dl' (overrides --streams)")
     ap.add_argument("--ref-subcarriers", type=int, default=60)
     args = ap.parse_args()
 
@@ -303,22 +306,23 @@ def main():
             dbp.detect_cg(ctx, Hg, yg, rho=UL.N0, mod=UL.mod, T=T, x_hat=x_hat, hard=hard2, ws=ws["cg_ul"],
                           stream=sp)
 
-    # Step schedule.  world == 1: the uplink solvers (ADMM-UL, then CG-UL: same H, one stream) and
-    # the downlink solver (its own H^d) on two streams, so each kernel's CTAs fill the other's wave
-    # tail.  world > 1: sequential on one stream (every solver issues one NCCL allreduce per round
+    # Step schedule.  world == 1: ADMM-UL then ADMM-DL on one stream, CG-UL on a second, so each
+    # kernel's CTAs fill the other's wave tail (the fastest of the six two-lane orders measured,
+    # DESIGN.md section 6).  world > 1: sequential on one stream (every solver issues one NCCL allreduce per round
     # on the same communicator; two streams could order them differently across ranks).
     concurrent = world == 1 and not args.sequential
-    side = tuple(torch.cuda.Stream(dev) for _ in range(args.streams)) if concurrent else None
+    plan = args.plan or ("admm_ul|admm_dl|cg_ul" if args.streams == 3 else "admm_ul,admm_dl|cg_ul")
+    plan = [lane.split(",") for lane in plan.split("|")]
+    assert sorted(sum(plan, [])) == ["admm_dl", "admm_ul", "cg_ul"], "--plan must name each solver once"
+    side = tuple(torch.cuda.Stream(dev) for _ in plan) if concurrent else None
     join = (torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event())
 
     def step_concurrent(T, e_start):
-        sa, sb = side[0], side[1]
-        sc = side[2] if len(side) > 2 else sa
         for sx in side:
             sx.wait_event(e_start)
-        solver("admm_ul", T, sa)
-        solver("cg_ul", T, sc)
-        solver("admm_dl", T, sb)
+        for sx, lane in zip(side, plan):
+            for nm in lane:
+                solver(nm, T, sx)
         for i, sx in enumerate(side):
             join[i].record(sx)
             stream.wait_event(join[i])
@@ -538,8 +542,7 @@ def main():
         launches = st1["kernel_launches"] - st0["kernel_launches"]
         line = {"metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_step_sequential": ms_seq,
-                "schedule": (("concurrent: each solver on its own stream" if args.streams == 3 else
-                              "concurrent: ADMM-UL then CG-UL on one stream, ADMM-DL on a second")
+                "schedule": ("concurrent, one stream per lane: " + " | ".join(" then ".join(l) for l in plan)
                              if concurrent else "sequential on one stream"),
                 "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Philox-4x32: i.i.d. Rayleigh "
