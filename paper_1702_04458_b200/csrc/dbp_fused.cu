@@ -24,6 +24,7 @@
 // Versus the split path (k_prefold -> B^{-1} in HBM -> iteration kernels):
 // no per-pair inverse is written or re-read (2 x 42 MB for config C/D), the
 // DL output's second H read hits L2, and each solver is a single launch.
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -509,10 +510,12 @@ static bool launch_fz_t(const LaunchCtx& L, const float2* H, const float2* y, Fu
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, Z::WARPS * 32, Z::SMEM);
     const int ngroups = (a.N + a.NPC - 1) / a.NPC;
-#ifndef DBP_FZ_PERSIST
-#define DBP_FZ_PERSIST 1
-#endif
-    const int grid = DBP_FZ_PERSIST ? std::min(ngroups, g_sms_fz * std::max(per_sm, 1)) : ngroups;
+    // Grid per solver (bit SOLVER of the mask set: persistent, one wave of resident CTAs striding over the
+    // subcarrier groups; clear: one CTA per group, the hardware scheduler balancing the tail).  Measured
+    // on config C/D: one CTA per group is faster for ADMM-UL / ADMM-DL (99.5 -> 95.7,
+    // 111.5 -> 107.7 us) and persistent for CG-UL in the two-stream step.  DBP_FZ_PERSIST overrides the mask.
+    static const int persist = [] { const char* e = getenv("DBP_FZ_PERSIST"); return e ? atoi(e) : 0x19; }();
+    const int grid = (persist >> SOLVER) & 1 ? std::min(ngroups, g_sms_fz * std::max(per_sm, 1)) : ngroups;
     k<<<grid, Z::WARPS * 32, Z::SMEM, L.stream>>>(tmH, tmY, a);
     L.count(1);
     return true;
