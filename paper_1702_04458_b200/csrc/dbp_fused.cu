@@ -513,8 +513,9 @@ static bool launch_fz_t(const LaunchCtx& L, const float2* H, const float2* y, Fu
     // Grid per solver (bit SOLVER of the mask set: persistent, one wave of resident CTAs striding over the
     // subcarrier groups; clear: one CTA per group, the hardware scheduler balancing the tail).  Measured
     // on config C/D: one CTA per group is faster for ADMM-UL / ADMM-DL (99.5 -> 95.7,
-    // 111.5 -> 107.7 us) and persistent for CG-UL in the two-stream step.  DBP_FZ_PERSIST overrides the mask.
-    static const int persist = [] { const char* e = getenv("DBP_FZ_PERSIST"); return e ? atoi(e) : 0x19; }();
+    // 111.5 -> 107.7 us) and ZF-DL (83 -> 80 us), persistent for CG-UL (two-stream step) and MMSE-UL
+    // (66.5 vs 69 us).  DBP_FZ_PERSIST overrides the mask.
+    static const int persist = [] { const char* e = getenv("DBP_FZ_PERSIST"); return e ? atoi(e) : 0x09; }();
     const int grid = (persist >> SOLVER) & 1 ? std::min(ngroups, g_sms_fz * std::max(per_sm, 1)) : ngroups;
     k<<<grid, Z::WARPS * 32, Z::SMEM, L.stream>>>(tmH, tmY, a);
     L.count(1);
