@@ -111,7 +111,15 @@ typedef enum {
      * protocol); no collective per round.  Needs peer access between all ranks' GPUs (creating the
      * buffer is collective: every rank must make the same call).  2: as 1, and also at world == 1
      * against the rank's own buffer (a self-peer exercise of the device protocol for testing).
-     * Unverified across GPUs in round 1 (single-GPU environment). */
+     * Safety: the kernel is launched cooperatively on a persistent grid (all CTAs co-resident, or
+     * the launch fails); when this mode selects the fused kernel, a rank-local failure (unaligned
+     * H / y, launch error) returns an error instead of falling back to the NCCL path; every wait on
+     * a peer's round is bounded (DBP_XC_TIMEOUT_NS, 4 s), after which dbp_sync returns
+     * DBP_ERR_CUDA ("device consensus timed out") and the outputs are undefined -- a fault on one
+     * rank never hangs the GPUs.  Shapes the fused kernel does not take (N_sym > 1, U > 16) use the
+     * NCCL path on every rank (the decision depends only on the dims).  Round ids are consecutive
+     * within and across calls (ADMM-UL T, CG-UL T + 1, ADMM-DL T - 1 rounds).
+     * Unverified across GPUs (single-GPU environment). */
     DBP_OPT_DEVICE_CONSENSUS = 4
 } dbp_option;
 
@@ -236,7 +244,8 @@ dbp_status dbp_complexity(int algo, int mode, int metric, int64_t U, int64_t S, 
                           int64_t out[4]);
 
 /* Synchronise `stream`; returns DBP_ERR_NOT_HPD if a Cholesky pivot failed in
- * any call since the previous dbp_sync (and clears the flag), or
+ * any call since the previous dbp_sync (and clears the flag), DBP_ERR_CUDA if a
+ * device-consensus wait timed out (DBP_OPT_DEVICE_CONSENSUS), or
  * DBP_ERR_CUDA / DBP_ERR_NCCL for deferred runtime errors. */
 dbp_status dbp_sync(dbp_ctx* ctx, void* stream);
 

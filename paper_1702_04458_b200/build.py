@@ -45,22 +45,45 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
-    """Build libdbp.so in-tree (or `out`, with extra -D`defines`, for tuning variants)."""
+    """Build libdbp.so in-tree (or `out`, with extra -D`defines`, for tuning variants).
+    Each .cu compiles to its own object in parallel (build_var/obj), then one link."""
     if out is None and not force and not stale():
         return LIB
     dest = out or LIB
     inc, lib = nccl_dirs()
-    tmp = dest + f".tmp{os.getpid()}"
-    cmd = ["nvcc", ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",
-           "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
-           *[f"-D{d}" for d in defines], "-o", tmp] + sources() + ["-L", lib, "-l:libnccl.so.2", f"-Xlinker=-rpath={lib}"]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    tag = f"{os.getpid()}"
+    objdir = os.path.join(ROOT, "build_var", "obj")
+    os.makedirs(objdir, exist_ok=True)
+    flags = [ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+             "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc,
+             *[f"-D{d}" for d in defines]]
+    procs, objs = [], []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + f".{tag}.o")
+        objs.append(obj)
+        procs.append(subprocess.Popen(["nvcc", *flags, "-c", "-o", obj, src], stdout=subprocess.PIPE,
+                                      stderr=subprocess.PIPE, text=True))
+    failed = False
+    for p in procs:
+        o, e = p.communicate()
+        if p.returncode != 0:
+            sys.stderr.write(o + e)
+            failed = True
+        elif verbose:
+            sys.stderr.write(e)
+    if failed:
+        raise RuntimeError("nvcc failed building libdbp.so")
+    tmp = dest + f".tmp{tag}"
+    r = subprocess.run(["nvcc", ARCH, "-shared", "-o", tmp, *objs, "-L", lib, "-l:libnccl.so.2",
+                        f"-Xlinker=-rpath={lib}"], capture_output=True, text=True)
+    for o in objs:
+        try:
+            os.remove(o)
+        except OSError:
+            pass
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libdbp.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("nvcc failed linking libdbp.so")
     os.replace(tmp, dest)
     return dest
 

@@ -434,9 +434,20 @@ static XArgs xargs_for(dbp_ctx* c, int rounds) {
     x.rank = c->rank;
     x.cap = c->xcap;
     for (int r = 0; r < c->world; ++r) x.part[r] = static_cast<uint4*>(c->xpeer[r]);
+    // This call's rounds use ids base + 1 .. base + rounds; the next call continues at
+    // base + rounds + 1, so consecutive rounds -- also across calls -- alternate buffer parity
+    // (the two-buffer argument of DESIGN.md section 7 needs consecutive ids).
     x.base = c->xround;
-    c->xround += (unsigned)rounds + 2;      // round ids of different calls never overlap
+    c->xround += (unsigned)rounds;
     return x;
+}
+
+// Device consensus preconditions that can differ between ranks (checked before any rank-local
+// launch decision, so a rank never silently leaves the protocol its peers are spinning in).
+static dbp_status xc_check(const void* a, const void* b) {
+    if ((reinterpret_cast<uintptr_t>(a) & 15) || (reinterpret_cast<uintptr_t>(b) & 15))
+        return fail(DBP_ERR_UNSUPPORTED, "device consensus needs 16-byte aligned H / y (TMA); peers will time out");
+    return DBP_OK;
 }
 
 // ============================================================ Algorithm 1
@@ -477,6 +488,7 @@ extern "C" dbp_status dbp_detect_admm(dbp_ctx* c, const dbp_dims* d, const dbp_c
         // a1-a8 in one per-subcarrier kernel (world == 1, or world > 1 with device-side consensus)
         XArgs xa{};
         if (xc_on) {
+            if ((st = xc_check(dH, dy))) return st;
             if ((st = xbuf_ensure(c, sh.N, s))) return st;
             xa = xargs_for(c, T);
         }
@@ -490,6 +502,7 @@ extern "C" dbp_status dbp_detect_admm(dbp_ctx* c, const dbp_dims* d, const dbp_c
             c->consensus_rounds += T;
             return end_call(c, k, s);
         }
+        if (xc_on) return fail(DBP_ERR_CUDA, "fused ADMM-UL launch with device consensus failed (rank %d)", c->rank);
     }
     float2* yreg = reinterpret_cast<float2*>(k.ws + Lw.off[2]);
     // a1-a3: G_c = H_c^H H_c + rho I, B_c^{-1} and y^reg = B_c^{-1} H_c^H y_c (Alg. 1 lines 7-8)
@@ -572,6 +585,7 @@ extern "C" dbp_status dbp_detect_cg(dbp_ctx* c, const dbp_dims* d, const dbp_cf3
         // b1-b5 in one per-subcarrier kernel (world == 1, or world > 1 with device-side consensus)
         XArgs xa{};
         if (xc_on) {
+            if ((st = xc_check(k.io[0].dev, k.io[1].dev))) return st;
             if ((st = xbuf_ensure(c, sh.N, s))) return st;
             xa = xargs_for(c, T + 1);
         }
@@ -585,6 +599,7 @@ extern "C" dbp_status dbp_detect_cg(dbp_ctx* c, const dbp_dims* d, const dbp_cf3
             c->consensus_rounds += T + 1;
             return end_call(c, k, s);
         }
+        if (xc_on) return fail(DBP_ERR_CUDA, "fused CG launch with device consensus failed (rank %d)", c->rank);
     }
     // b1: per-pair Gram H_c^H H_c and matched filter H_c^H y_c, then the
     // per-GPU sums (G_loc, local y^MRC) in fixed cluster order.
@@ -654,8 +669,9 @@ extern "C" dbp_status dbp_beamform_admm(dbp_ctx* c, const dbp_dims* d, const dbp
         // c1-c4 in one per-subcarrier kernel (world == 1, or world > 1 with device-side consensus)
         XArgs xa{};
         if (xc_on) {
+            if ((st = xc_check(a.Hd, a.s))) return st;
             if ((st = xbuf_ensure(c, sh.N, s))) return st;
-            xa = xargs_for(c, T);
+            xa = xargs_for(c, T - 1);               // Alg. 3: T - 1 consensus rounds (P811)
         }
         bool launched = false;
         KT("fused_dl", (launched = launch_fused_dl(L, sh.UP, a.Hd, a.s, sh.C_loc, sh.C, sh.N, sh.S, sh.U, T, rho,
@@ -665,6 +681,7 @@ extern "C" dbp_status dbp_beamform_admm(dbp_ctx* c, const dbp_dims* d, const dbp
             c->consensus_rounds += T - 1;
             return end_call(c, k, s);
         }
+        if (xc_on) return fail(DBP_ERR_CUDA, "fused ADMM-DL launch with device consensus failed (rank %d)", c->rank);
     }
     // c1: B_c = H_c H_c^H + rho^{-1} I_U and its inverse (Alg. 3 lines 5-6)
     KT("pre_dl", launch_prelr(L, sh.UP, 2, a.Hd, nullptr, sh.S, sh.U, sh.J, sh.pairs(), a.rho_inv, G, nullptr));
@@ -832,6 +849,8 @@ extern "C" dbp_status dbp_sync(dbp_ctx* c, void* stream) {
     CU(cudaMemcpy(&flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost));
     if (flag) {
         CU(cudaMemset(c->d_flag, 0, sizeof(int)));
+        if (flag & DBP_FLAG_XC_TIMEOUT)
+            return fail(DBP_ERR_CUDA, "device consensus timed out waiting for a peer rank's round (outputs undefined)");
         return fail(DBP_ERR_NOT_HPD, "a Cholesky pivot was not positive/finite (non-HPD or non-finite input)");
     }
     CU(cudaGetLastError());

@@ -151,12 +151,35 @@ __device__ __forceinline__ void st_ll_sys(uint4* p, float2 v, unsigned id) {
     asm volatile("st.relaxed.sys.global.v4.u32 [%0], {%1, %2, %3, %4};"
                  ::"l"(p), "r"(__float_as_uint(v.x)), "r"(id), "r"(__float_as_uint(v.y)), "r"(id) : "memory");
 }
-__device__ __forceinline__ float2 ld_ll_sys(const uint4* p, unsigned id) {
+// Bounded wait: polls until both ids equal `id`; after DBP_XC_TIMEOUT_NS of %globaltimer (or as
+// soon as another thread of this GPU has timed out) it sets bit DBP_FLAG_XC_TIMEOUT of `flag`
+// and returns 0 -- a protocol or launch fault on any rank becomes DBP_ERR_CUDA from dbp_sync,
+// never a hung GPU.
+#ifndef DBP_XC_TIMEOUT_NS
+#define DBP_XC_TIMEOUT_NS 4000000000ull
+#endif
+constexpr int DBP_FLAG_XC_TIMEOUT = 2;
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ float2 ld_ll_sys(const uint4* p, unsigned id, int* flag) {
     unsigned a, b, c, d;
-    do {
+    unsigned long long t0 = 0;
+    for (unsigned k = 0;; ++k) {
         asm volatile("ld.relaxed.sys.global.v4.u32 {%0, %1, %2, %3}, [%4];"
                      : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(p) : "memory");
-    } while (b != id || d != id);
+        if (b == id && d == id) break;
+        if ((k & 255u) == 0u) {
+            const unsigned long long now = globaltimer_ns();
+            if (k == 0u) t0 = now;
+            if (now - t0 > DBP_XC_TIMEOUT_NS || (*(volatile int*)flag & DBP_FLAG_XC_TIMEOUT)) {
+                atomicOr(flag, DBP_FLAG_XC_TIMEOUT);
+                return make_float2(0.f, 0.f);
+            }
+        }
+    }
     return make_float2(__uint_as_float(a), __uint_as_float(c));
 }
 // 16-B asynchronous global -> shared copies (LDGSTS), completed by cp_async_wait_all.

@@ -303,7 +303,8 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                             float2 sum = make_float2(0.f, 0.f);
                             for (int pk = 0; pk < a.xc.world; ++pk)
                                 sum = c_add(sum, ld_ll_sys(a.xc.part[a.xc.rank] +
-                                                           ((size_t)(par * 8 + pk) * a.xc.cap + nn) * UP + u, rid));
+                                                           ((size_t)(par * 8 + pk) * a.xc.cap + nn) * UP + u, rid,
+                                                           a.flag));
                             return sum;
                         };
                         float2 r = xsum(1, Sv[warp * UP + u]);  // line 6: r = y^MRC (consensus), p = r, x = 0
@@ -387,7 +388,8 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                         for (int r = 0; r < a.xc.world; ++r) st_ll_sys(a.xc.part[r] + o, acc, rid);
                         for (int p = 0; p < a.xc.world; ++p)        // rank order: identical sums everywhere
                             sum = c_add(sum, ld_ll_sys(a.xc.part[a.xc.rank] +
-                                                       ((size_t)(par * 8 + p) * a.xc.cap + n0 + jj) * UP + u, rid));
+                                                       ((size_t)(par * 8 + p) * a.xc.cap + n0 + jj) * UP + u, rid,
+                                                       a.flag));
                     }
                     Sv[tid] = do_prox ? prox(sum, a.px) : sum;
                 }
@@ -451,7 +453,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                     w[m] = c_sub(mm[m], lam[m]);                                   // line 12
                 }
                 float2 W[R];
-                consensus(t, w, false, W);                                         // line 13
+                consensus(t - 1, w, false, W);                                     // line 13 (round ids base+1..)
                 float2 dv[R];
                 float nrm2 = 0.f;
 #pragma unroll
@@ -515,7 +517,30 @@ static bool launch_fz_t(const LaunchCtx& L, const float2* H, const float2* y, Fu
     // on config C/D: one CTA per group is faster for ADMM-UL / ADMM-DL (99.5 -> 95.7,
     // 111.5 -> 107.7 us) and ZF-DL (83 -> 80 us), persistent for CG-UL (two-stream step) and MMSE-UL
     // (66.5 vs 69 us).  DBP_FZ_PERSIST overrides the mask.
-    static const int persist = [] { const char* e = getenv("DBP_FZ_PERSIST"); return e ? atoi(e) : 0x09; }();
+    static const int persist = [] { const char* e = getenv("DBP_FZ_PERSIST"); return e ? (int)strtol(e, nullptr, 0) : 0x09; }();
+    if (a.xc.on) {
+        // Device-side consensus: CTAs spin on peers' rounds, so every CTA of the grid must be resident
+        // at once on every rank.  Persistent grid (identical on every rank: same
+        // N, same device model) launched cooperatively -- the launch fails instead of deadlocking if
+        // the grid cannot be co-resident.
+        if (per_sm < 1) return false;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)std::min(ngroups, g_sms_fz * per_sm));
+        cfg.blockDim = dim3(Z::WARPS * 32);
+        cfg.dynamicSmemBytes = Z::SMEM;
+        cfg.stream = L.stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, k, tmH, tmY, a) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        L.count(1);
+        return true;
+    }
     const int grid = (persist >> SOLVER) & 1 ? std::min(ngroups, g_sms_fz * std::max(per_sm, 1)) : ngroups;
     k<<<grid, Z::WARPS * 32, Z::SMEM, L.stream>>>(tmH, tmY, a);
     L.count(1);

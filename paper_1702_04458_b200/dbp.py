@@ -136,16 +136,54 @@ def _empty_like_io(ref, shape, kind):
     return np.empty(shape, dtype=np.complex64 if kind == "c" else np.uint8)
 
 
-def _need_contig(*xs):
-    for x in xs:
+def _check_args(ctx, spec, ws=None):
+    """Validate every array against the dims the C ABI will be told (the library trusts them):
+    spec = [(name, array or None, expected shape, 'c' complex64 | 'u' uint8), ...].  All arrays
+    must be on one side -- torch tensors on ctx's CUDA device, or host (numpy / CPU) arrays --
+    C-contiguous, and of the exact shape and dtype; raises ValueError otherwise."""
+    kinds = set()
+    for name, x, shape, kind in spec:
         if x is None:
             continue
-        ok = x.is_contiguous() if _is_torch(x) else x.flags["C_CONTIGUOUS"]
+        shp = tuple(int(v) for v in x.shape)
+        if shp != tuple(shape):
+            raise ValueError(f"{name}: shape {shp}, expected {tuple(shape)}")
         dt = str(x.dtype)
-        if not ok:
-            raise ValueError("arrays must be contiguous")
-        if "complex64" not in dt and "uint8" not in dt:
-            raise ValueError(f"complex64 (or uint8) required, got {dt}")
+        want = "complex64" if kind == "c" else "uint8"
+        if not dt.endswith(want):
+            raise ValueError(f"{name}: dtype {dt}, expected {want}")
+        if _is_torch(x):
+            if not x.is_contiguous():
+                raise ValueError(f"{name}: must be contiguous")
+            if x.is_cuda:
+                if x.device.index != ctx.device:
+                    raise ValueError(f"{name}: on {x.device}, the context is on cuda:{ctx.device}")
+                kinds.add("device")
+            else:
+                kinds.add("host")
+        else:
+            if not x.flags["C_CONTIGUOUS"]:
+                raise ValueError(f"{name}: must be C-contiguous")
+            kinds.add("host")
+    if len(kinds) > 1:
+        raise ValueError("all arrays of one call must be device tensors or all host arrays")
+    if ws is not None:
+        if not (_is_torch(ws) and ws.is_cuda and ws.device.index == ctx.device):
+            raise ValueError(f"ws must be a CUDA tensor on cuda:{ctx.device}")
+        if not ws.is_contiguous():
+            raise ValueError("ws must be contiguous")
+
+
+def _dims4(x, name):
+    if len(x.shape) != 4:
+        raise ValueError(f"{name}: expected 4 dims, got shape {tuple(x.shape)}")
+    return tuple(int(v) for v in x.shape)
+
+
+def _dim(x, i, name):
+    if len(x.shape) <= i:
+        raise ValueError(f"{name}: shape {tuple(x.shape)} has no dim {i}")
+    return int(x.shape[i])
 
 
 class Context:
@@ -209,13 +247,14 @@ def _cur_stream():
 def detect_admm(ctx: Context, H, y, *, rho=1.0, gamma=1.0, N0=0.0, Es=1.0, reg="mmse", mod="qam64", T=5,
                 s_hat=None, hard=None, want_hard=True, ws=None, stream=None):
     """Algorithm 1.  H [C_loc][N][S][U], y [C_loc][N][N_sym][S] -> (s_hat [N][N_sym][U], hard)."""
-    C_loc, N, S, U = H.shape
-    J = y.shape[2]
+    C_loc, N, S, U = _dims4(H, "H")
+    J = _dim(y, 2, "y")
     if s_hat is None:
         s_hat = _empty_like_io(H, (N, J, U), "c")
     if hard is None and want_hard:
         hard = _empty_like_io(H, (N, J, U), "u")
-    _need_contig(H, y, s_hat, hard)
+    _check_args(ctx, [("H", H, (C_loc, N, S, U), "c"), ("y", y, (C_loc, N, J, S), "c"),
+                      ("s_hat", s_hat, (N, J, U), "c"), ("hard", hard, (N, J, U), "u")], ws)
     d = Dims(C_loc * ctx.world, S, U, N, J)
     wsb = 0 if ws is None else (ws.numel() * ws.element_size() if _is_torch(ws) else ws.nbytes)
     _check(load().dbp_detect_admm(ctx._h, ctypes.byref(d), _ptr(H), _ptr(y), rho, gamma, N0, Es, REG[reg],
@@ -226,13 +265,14 @@ def detect_admm(ctx: Context, H, y, *, rho=1.0, gamma=1.0, N0=0.0, Es=1.0, reg="
 def detect_cg(ctx: Context, H, y, *, rho=0.0, mod="qam64", T=5, x_hat=None, hard=None, want_hard=True,
               ws=None, stream=None):
     """Algorithm 2.  -> (x_hat [N][N_sym][U], hard)."""
-    C_loc, N, S, U = H.shape
-    J = y.shape[2]
+    C_loc, N, S, U = _dims4(H, "H")
+    J = _dim(y, 2, "y")
     if x_hat is None:
         x_hat = _empty_like_io(H, (N, J, U), "c")
     if hard is None and want_hard:
         hard = _empty_like_io(H, (N, J, U), "u")
-    _need_contig(H, y, x_hat, hard)
+    _check_args(ctx, [("H", H, (C_loc, N, S, U), "c"), ("y", y, (C_loc, N, J, S), "c"),
+                      ("x_hat", x_hat, (N, J, U), "c"), ("hard", hard, (N, J, U), "u")], ws)
     d = Dims(C_loc * ctx.world, S, U, N, J)
     wsb = 0 if ws is None else (ws.numel() * ws.element_size() if _is_torch(ws) else ws.nbytes)
     _check(load().dbp_detect_cg(ctx._h, ctypes.byref(d), _ptr(H), _ptr(y), rho, MOD[mod], T, _ptr(x_hat),
@@ -242,11 +282,12 @@ def detect_cg(ctx: Context, H, y, *, rho=0.0, mod="qam64", T=5, x_hat=None, hard
 
 def beamform_admm(ctx: Context, Hd, s, *, rho=1.0, gamma=1.0, eps=0.0, T=5, x=None, ws=None, stream=None):
     """Algorithm 3.  Hd [C_loc][N][U][S], s [N][N_sym][U] -> x [C_loc][N][N_sym][S]."""
-    C_loc, N, U, S = Hd.shape
-    J = s.shape[1]
+    C_loc, N, U, S = _dims4(Hd, "Hd")
+    J = _dim(s, 1, "s")
     if x is None:
         x = _empty_like_io(Hd, (C_loc, N, J, S), "c")
-    _need_contig(Hd, s, x)
+    _check_args(ctx, [("Hd", Hd, (C_loc, N, U, S), "c"), ("s", s, (N, J, U), "c"),
+                      ("x", x, (C_loc, N, J, S), "c")], ws)
     d = Dims(C_loc * ctx.world, S, U, N, J)
     wsb = 0 if ws is None else (ws.numel() * ws.element_size() if _is_torch(ws) else ws.nbytes)
     _check(load().dbp_beamform_admm(ctx._h, ctypes.byref(d), _ptr(Hd), _ptr(s), rho, gamma, eps, T, _ptr(x),
@@ -257,13 +298,14 @@ def beamform_admm(ctx: Context, Hd, s, *, rho=1.0, gamma=1.0, eps=0.0, T=5, x=No
 def detect_mmse(ctx: Context, H, y, *, N0=0.0, Es=1.0, mod="qam64", x_hat=None, hard=None, want_hard=True,
                 ws=None, stream=None):
     """Centralized MMSE-UL detection (N0 = 0: ZF) over all clusters.  -> (x_hat [N][N_sym][U], hard)."""
-    C_loc, N, S, U = H.shape
-    J = y.shape[2]
+    C_loc, N, S, U = _dims4(H, "H")
+    J = _dim(y, 2, "y")
     if x_hat is None:
         x_hat = _empty_like_io(H, (N, J, U), "c")
     if hard is None and want_hard:
         hard = _empty_like_io(H, (N, J, U), "u")
-    _need_contig(H, y, x_hat, hard)
+    _check_args(ctx, [("H", H, (C_loc, N, S, U), "c"), ("y", y, (C_loc, N, J, S), "c"),
+                      ("x_hat", x_hat, (N, J, U), "c"), ("hard", hard, (N, J, U), "u")], ws)
     d = Dims(C_loc * ctx.world, S, U, N, J)
     wsb = 0 if ws is None else (ws.numel() * ws.element_size() if _is_torch(ws) else ws.nbytes)
     _check(load().dbp_detect_mmse(ctx._h, ctypes.byref(d), _ptr(H), _ptr(y), N0, Es, MOD[mod], _ptr(x_hat),
@@ -273,11 +315,12 @@ def detect_mmse(ctx: Context, H, y, *, N0=0.0, Es=1.0, mod="qam64", x_hat=None, 
 
 def precode_zf(ctx: Context, Hd, s, *, x=None, ws=None, stream=None):
     """Centralized ZF-DL precoding x_c = H_c^H (sum_c H_c H_c^H)^{-1} s -> x [C_loc][N][N_sym][S]."""
-    C_loc, N, U, S = Hd.shape
-    J = s.shape[1]
+    C_loc, N, U, S = _dims4(Hd, "Hd")
+    J = _dim(s, 1, "s")
     if x is None:
         x = _empty_like_io(Hd, (C_loc, N, J, S), "c")
-    _need_contig(Hd, s, x)
+    _check_args(ctx, [("Hd", Hd, (C_loc, N, U, S), "c"), ("s", s, (N, J, U), "c"),
+                      ("x", x, (C_loc, N, J, S), "c")], ws)
     d = Dims(C_loc * ctx.world, S, U, N, J)
     wsb = 0 if ws is None else (ws.numel() * ws.element_size() if _is_torch(ws) else ws.nbytes)
     _check(load().dbp_precode_zf(ctx._h, ctypes.byref(d), _ptr(Hd), _ptr(s), _ptr(x), _ptr(ws), wsb,
@@ -297,7 +340,7 @@ def slice_bits(ctx: Context, x, mod: str, out=None, stream=None):
     """Hard slicer (P210) on device or host complex64 data."""
     if out is None:
         out = _empty_like_io(x, tuple(x.shape), "u")
-    _need_contig(x, out)
+    _check_args(ctx, [("x", x, tuple(int(v) for v in x.shape), "c"), ("out", out, tuple(int(v) for v in x.shape), "u")])
     n = x.numel() if _is_torch(x) else x.size
     _check(load().dbp_slice(ctx._h, MOD[mod], n, _ptr(x), _ptr(out), _stream(stream, x)))
     return out

@@ -18,3 +18,14 @@ def oracle_mod():
     import oracle
     oracle.build()
     return oracle
+
+
+def pytest_terminal_summary(terminalreporter):
+    """Report the worst GPU-vs-oracle soft errors seen (whole-tensor rel-L2 and the largest
+    per-subcarrier rel-L2), SURVEY 8(c)'s parity contract."""
+    mod = sys.modules.get("tests.test_gpu_parity") or sys.modules.get("test_gpu_parity")
+    worst = getattr(mod, "WORST", None)
+    if worst and (worst["rel_l2"] or worst["max_subcarrier"]):
+        terminalreporter.write_line(
+            f"parity worst: rel-L2 {worst['rel_l2']:.3e}, max per-subcarrier rel-L2 {worst['max_subcarrier']:.3e} "
+            f"(bar 1e-4)")

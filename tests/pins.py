@@ -76,6 +76,16 @@ def box_ls(H: np.ndarray, y: np.ndarray, r: float) -> np.ndarray:
     return res.x[:U] + 1j * res.x[U:]
 
 
+def box_ls_real(H: np.ndarray, y: np.ndarray, r: float) -> np.ndarray:
+    """BPSK box equalizer (P344): s real in [-r, r]^U minimising ||y - H s||; the complex
+    system stacked as [Re H; Im H] s = [Re y; Im y], scipy bounded least squares."""
+    from scipy.optimize import lsq_linear
+    A = np.concatenate([H.real, H.imag], axis=0)
+    b = np.concatenate([y.real, y.imag])
+    res = lsq_linear(A, b, bounds=(-r, r), method="bvls", tol=1e-14)
+    return res.x + 0j
+
+
 def constellation(mod: str) -> np.ndarray:
     """All points of the Es = 1 Gray alphabet (reading 17)."""
     m, norm = {"bpsk": (2, 1.0), "qpsk": (2, 2.0), "qam16": (4, 10.0), "qam64": (8, 42.0)}[mod]

@@ -64,3 +64,39 @@ def test_product_package_does_not_import_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "dbp_oracle" not in txt, f
+
+
+def test_binding_validates_shapes_and_dtypes():
+    """the wrappers check every array against the dims passed to the C ABI (which
+    trusts them) before any call -- a mismatched y / output buffer / dtype raises ValueError
+    instead of an out-of-bounds device or host access."""
+    import types
+
+    import numpy as np
+    import pytest as _pt
+
+    from paper_1702_04458_b200 import dbp
+    ctx = types.SimpleNamespace(device=0, world=1, rank=0)
+    C, N, S, U = 2, 5, 8, 4
+    H = np.zeros((C, N, S, U), np.complex64)
+    y = np.zeros((C, N, 1, S), np.complex64)
+    Hd = np.zeros((C, N, U, S), np.complex64)
+    s = np.zeros((N, 1, U), np.complex64)
+    bad = [
+        lambda: dbp.detect_admm(ctx, H, y[:, :4]),                                    # y: fewer subcarriers
+        lambda: dbp.detect_admm(ctx, H, np.zeros((C, N, 1, S + 1), np.complex64)),    # y: wrong S
+        lambda: dbp.detect_admm(ctx, H, y, s_hat=np.zeros((N, 1, U - 1), np.complex64)),
+        lambda: dbp.detect_admm(ctx, H, y, hard=np.zeros((N, 1, U), np.complex64)),   # hard must be uint8
+        lambda: dbp.detect_admm(ctx, H.astype(np.complex128), y),
+        lambda: dbp.detect_cg(ctx, H, y.astype(np.uint8)),                            # uint8 for a complex input
+        lambda: dbp.detect_cg(ctx, H, y, x_hat=np.zeros((N + 1, 1, U), np.complex64)),
+        lambda: dbp.beamform_admm(ctx, Hd, s[:3]),
+        lambda: dbp.beamform_admm(ctx, Hd, s, x=np.zeros((C, N, 1, S - 1), np.complex64)),
+        lambda: dbp.detect_mmse(ctx, H[:, :, :, :3], y),
+        lambda: dbp.precode_zf(ctx, Hd, np.zeros((N, 1, U + 1), np.complex64)),
+        lambda: dbp.detect_admm(ctx, np.asfortranarray(H), y),                        # not C-contiguous
+        lambda: dbp.detect_admm(ctx, H[0], y),                                        # 3-D H
+    ]
+    for f in bad:
+        with _pt.raises(ValueError):
+            f()

@@ -28,8 +28,28 @@ def env():
     ctx.close()
 
 
+WORST = {"rel_l2": 0.0, "max_subcarrier": 0.0}   # reported in the terminal summary (conftest.py)
+
+
 def rel(a, b):
-    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-30))
+    """max(relative L2 over the whole tensor, largest per-subcarrier relative L2) -- SURVEY
+    8(c)'s contract asks for both.  The subcarrier axis is 0 for [N][N_sym][U] outputs and 1
+    for the downlink's [C][N][N_sym][S]; a subcarrier's denominator is floored at 1e-3 of
+    the tensor's RMS subcarrier norm so an all-zero subcarrier cannot divide by ~0."""
+    a = np.asarray(a)
+    b = np.asarray(b)
+    whole = float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+    ax = 1 if b.ndim == 4 else 0
+    if b.ndim == 0 or b.shape[ax] == 0:
+        return whole
+    ar = np.moveaxis(a, ax, 0).reshape(b.shape[ax], -1)
+    br = np.moveaxis(b, ax, 0).reshape(b.shape[ax], -1)
+    nb = np.linalg.norm(br, axis=1)
+    floor = max(1e-3 * float(np.sqrt(np.mean(nb ** 2))), 1e-30)
+    per = float(np.max(np.linalg.norm(ar - br, axis=1) / np.maximum(nb, floor)))
+    WORST["rel_l2"] = max(WORST["rel_l2"], whole)
+    WORST["max_subcarrier"] = max(WORST["max_subcarrier"], per)
+    return max(whole, per)
 
 
 _LV = {"bpsk": (2, 1.0), "qpsk": (2, 2.0), "qam16": (4, 10.0), "qam64": (8, 42.0)}
@@ -119,12 +139,19 @@ def test_admm_regs_and_T(env, reg, T):
         check_hard(hard, hard_ref, s_ref, cfg.mod)
 
 
-def test_admm_bpsk_box(env):
-    cfg = synth.Config("bpsk", "admm_ul", C=2, S=8, U=4, N=8, mod="bpsk", snr_db=5)
-    s, hard, s_ref, hard_ref = run_admm(env, cfg, False, reg="box", T=6)
+@pytest.mark.parametrize("mod", ["bpsk", "qpsk", "qam16", "qam64"])
+@pytest.mark.parametrize("path", PATHS)
+def test_admm_box_all_mods(env, mod, path):
+    """BOX prox (P335-343) at every alphabet's radius, BPSK's real segment (P344), on all
+    three paths; 0 dB so the clamp is active (checked on the oracle's output)."""
+    cfg = synth.Config("box", "admm_ul", C=4, S=8, U=8, N=12, mod=mod, snr_db=0)
+    s, hard, s_ref, hard_ref = run_admm(env, cfg, path, reg="box", T=6)
+    r = {"bpsk": 1.0, "qpsk": 1 / np.sqrt(2), "qam16": 3 / np.sqrt(10), "qam64": 7 / np.sqrt(42)}[mod]
+    assert np.any(np.isclose(np.abs(s_ref.real), r, rtol=0, atol=1e-12))
     assert rel(s, s_ref) < TOL
-    assert np.all(s.imag == 0)
-    check_hard(hard, hard_ref, s_ref, "bpsk")
+    if mod == "bpsk":
+        assert np.all(s.imag == 0)
+    check_hard(hard, hard_ref, s_ref, mod)
 
 
 def test_admm_host_pointers_match_device(env):

@@ -124,15 +124,30 @@ def test_admm_zf_converges_to_ls(oracle_mod):
     assert pins.rel(s_hat[0, 0], pins.ls(full_H(H), full_y(y))) < 1e-6
 
 
-def test_admm_box_converges_to_bounded_ls(oracle_mod):
-    """(E2-BOX) (P339-343): fixed point = box-constrained LS (scipy bvls)."""
+BOX_MODS = ["bpsk", "qpsk", "qam16", "qam64"]
+
+
+def box_r(mod):
+    """Box radius from the alphabet itself (largest per-axis coordinate, P343, reading 17)."""
+    return float(np.max(pins.constellation(mod).real))
+
+
+@pytest.mark.parametrize("mod", BOX_MODS)
+def test_admm_box_converges_to_bounded_ls(oracle_mod, mod):
+    """(E2-BOX) (P339-343): fixed point = box-constrained LS (scipy bvls) on the radius of
+    each alphabet; BPSK (P344): real-valued s, the real-stacked system with Im(s) = 0."""
     rng = np.random.default_rng(5)
+    r = box_r(mod)
     hits = 0
     for _ in range(4):
-        H, y, _, _ = rand_ul(rng, 2, 4, 4, snr_db=0)
-        s_hat, _ = oracle_mod.detect_admm(H, y, reg="box", rho=1.0, T=3000, mod="qpsk")
-        ref = pins.box_ls(full_H(H), full_y(y), 1 / np.sqrt(2))
-        hits += np.any(np.abs(np.abs(ref.real) - 1 / np.sqrt(2)) < 1e-9)
+        H, y, _, _ = rand_ul(rng, 2, 4, 4, snr_db=0, mod=mod)
+        s_hat, _ = oracle_mod.detect_admm(H, y, reg="box", rho=1.0, T=3000, mod=mod)
+        if mod == "bpsk":
+            ref = pins.box_ls_real(full_H(H), full_y(y), r)
+            assert np.all(s_hat[0, 0].imag == 0)
+        else:
+            ref = pins.box_ls(full_H(H), full_y(y), r)
+        hits += np.any(np.abs(np.abs(ref.real) - r) < 1e-9) + np.any(np.abs(np.abs(ref.imag) - r) < 1e-9)
         assert pins.rel(s_hat[0, 0], ref) < 1e-5
     assert hits > 0  # the box is active in at least one instance
 
@@ -148,18 +163,21 @@ def test_admm_mode_equivalence(oracle_mod, S, U):
         assert pins.rel(a, b) < 1e-9
 
 
-@pytest.mark.parametrize("reg", ["mmse", "zf", "box"])
-def test_admm_steps_satisfy_E1_E2_E3(oracle_mod, reg):
+@pytest.mark.parametrize("reg,mod", [("mmse", "qpsk"), ("zf", "qpsk")] + [("box", m) for m in BOX_MODS])
+def test_admm_steps_satisfy_E1_E2_E3(oracle_mod, reg, mod):
     """Every iterate satisfies the optimality conditions of (E1), (E2)/Lemma 1 and
-    the update (E3) as reordered by Alg. 1 (P238-249, P304-312, P356-357)."""
+    the update (E3) as reordered by Alg. 1 (P238-249, P304-312, P356-357).  BOX runs
+    every alphabet's radius (P343) at 0 dB so the clamp is active; BPSK projects onto
+    the real segment [-1, 1] (P344)."""
     rng = np.random.default_rng(17)
     C, S, U, rho, gamma, T = 3, 6, 4, 0.8, 1.0, 6
-    H, y, _, N0 = rand_ul(rng, C, S, U, snr_db=5)
+    H, y, _, N0 = rand_ul(rng, C, S, U, snr_db=0 if reg == "box" else 5, mod=mod)
     s, z, lam = oracle_mod.detect_admm_trace(H, y, rho=rho, gamma=gamma, N0=N0, reg=reg, T=T,
-                                             mod="qpsk")
+                                             mod=mod)
     Hc = [H[c, 0].astype(np.complex128) for c in range(C)]
     yc = [y[c, 0, 0].astype(np.complex128) for c in range(C)]
-    r = 1 / np.sqrt(2)
+    r = box_r(mod)
+    clipped = 0
     for t in range(T):
         for c in range(C):
             sp = s[t - 1] if t > 0 else np.zeros(U)
@@ -174,10 +192,17 @@ def test_admm_steps_satisfy_E1_E2_E3(oracle_mod, reg):
             assert np.linalg.norm(N0 * s[t] + rho * (C * s[t] - w)) < 1e-10
         elif reg == "zf":
             assert np.linalg.norm(C * s[t] - w) < 1e-10
-        else:               # projection of v = w/C onto the box (Lemma 1 + P343)
+        else:               # projection of v = w/C onto the box (Lemma 1 + P343; BPSK P344)
             v = w / C
-            want = np.clip(v.real, -r, r) + 1j * np.clip(v.imag, -r, r)
+            if mod == "bpsk":
+                want = np.clip(v.real, -r, r) + 0j
+                clipped += int(np.sum(np.abs(v.real) > r))
+            else:
+                want = np.clip(v.real, -r, r) + 1j * np.clip(v.imag, -r, r)
+                clipped += int(np.sum(np.abs(v.real) > r) + np.sum(np.abs(v.imag) > r))
             assert np.allclose(s[t], want, atol=1e-12)
+    if reg == "box":
+        assert clipped > 0   # the radius constant is exercised, not just the identity branch
 
 
 def test_admm_invariances(oracle_mod):
