@@ -51,7 +51,7 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
         return LIB
     dest = out or LIB
     inc, lib = nccl_dirs()
-    tag = f"{os.getpid()}"
+    tag = f"{os.getpid()}.{abs(hash((dest, tuple(defines)))) % 100000}"
     objdir = os.path.join(ROOT, "build_var", "obj")
     os.makedirs(objdir, exist_ok=True)
     flags = [ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

@@ -34,6 +34,7 @@
 #include "dbp_device.cuh"
 #include "dbp_fold.cuh"
 #include "dbp_internal.h"
+#include "dbp_tc.cuh"
 
 #pragma nv_diag_suppress 128   // SOLVER 0 continues before the inverse: "loop is not reachable"
 
@@ -51,20 +52,34 @@ struct FZ {
 #define DBP_FZ_NST 2
 #endif
     static constexpr int NST = DBP_FZ_NST;
+#ifndef DBP_FZ_TC
+#define DBP_FZ_TC 0
+#endif
+    // UP = 16: the per-pair Gram (+ matched filter) runs on the tensor cores (dbp_tc.cuh); a
+    // TMA stage is then one whole pair (runtime size, 128B-swizzled), the warp's 8 pairs are
+    // computed one after another and handed to the folded layout through shared memory in two
+    // halves of 4 pairs (gtri / mfl, aliasing the mat-vec partials ybuf).
+    static constexpr bool TC = UP == 16 && DBP_FZ_TC;
     static constexpr int PWL = F::PW * F::PLP;            // pivot / vector lines (float2)
     static constexpr int DLN = F::PW * UP;                // Jacobi scales (float)
     static constexpr int YB = F::PW * fold_ybuf_pair<UP>(); // mat-vec partials (float2), padded
-    static constexpr int WREG = (NST * G::STG + PWL * 8 + DLN * 4 + YB * 8 + 127) / 128 * 128;
+    static constexpr int TCB = TC ? 4 * F::TRI + 4 * UP : 0;  // TC hand-off: 4 packed Grams + 4 H^H y
+    static constexpr int UNI = (YB > TCB ? YB : TCB);      // float2
+    // per-warp region after the ring: pivot lines, Jacobi scales, ybuf / TC hand-off
+    static constexpr int LOC = (PWL * 8 + DLN * 4 + UNI * 8 + 127) / 128 * 128;
+    static constexpr int WREG = (NST * G::STG + LOC + 127) / 128 * 128;   // non-TC (stage size static)
     // CTA-shared: per-warp consensus partials [WARPS][UP] + per-subcarrier sums [4][UP];
     // CG: per-warp Gram partials [WARPS][TRI] + per-subcarrier Gram [4][TRI]
     static constexpr int CBUF = WARPS * UP * 8 + WARPS * UP * 8;       // Wp + Sv
     static constexpr int GBUF = SUMS ? 2 * WARPS * F::TRI * 8 : 0;
-    static constexpr size_t SMEM = 128 + (size_t)WARPS * WREG + CBUF + GBUF;
+    // + 1024: the base is rounded up to 1024 B in the kernel (128B-swizzled TMA destinations)
+    static size_t smem(int wreg) { return 1024 + (size_t)WARPS * wreg + 128 + CBUF + GBUF; }
 };
 
 struct FuArgs {
     XArgs xc;
     int S, U, N, C, T, WPS, NPC;
+    int stg, wreg, nkk, nsb, stage_bytes;   // ring stage pitch, per-warp region pitch; TC: K8 steps, DL boxes
     float rho, gamma, delta;
     // UL outputs (SOLVER 0, 1)
     float2* s_hat;        // [N][U]
@@ -88,13 +103,18 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     constexpr bool DL = Z::DL, MF = Z::MF;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw) + warp * NST;
-    unsigned char* wbase = smem_raw + 128 + (size_t)warp * Z::WREG;
+    // 1024-aligned base: [4 warp regions][mbarriers + CG queue (128 B)][Wp, Sv, Gp, Gs]
+    unsigned char* const base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    unsigned char* const cta = base + (size_t)Z::WARPS * a.wreg;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(cta) + warp * NST;
+    unsigned char* wbase = base + (size_t)warp * a.wreg;
+    unsigned char* const wloc = wbase + NST * a.stg;
     const int q = lane / L, l = lane % L;
-    float2* pl = reinterpret_cast<float2*>(wbase + NST * G::STG) + q * F::PLP;             // pivots / vectors
-    float* dline = reinterpret_cast<float*>(wbase + NST * G::STG + Z::PWL * 8) + q * UP;
-    float2* ybuf = reinterpret_cast<float2*>(wbase + NST * G::STG + Z::PWL * 8 + Z::DLN * 4) + q * fold_ybuf_pair<UP>();
-    float2* Wp = reinterpret_cast<float2*>(smem_raw + 128 + (size_t)Z::WARPS * Z::WREG);   // [4 warps][UP]
+    float2* pl = reinterpret_cast<float2*>(wloc) + q * F::PLP;                             // pivots / vectors
+    float* dline = reinterpret_cast<float*>(wloc + Z::PWL * 8) + q * UP;
+    float2* const uni = reinterpret_cast<float2*>(wloc + Z::PWL * 8 + Z::DLN * 4);
+    float2* ybuf = uni + q * fold_ybuf_pair<UP>();
+    float2* Wp = reinterpret_cast<float2*>(cta + 128);                                     // [4 warps][UP]
     float2* Sv = Wp + Z::WARPS * UP;                                                       // [4 subc.][UP]
     float2* Gp = Sv + Z::WARPS * UP;                                                       // CG: [4 warps][TRI]
     float2* Gs = Gp + (Z::SUMS ? Z::WARPS * TRI : 0);                                      // queue: [4][TRI]
@@ -109,7 +129,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     const int c = cb * PW + q;                         // this pair's cluster
     const int ngroups = (a.N + NPC - 1) / NPC;
     const int nitems = blockIdx.x < ngroups ? (ngroups - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const int nch = (a.S + SC - 1) / SC;
+    const int nch = Z::TC ? PW : (a.S + SC - 1) / SC;  // stages per pass: TC one per pair, else SC antennas
     const int per_item = DL ? 2 * nch : nch;           // DL: Gram pass + output pass
     const int nseq = nitems * per_item;
 
@@ -119,9 +139,17 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     auto issue = [&](int st) {
         const int ch = is_ch >= nch ? is_ch - nch : is_ch;
         const int n = (blockIdx.x + is_item * gridDim.x) * NPC + j;
-        unsigned char* dst = wbase + st * G::STG;
-        mbar_arrive_expect_tx(&bar[st], (uint32_t)G::BYTES);
-        if (DL) {
+        unsigned char* dst = wbase + st * a.stg;
+        mbar_arrive_expect_tx(&bar[st], (uint32_t)a.stage_bytes);
+        if (Z::TC) {
+            // one whole pair (cluster cb * PW + ch): UL H [S8][16] + y [S8]; DL nsb boxes [16][16]
+            if (DL) {
+                for (int sb = 0; sb < a.nsb; ++sb) tma_load4(dst + sb * 2048, &tmH, 16 * sb, 0, n, cb * PW + ch, &bar[st]);
+            } else {
+                tma_load4(dst, &tmH, 0, 0, n, cb * PW + ch, &bar[st]);
+                tma_load4(dst + a.nkk * 1024, &tmY, 0, 0, n, cb * PW + ch, &bar[st]);
+            }
+        } else if (DL) {
             tma_load4(dst, &tmH, ch * SC, 0, n, cb * PW, &bar[st]);
         } else {
             tma_load4(dst, &tmH, 0, ch * SC, n, cb * PW, &bar[st]);
@@ -140,7 +168,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     int sq = 0, st = 0, qn = 0;
     uint32_t phase = 0;
     static_assert(Z::WARPS * NST * 8 <= 96, "mbarriers overlap the CG queue indices");
-    int* qsub = reinterpret_cast<int*>(smem_raw + 96);     // CG queue: subcarrier of each slot
+    int* qsub = reinterpret_cast<int*>(cta + 96);          // CG queue: subcarrier of each slot
     auto next_stage = [&]() {
         __syncwarp();
         if (lane == 0 && sq + NST < nseq) {
@@ -154,12 +182,36 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     // DL output pass: x_c[s] = sum_u conj(H_us) r_u, re-streaming H_c through the ring (its second
     // pass, L2-resident); lane l takes antennas l, l+L, ... of each stage.  (Reading H_c directly
     // from L2 with LDG instead measured 30% slower for the whole kernel.)
+    // TC: the warp's PW pairs one after another, pair p's H^d re-streamed as one stage; lane s
+    // takes antennas s, s + 32 (128B-swizzled [16 users][16 antennas] boxes); r of pair p is the
+    // UP-line rl + p * rstride (ADMM-DL: the pair's pivot line; ZF-DL: the subcarrier's solution).
+    auto dl_output_tc = [&](const float2* rl, int rstride, int n) {
+        for (int p = 0; p < PW; ++p) {
+            mbar_wait(&bar[st], phase);
+            const unsigned char* hs = wbase + st * a.stg;
+            float2 r[UP];
+            read_vec<UP>(rl + p * rstride, r);
+            const int cl = cb * PW + p;
+            for (int s = lane; s < a.S; s += 32) {
+                const int sb = s >> 4, sl = s & 15;
+                f2x acc = 0ull;
+#pragma unroll
+                for (int u = 0; u < UP; ++u) {
+                    const float2 h = *reinterpret_cast<const float2*>(hs + sb * 2048 + u * 128 +
+                                                                     (((sl >> 1) ^ (u & 7)) << 4) + ((sl & 1) << 3));
+                    x2_cmac(acc, r[u], h.x, h.y);
+                }
+                if (n < a.N && cl < a.C) a.x[((size_t)cl * a.N + n) * a.S + s] = c_conj(upk2(acc));
+            }
+            next_stage();
+        }
+    };
     auto dl_output = [&](const float2 (&r)[UP], int n, bool valid) {
         using GD = FoldStage<UP, true, false>;
         float2* xo = a.x + ((size_t)c * a.N + n) * a.S;
         for (int ch = 0; ch < nch; ++ch) {
             mbar_wait(&bar[st], phase);
-            const float2* hq = reinterpret_cast<const float2*>(wbase + st * G::STG) + q * GD::NL * GD::HL;
+            const float2* hq = reinterpret_cast<const float2*>(wbase + st * a.stg) + q * GD::NL * GD::HL;
 #pragma unroll
             for (int sl = l; sl < SC; sl += L) {
                 // conj(x_s) = sum_u conj(r_u) H_us: r_u is the reused FFMA2 pair operand
@@ -187,12 +239,41 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
         f2x E[R];
 #pragma unroll
         for (int m = 0; m < R; ++m) E[m] = 0ull;
-        for (int ch = 0; ch < nch; ++ch) {
-            mbar_wait(&bar[st], phase);
-            const float2* stage = reinterpret_cast<const float2*>(wbase + st * G::STG);
-            if (DL) fold_gram_dl<UP>(A, stage, q, row);
-            else fold_gram_ul<UP, true>(A, E, stage, q, row);
-            next_stage();
+        if constexpr (Z::TC) {
+            // tensor-core Gram (+ H^H y), one pair per stage, handed to the folded slots 4 pairs at a time
+            const int g = lane >> 2, t4 = lane & 3;
+            float2* gtri = uni;
+            float2* mfl = uni + 4 * TRI;
+            for (int h = 0; h < 2; ++h) {
+                for (int p4 = 0; p4 < 4; ++p4) {
+                    mbar_wait(&bar[st], phase);
+                    float acc[5][4];
+                    tc_gram<DL, MF>(acc, wbase + st * a.stg, a.nkk, g, t4);
+                    tc_store<DL, MF>(acc, gtri + p4 * TRI, mfl + p4 * UP, g, t4);
+                    next_stage();
+                }
+                __syncwarp();
+                if ((q >> 2) == h) {
+                    const float2* gq = gtri + (q & 3) * TRI;
+#pragma unroll
+                    for (int m = 0; m < R; ++m) {
+                        const int rb = (row[m] * (row[m] + 1)) / 2;
+#pragma unroll
+                        for (int tt = 0; tt < (m + 1) * L; ++tt)
+                            A[F::off(m) + tt] = tt <= row[m] ? pk2(gq[rb + tt]) : 0ull;
+                        if (MF) E[m] = pk2(mfl[(q & 3) * UP + row[m]]);
+                    }
+                }
+                __syncwarp();
+            }
+        } else {
+            for (int ch = 0; ch < nch; ++ch) {
+                mbar_wait(&bar[st], phase);
+                const float2* stage = reinterpret_cast<const float2*>(wbase + st * a.stg);
+                if (DL) fold_gram_dl<UP>(A, stage, q, row);
+                else fold_gram_ul<UP, true>(A, E, stage, q, row);
+                next_stage();
+            }
         }
         float dg[R];
         fold_diag<UP>(A, row, a.delta, dg);
@@ -272,9 +353,13 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                 }
                 qn = 0;
                 __syncthreads();
-                float2 r[UP];
-                read_vec<UP>(Sv + j * UP, r);
-                dl_output(r, n, valid);
+                if constexpr (Z::TC) {
+                    dl_output_tc(Sv + j * UP, 0, n);
+                } else {
+                    float2 r[UP];
+                    read_vec<UP>(Sv + j * UP, r);
+                    dl_output(r, n, valid);
+                }
                 __syncthreads();                        // Sv / Gs reused by the next item
                 continue;
             } else {
@@ -478,9 +563,13 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
 #pragma unroll
             for (int m = 0; m < R; ++m) pl[row[m]] = rv[m];
             __syncwarp();
-            float2 r[UP];
-            read_vec<UP>(pl, r);
-            dl_output(r, n, valid);
+            if constexpr (Z::TC) {
+                dl_output_tc(pl - q * F::PLP, F::PLP, n);
+            } else {
+                float2 r[UP];
+                read_vec<UP>(pl, r);
+                dl_output(r, n, valid);
+            }
         }
     }
 }
@@ -488,29 +577,53 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
 static int g_sms_fz = 0;
 
 template <int UP, int SOLVER>
+constexpr int NST_of() { return FZ<UP, SOLVER>::NST; }
+
+template <int UP, int SOLVER>
 static bool launch_fz_t(const LaunchCtx& L, const float2* H, const float2* y, FuArgs a) {
     using Z = FZ<UP, SOLVER>;
     using F = Fold<UP>;
     CUtensorMap tmH{}, tmY{};
     // H: UL [C][N][S][U] -> dims (U, S, N, C); DL [C][N][U][S] -> dims (S, U, N, C); y [C][N][1][S]
-    if (!Z::DL) {
-        if (!make_map4(&tmH, H, a.U, a.S, a.N, a.C, UP + 2, F::SC, 1, F::PW)) return false;
-        if (!make_map4(&tmY, y, a.S, 1, a.N, a.C, F::SC, 1, 1, F::PW)) return false;
+    if constexpr (Z::TC) {
+        const int S8 = (a.S + 7) / 8 * 8;
+        a.nsb = (a.S + 15) / 16;
+        if (!Z::DL) {
+            if (!make_map4(&tmH, H, a.U, a.S, a.N, a.C, 16, S8, 1, 1, true)) return false;
+            if (!make_map4(&tmY, y, a.S, 1, a.N, a.C, S8, 1, 1, 1)) return false;
+            a.nkk = S8 / 8;
+            a.stage_bytes = S8 * 128 + S8 * 8;
+        } else {
+            if (!make_map4(&tmH, H, a.S, a.U, a.N, a.C, 16, 16, 1, 1, true)) return false;
+            a.nkk = 2 * a.nsb;
+            a.stage_bytes = a.nsb * 2048;
+        }
+        a.stg = (a.stage_bytes + 1023) / 1024 * 1024;
+        a.wreg = (NST_of<UP, SOLVER>() * a.stg + Z::LOC + 1023) / 1024 * 1024;
     } else {
-        if (!make_map4(&tmH, H, a.S, a.U, a.N, a.C, F::SC, UP + 1, 1, F::PW)) return false;
+        if (!Z::DL) {
+            if (!make_map4(&tmH, H, a.U, a.S, a.N, a.C, UP + 2, F::SC, 1, F::PW)) return false;
+            if (!make_map4(&tmY, y, a.S, 1, a.N, a.C, F::SC, 1, 1, F::PW)) return false;
+        } else {
+            if (!make_map4(&tmH, H, a.S, a.U, a.N, a.C, F::SC, UP + 1, 1, F::PW)) return false;
+        }
+        a.stg = Z::G::STG;
+        a.stage_bytes = Z::G::BYTES;
+        a.wreg = Z::WREG;
     }
+    const size_t SMEM = Z::smem(a.wreg);
     if (!g_sms_fz) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_sms_fz, cudaDevAttrMultiProcessorCount, dev);
     }
     auto k = k_fused<UP, SOLVER>;
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z::SMEM) != cudaSuccess) {
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, Z::WARPS * 32, Z::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, Z::WARPS * 32, SMEM);
     const int ngroups = (a.N + a.NPC - 1) / a.NPC;
     // Grid per solver (bit SOLVER of the mask set: persistent, one wave of resident CTAs striding over the
     // subcarrier groups; clear: one CTA per group, the hardware scheduler balancing the tail).  Measured
@@ -527,7 +640,7 @@ static bool launch_fz_t(const LaunchCtx& L, const float2* H, const float2* y, Fu
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((unsigned)std::min(ngroups, g_sms_fz * per_sm));
         cfg.blockDim = dim3(Z::WARPS * 32);
-        cfg.dynamicSmemBytes = Z::SMEM;
+        cfg.dynamicSmemBytes = SMEM;
         cfg.stream = L.stream;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeCooperative;
@@ -542,7 +655,7 @@ static bool launch_fz_t(const LaunchCtx& L, const float2* H, const float2* y, Fu
         return true;
     }
     const int grid = (persist >> SOLVER) & 1 ? std::min(ngroups, g_sms_fz * std::max(per_sm, 1)) : ngroups;
-    k<<<grid, Z::WARPS * 32, Z::SMEM, L.stream>>>(tmH, tmY, a);
+    k<<<grid, Z::WARPS * 32, SMEM, L.stream>>>(tmH, tmY, a);
     L.count(1);
     return true;
 }

@@ -48,8 +48,10 @@ struct CgArgs {
 // the tensor: out-of-bounds elements are zero-filled).  false if unsupported.
 bool make_map3(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1,
                uint32_t b2);
+// swz128: CU_TENSOR_MAP_SWIZZLE_128B (16-B chunk c of 128-B row r lands at chunk c ^ (r & 7); the
+// shared-memory destination must be 1024-B aligned), box inner extent <= 16 elements.
 bool make_map4(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3, uint32_t b0,
-               uint32_t b1, uint32_t b2, uint32_t b3);
+               uint32_t b1, uint32_t b2, uint32_t b3, bool swz128 = false);
 // Device-side consensus over ranks (NEXT-1, DBP_OPT_DEVICE_CONSENSUS): every rank owns one
 // symmetric buffer, mapped into all ranks (CUDA IPC over NVLink):
 //   part [2 round parity][8 ranks][cap subcarriers][16 users] uint4 = {re, id, im, id}.

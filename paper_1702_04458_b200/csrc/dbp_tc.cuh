@@ -1,0 +1,152 @@
+// dbp_tc.cuh -- the per-pair Gram (+ matched filter) on the tensor cores, for UP = 16
+// (G_c = H_c^H H_c (P295, P391), B_c = H_c H_c^H (P503),
+// H_c^H y_c (P296)).
+//
+// One warp computes one pair with mma.sync m16n8k8 TF32 (the warp-level tensor path; 242
+// TFLOP/s measured on B200, scripts/micro/tc_gram.cu) in "3xTF32": every fp32 operand v is
+// split exactly into hi = v with the low 13 mantissa bits cleared (a TF32 value) and
+// lo = v - hi (exact in fp32; the tensor core keeps its top 19 bits), and
+// hi*hi + hi*lo + lo*hi is accumulated in fp32 -- the dropped lo*lo term and lo's
+// truncation are ~2^-22 relative, so the Gram matches an fp32 FMA Gram (measured 6e-7
+// relative to fp64, vs 1.5e-4 for plain TF32).  Scale-free (TF32 keeps the fp32 exponent).
+//
+// Real form: with A[u][k] = (Re or Im) of h_{k,u} over the K index k = antenna (a K8 step
+// is 8 antennas, taken once for the real and once for the imaginary parts),
+//   Re G = A_re^T A_re + A_im^T A_im,   Im G = A_re^T A_im - A_im^T A_re  (UL: G = H^H H),
+// so M = 16 users, N = 32 ([Re G | Im G], four n8 tiles), and the B operand of the Re tiles
+// is A^T itself: every fragment is built from the same 4 complex values per lane and K8 step,
+//   v[e1][e2] = h(user g + 8 e1, antenna 8 kk + 2 t + e2),   g = lane / 4, t = lane % 4
+// (K index t <-> antenna 2t, t + 4 <-> 2t + 1: the 8 lanes of a quarter-warp then read 8
+// distinct 16-B chunks of the 128B-swizzled TMA stage, see below).  A fifth n8 tile carries
+// the matched filter: columns [y_re; y_im] and [y_im; -y_re] give Re and Im of H^H y.
+//
+// Stage layouts in shared memory (TMA, CU_TENSOR_MAP_SWIZZLE_128B, 1024-B aligned):
+//   UL: H_c [S8 antennas][16 users] (128-B rows: chunk c of row s at c ^ (s & 7)), then
+//       y_c [S8] unswizzled;
+//   DL: H^d_c as ceil(S/16) boxes of [16 users][16 antennas] (2 KB each; chunk c of row u
+//       at c ^ (u & 7)).  B = H H^H has Im of the opposite sign (conjugate of the UL form).
+#pragma once
+
+#include "dbp_device.cuh"
+
+namespace dbp {
+
+__device__ __forceinline__ void mma_tf32(float (&d)[4], unsigned a0, unsigned a1, unsigned a2, unsigned a3,
+                                         unsigned b0, unsigned b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// Exact split v = hi + lo, hi a TF32 value (low 13 mantissa bits cleared).
+__device__ __forceinline__ void tc_split(float v, unsigned& hi, unsigned& lo) {
+    hi = __float_as_uint(v) & 0xffffe000u;
+    lo = __float_as_uint(v - __uint_as_float(hi));
+}
+
+constexpr unsigned TC_NEG = 0x80000000u;
+
+// Gram (+ matched filter) of one pair from its TMA stage; acc[0..1] Re tiles (columns
+// 0-7, 8-15), acc[2..3] Im tiles, acc[4] matched filter (columns 0 = Re, 1 = Im).
+// nkk = number of K8 steps (ceil(S / 8)); antennas >= S are zero-filled by the TMA.
+template <bool DL, bool MF>
+__device__ __forceinline__ void tc_gram(float (&acc)[5][4], const unsigned char* stage, int nkk, int g, int t) {
+#pragma unroll
+    for (int i = 0; i < 5; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[i][e] = 0.f;
+    const float2* yv = reinterpret_cast<const float2*>(stage + nkk * 8 * 128);   // UL: y after H
+#pragma unroll 2
+    for (int kk = 0; kk < nkk; ++kk) {
+        float2 v[2][2];
+        if (DL) {
+            // box kk/2, row u, the 16-B chunk holding antennas 8(kk&1) + 2t, +1
+#pragma unroll
+            for (int e1 = 0; e1 < 2; ++e1) {
+                const int u = g + 8 * e1;
+                const float4 q = *reinterpret_cast<const float4*>(stage + (kk >> 1) * 2048 + u * 128 +
+                                                                  (((4 * (kk & 1) + t) ^ g) << 4));
+                v[e1][0] = make_float2(q.x, q.y);
+                v[e1][1] = make_float2(q.z, q.w);
+            }
+        } else {
+#pragma unroll
+            for (int e2 = 0; e2 < 2; ++e2) {
+                const int s = 8 * kk + 2 * t + e2;
+#pragma unroll
+                for (int e1 = 0; e1 < 2; ++e1) {
+                    const int u = g + 8 * e1;
+                    v[e1][e2] = *reinterpret_cast<const float2*>(stage + s * 128 + (((u >> 1) ^ (s & 7)) << 4) +
+                                                                 ((u & 1) << 3));
+                }
+            }
+        }
+        // fragment order a0 (user g, k t), a1 (g + 8, t), a2 (g, t + 4), a3 (g + 8, t + 4)
+        unsigned rh[4], rl[4], ih[4], il[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float2 x = v[e & 1][e >> 1];
+            tc_split(x.x, rh[e], rl[e]);
+            tc_split(x.y, ih[e], il[e]);
+        }
+        unsigned yrh[2], yrl[2], yih[2], yil[2];
+        if (MF) {
+            // B[k][col g] of the matched-filter tile: col 0 = (y_re | y_im), col 1 = (y_im | -y_re)
+            // over the (re | im) K steps; b0 <- antenna 2t, b1 <- 2t + 1; columns >= 2 are zero
+            const float4 yy = *reinterpret_cast<const float4*>(yv + 8 * kk + 2 * t);
+            const float re0 = g == 0 ? yy.x : (g == 1 ? yy.y : 0.f), re1 = g == 0 ? yy.z : (g == 1 ? yy.w : 0.f);
+            const float im0 = g == 0 ? yy.y : (g == 1 ? -yy.x : 0.f), im1 = g == 0 ? yy.w : (g == 1 ? -yy.z : 0.f);
+            tc_split(re0, yrh[0], yrl[0]);
+            tc_split(re1, yrh[1], yrl[1]);
+            tc_split(im0, yih[0], yil[0]);
+            tc_split(im1, yih[1], yil[1]);
+        }
+        // three passes: (A hi, B hi), (A hi, B lo), (A lo, B hi)
+#pragma unroll
+        for (int pass = 0; pass < 3; ++pass) {
+            const unsigned* Ar = pass == 2 ? rl : rh;
+            const unsigned* Ai = pass == 2 ? il : ih;
+            const unsigned* Br = pass == 1 ? rl : rh;
+            const unsigned* Bi = pass == 1 ? il : ih;
+            mma_tf32(acc[0], Ar[0], Ar[1], Ar[2], Ar[3], Br[0], Br[2]);
+            mma_tf32(acc[0], Ai[0], Ai[1], Ai[2], Ai[3], Bi[0], Bi[2]);
+            mma_tf32(acc[1], Ar[0], Ar[1], Ar[2], Ar[3], Br[1], Br[3]);
+            mma_tf32(acc[1], Ai[0], Ai[1], Ai[2], Ai[3], Bi[1], Bi[3]);
+            mma_tf32(acc[2], Ar[0], Ar[1], Ar[2], Ar[3], Bi[0], Bi[2]);
+            mma_tf32(acc[2], Ai[0], Ai[1], Ai[2], Ai[3], Br[0] ^ TC_NEG, Br[2] ^ TC_NEG);
+            mma_tf32(acc[3], Ar[0], Ar[1], Ar[2], Ar[3], Bi[1], Bi[3]);
+            mma_tf32(acc[3], Ai[0], Ai[1], Ai[2], Ai[3], Br[1] ^ TC_NEG, Br[3] ^ TC_NEG);
+            if (MF) {
+                const unsigned* Yr = pass == 1 ? yrl : yrh;
+                const unsigned* Yi = pass == 1 ? yil : yih;
+                mma_tf32(acc[4], Ar[0], Ar[1], Ar[2], Ar[3], Yr[0], Yr[1]);
+                mma_tf32(acc[4], Ai[0], Ai[1], Ai[2], Ai[3], Yi[0], Yi[1]);
+            }
+        }
+    }
+}
+
+// Lower triangle of the pair's Gram (DL: conjugated to B = H H^H) into a packed [TRI] line,
+// and (MF) H^H y into a [16] line.  D fragment: c0 (row g, col 2t), c1 (g, 2t+1), c2 (g+8, 2t),
+// c3 (g+8, 2t+1) of each n8 tile; columns 8h + 2t + cc of tile h (Re) and 2 + h (Im).
+template <bool DL, bool MF>
+__device__ __forceinline__ void tc_store(const float (&acc)[5][4], float2* gtri, float2* mfl, int g, int t) {
+    const float sg = DL ? -1.f : 1.f;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int e1 = 0; e1 < 2; ++e1)
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+                const int r = g + 8 * e1, col = 8 * h + 2 * t + cc;
+                if (col <= r) gtri[pidx(r, col)] = make_float2(acc[h][2 * e1 + cc], sg * acc[2 + h][2 * e1 + cc]);
+            }
+    if (MF && t == 0) {
+        mfl[g] = make_float2(acc[4][0], acc[4][1]);
+        mfl[g + 8] = make_float2(acc[4][2], acc[4][3]);
+    }
+}
+
+}  // namespace dbp

@@ -41,18 +41,20 @@ bool make_map3(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint6
 }
 
 bool make_map4(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3, uint32_t b0,
-               uint32_t b1, uint32_t b2, uint32_t b3) {
+               uint32_t b1, uint32_t b2, uint32_t b3, bool swz128) {
     auto fn = encode_fn();
     if (!fn) return false;
     if ((reinterpret_cast<uintptr_t>(base) & 15) || ((d0 * 8) & 15)) return false;
     if (d2 > (1ull << 32) || d3 > (1ull << 32) || b0 > 256 || b1 > 256 || b2 > 256 || b3 > 256 || ((b0 * 8) & 15))
         return false;
+    if (swz128 && b0 * 8 > 128) return false;        // 128B swizzle: the box's inner extent is <= 128 bytes
     cuuint64_t dims[4] = {d0, d1, d2, d3};
     cuuint64_t strides[3] = {d0 * 8, d0 * d1 * 8, d0 * d1 * d2 * 8};
     cuuint32_t box[4] = {b0, b1, b2, b3};
     cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), dims, strides, box, es,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
