@@ -4,38 +4,52 @@
 Workload: one TDD slot on the B = 1024-antenna array of
 BASELINE configs C and D -- C = 32 clusters of S = 32 antennas, U = 16 users,
 N = 1200 subcarriers, N_sym = 1, T = 5 iterations, rho = 1.  A step runs the
-whole hot path (every SURVEY 8(a) row) on one synthetic frame:
-  * uplink 64-QAM frame (SNR 25 dB) detected by ADMM (Alg. 1) and by
-    decentralized CG (Alg. 2);
-  * downlink 16-QAM frame precoded by ADMM beamforming (Alg. 3).
+whole hot path (every SURVEY 8(a) row) on three synthetic frames:
+  * a 64-QAM uplink frame (SNR 25 dB) detected by ADMM (Alg. 1);
+  * a second, independent 64-QAM uplink frame (its own seed) detected by
+    decentralized CG (Alg. 2) -- no two passes of a step share a channel, so
+    no pass can be served from another's L2 lines;
+  * a 16-QAM downlink frame precoded by ADMM beamforming (Alg. 3).
 value = (bits detected by ADMM + bits detected by CG + bits precoded) / step
-time, bits = U * N * N_sym * log2|O| per solver (P753, P800).  Clusters are
+time, bits = U * N * N_sym * log2|O| per frame (P753, P800).  Clusters are
 split over the ranks (strong scaling) with one NCCL allreduce per consensus
 round -- the only communication (P744-746).
+
+Launch: `--gpus N` with N > 1 and no torchrun environment re-executes itself
+under `torch.distributed.run` (127.0.0.1) with N ranks, after checking that N
+GPUs are visible (it fails loudly otherwise); under torchrun WORLD_SIZE must
+equal --gpus.  At world > 1 the run also reports (i) the same step with the
+device-side consensus (DBP_OPT_DEVICE_CONSENSUS, NEXT-1) cross-checked against
+the NCCL path, (ii) a world-1 solve of the whole frame on every rank that both
+must match to rel-L2 <= 1e-5 (SURVEY 8(c) "across GPU counts"), (iii) the
+subcarrier-sharded control (every rank all clusters of N/G subcarriers, no
+communication) and (iv) per-rank exposed-allreduce time and the
+NCCL communicator size.
 
 Timing: W untimed warm-up steps; then exactly K steps, each bracketed by CUDA
 events on the launch stream, with an untimed 256 MiB L2-flush write between
 steps; barrier + synchronize on both sides; max over ranks.  At world = 1
-the step runs the uplink pair (ADMM-UL then CG-UL, one stream) concurrently
-with ADMM-DL (second stream, forked from and joined to the launch stream
-inside the event bracket); a separate sequential region (all three back to
-back on one stream) gives the per-solver times, per-iteration latencies and
-the kernel-timer shares the roofline uses.  At world > 1 the step is the
-sequential schedule (one communicator, one collective order).  The end-to-end
-figure (e2e) calls the same C ABI with pinned HOST buffers, so every step
-includes the host->device copy of its inputs and the device->host copy of
-its outputs.  `--impl reference` times the fp64 oracle (oracle/) on the
-host cores instead (rank 0 only).
+the step runs ADMM-UL then ADMM-DL on one stream concurrently with CG-UL on a
+second (forked from and joined to the launch stream inside the event
+bracket); a separate sequential region (all three back to back) gives the
+per-solver times, per-iteration latencies and the kernel-timer shares the
+roofline uses.  At world > 1 the step is sequential (one communicator, one
+collective order).  `e2e` calls the same C ABI with pinned HOST buffers, so
+every step includes the host->device copy of its inputs and the device->host
+copy of its outputs.  `--impl reference` times the fp64 oracle (oracle/) on
+the host cores instead (rank 0 only).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
 import time
+from concurrent.futures import ProcessPoolExecutor
 
 import numpy as np
 
@@ -46,17 +60,20 @@ from paper_1702_04458_b200 import synth  # noqa: E402
 
 METRIC = "detected Gbit/s per frame (and per-iteration latency) at 1/2/4/8 B200"
 UL = synth.CONFIGS["C"]
+CG = UL.scaled(name="C-cg", algo="cg_ul", seed=UL.seed + 1000)     # an independent uplink frame
 DL = synth.CONFIGS["D"]
-BITS = {"admm_ul": UL.bits_per_frame, "cg_ul": UL.bits_per_frame, "admm_dl": DL.bits_per_frame}
+BITS = {"admm_ul": UL.bits_per_frame, "cg_ul": CG.bits_per_frame, "admm_dl": DL.bits_per_frame}
 BITS_PER_STEP = sum(BITS.values())
+ORDER = ["admm_ul", "admm_dl", "cg_ul"]
 
 
 def workload_config(world: int) -> dict:
     return {"workload": "TDD slot on configs C+D: B=1024 (C=32 x S=32), U=16, N=1200, N_sym=1, T=5; "
-                        "ADMM-UL + CG-UL on a 64-QAM uplink frame (SNR 25 dB), ADMM-DL on a 16-QAM "
-                        "downlink frame",
+                        "ADMM-UL on a 64-QAM uplink frame, CG-UL on a second independent 64-QAM uplink "
+                        "frame (SNR 25 dB), ADMM-DL on a 16-QAM downlink frame",
             "B": UL.B, "C": UL.C, "S": UL.S, "U": UL.U, "N": UL.N, "N_sym": UL.N_sym, "T": UL.T,
             "rho": UL.rho, "mod_ul": UL.mod, "mod_dl": DL.mod, "snr_db": UL.snr_db,
+            "seeds": {"admm_ul": UL.seed, "cg_ul": CG.seed, "admm_dl": DL.seed},
             "bits_per_step": BITS_PER_STEP, "parallelism": f"clusters split over {world} GPU(s), "
                                                              f"{UL.C // world} per GPU",
             "l2": "L2 flushed between timed steps (untimed 256 MiB write + read-back, so no dirty lines "
@@ -102,34 +119,59 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
 
 
-# ------------------------------------------------------------------ oracle legs
-_SAMPLES = {}
-
-
-def _oracle_sample(n_sub: int):
-    """Oracle on subcarriers [0, n_sub) of the same workload; returns (seconds, bits).
-    The synthetic inputs are generated once per size (not timed)."""
-    import oracle
-    ul, dl = UL.scaled(N=n_sub), DL.scaled(N=n_sub)
-    if n_sub not in _SAMPLES:
-        H, y, _ = synth.uplink_frame(UL, n0=0, n1=n_sub)
-        Hd, s = synth.downlink_frame(DL, n0=0, n1=n_sub)
-        _SAMPLES[n_sub] = (H, y, Hd, s)
-    H, y, Hd, s = _SAMPLES[n_sub]
-    t0 = time.perf_counter()
-    oracle.detect_admm(H, y, rho=ul.rho, N0=ul.N0, mod=ul.mod, T=ul.T)
-    oracle.beamform_admm(Hd, s, rho=dl.rho, T=dl.T)
-    oracle.detect_cg(H, y, rho=ul.N0, mod=ul.mod, T=ul.T)
-    dt = time.perf_counter() - t0
-    bits = 2 * ul.bits_per_frame + dl.bits_per_frame
-    return dt, bits
-
-
+# ------------------------------------------------------------------ synthetic frames
 def host_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
     except AttributeError:
         return os.cpu_count() or 1
+
+
+def _gen(args):
+    kind, cfg, c0, c1, n0, n1 = args
+    if kind == "ul":
+        H, y, _ = synth.uplink_frame(cfg, c0, c1, n0, n1)
+        return H, y
+    return synth.downlink_frame(cfg, c0, c1, n0, n1)
+
+
+def gen_frame(kind: str, cfg, c0: int, c1: int, n0: int = 0, n1: int | None = None, workers: int = 1):
+    """synth frame of clusters [c0, c1), subcarriers [n0, n1), generated per cluster in parallel
+    (the values do not depend on the split: counter-based Philox)."""
+    n1 = cfg.N if n1 is None else n1
+    jobs = [(kind, cfg, c, c + 1, n0, n1) for c in range(c0, c1)]
+    if workers <= 1 or len(jobs) == 1:
+        parts = [_gen(j) for j in jobs]
+    else:
+        with ProcessPoolExecutor(max_workers=min(workers, len(jobs))) as ex:
+            parts = list(ex.map(_gen, jobs))
+    if kind == "ul":
+        return np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts])
+    return np.concatenate([p[0] for p in parts]), parts[0][1]
+
+
+# ------------------------------------------------------------------ oracle legs
+_SAMPLES = {}
+
+
+def _oracle_sample(n_sub: int):
+    """Oracle on subcarriers [0, n_sub) of the same three frames; returns (seconds, bits).
+    The synthetic inputs are generated once per size (not timed)."""
+    import oracle
+    ul, cg, dl = UL.scaled(N=n_sub), CG.scaled(N=n_sub), DL.scaled(N=n_sub)
+    if n_sub not in _SAMPLES:
+        H, y, _ = synth.uplink_frame(UL, n0=0, n1=n_sub)
+        Hc, yc, _ = synth.uplink_frame(CG, n0=0, n1=n_sub)
+        Hd, s = synth.downlink_frame(DL, n0=0, n1=n_sub)
+        _SAMPLES[n_sub] = (H, y, Hc, yc, Hd, s)
+    H, y, Hc, yc, Hd, s = _SAMPLES[n_sub]
+    t0 = time.perf_counter()
+    oracle.detect_admm(H, y, rho=ul.rho, N0=ul.N0, mod=ul.mod, T=ul.T)
+    oracle.beamform_admm(Hd, s, rho=dl.rho, T=dl.T)
+    oracle.detect_cg(Hc, yc, rho=cg.N0, mod=cg.mod, T=cg.T)
+    dt = time.perf_counter() - t0
+    bits = ul.bits_per_frame + cg.bits_per_frame + dl.bits_per_frame
+    return dt, bits
 
 
 def cpu_baseline(budget_s: float = 10.0, n_sub: int = 240) -> dict:
@@ -224,6 +266,87 @@ def load_traffic() -> dict:
     return {}
 
 
+# ------------------------------------------------------------------ launcher / rank plumbing
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch(args) -> int | None:
+    """--gpus N > 1 outside torchrun: re-exec under torch.distributed.run with N ranks (None: no
+    relaunch needed).  Refuses (exit 2) if fewer than N GPUs are visible -- a multi-GPU number is
+    never silently measured on fewer GPUs."""
+    if "RANK" in os.environ or args.gpus <= 1:
+        return None
+    if not args.plumbing_check:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible; "
+                             f"refusing to report a {args.gpus}-GPU number\n")
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def rank_env(args):
+    if "RANK" not in os.environ:
+        return 0, 1, 0
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}; launch one rank per GPU")
+    return rank, world, local
+
+
+def max_over_ranks(vals, world, dist, device=None):
+    if world == 1:
+        return np.asarray(vals, dtype=np.float64)
+    import torch
+    t = torch.tensor(np.asarray(vals, dtype=np.float64), device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.cpu().numpy()
+
+
+def gather_rows(row, world, dist, device=None):
+    """all ranks' float rows (same length) -> [world][len] on every rank."""
+    if world == 1:
+        return [list(row)]
+    import torch
+    t = torch.tensor(np.asarray(row, dtype=np.float64), device=device)
+    out = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    return [o.cpu().numpy().tolist() for o in out]
+
+
+def plumbing_check(args, rank: int, world: int):
+    """CPU stand-in for the multi-rank GPU run (gloo): the same launcher, rank/world checks,
+    unique-id broadcast, cluster partition and max-over-ranks / gather reductions, with a
+    rank-dependent fake step time -- so the N > 1 plumbing is testable without GPUs."""
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+    uid = None
+    if world > 1:
+        obj = [os.urandom(128) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    c0, c1 = synth.cluster_range(UL.C, rank, world)
+    fake_ms = 1.0 + rank
+    mx = float(max_over_ranks([fake_ms], world, dist)[0])
+    rows = gather_rows([rank, c0, c1, len(uid) if uid else 0], world, dist)
+    if rank == 0:
+        print(json.dumps({"plumbing": True, "n_gpus": world, "max_ms": mx,
+                          "ranks": [{"rank": int(r[0]), "clusters": [int(r[1]), int(r[2])], "uid_bytes": int(r[3])}
+                                    for r in rows]}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 # ------------------------------------------------------------------ main arm
 def main():
     ap = argparse.ArgumentParser()
@@ -234,10 +357,11 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-table2", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config entries (world = 1)")
     ap.add_argument("--sequential", action="store_true",
                     help="world = 1: time the step with the three solvers back to back on one stream")
-    ap.add_argument("--device-consensus", action="store_true",
-                    help="world > 1: consensus inside the fused kernels over NVLink (DBP_OPT_DEVICE_CONSENSUS)")
+    ap.add_argument("--no-device-consensus", action="store_true",
+                    help="world > 1: skip the device-side consensus leg (DBP_OPT_DEVICE_CONSENSUS)")
     ap.add_argument("--streams", type=int, default=2, choices=[2, 3],
                     help="world-1 concurrent schedule: 2 = ADMM-UL then ADMM-DL on one stream, CG-UL on another; "
                          "3 = every solver on its own stream")
@@ -245,13 +369,16 @@ def main():
                     help="world-1 concurrent schedule as solver lists per stream, e.g. "
                          "'admm_ul,cg_ul|admm_dl' (overrides --streams)")
     ap.add_argument("--ref-subcarriers", type=int, default=60)
+    ap.add_argument("--plumbing-check", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if "RANK" not in os.environ:
-        world = 1
+    rc = relaunch(args)
+    if rc is not None:
+        sys.exit(rc)
+    rank, world, local = rank_env(args)
+    if args.plumbing_check:
+        plumbing_check(args, rank, world)
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -269,15 +396,27 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     ctx = dbp.Context(device=local, rank=rank, world=world, unique_id=uid)
-    if args.device_consensus:
-        ctx.set_option(dbp.OPT_DEVICE_CONSENSUS, 1)
+    comm = ctx.comm_info()
+    if comm["nranks"] != world or comm["rank"] != rank:
+        raise SystemExit(f"bench.py: NCCL communicator {comm} does not match rank {rank} / world {world}")
 
+    workers = max(1, host_cores() // max(world, 1))
     c0, c1 = synth.cluster_range(UL.C, rank, world)
-    H, y, _ = synth.uplink_frame(UL, c0, c1)
-    Hd, s = synth.downlink_frame(DL, c0, c1)
     C_loc = c1 - c0
-    Hg, yg = torch.from_numpy(H).to(dev), torch.from_numpy(y).to(dev)
-    Hdg, sg = torch.from_numpy(Hd).to(dev), torch.from_numpy(s).to(dev)
+    if world == 1:
+        H, y = gen_frame("ul", UL, 0, UL.C, workers=workers)
+        Hc, yc = gen_frame("ul", CG, 0, CG.C, workers=workers)
+        Hd, s = gen_frame("dl", DL, 0, DL.C, workers=workers)
+        full = (H, y, Hc, yc, Hd, s)
+    else:
+        # every rank generates the whole frames: its cluster block runs the decentralized path, the
+        # whole frame the world-1 reference solve and the subcarrier-sharded control
+        full = (*gen_frame("ul", UL, 0, UL.C, workers=workers), *gen_frame("ul", CG, 0, CG.C, workers=workers),
+                *gen_frame("dl", DL, 0, DL.C, workers=workers))
+        H, y, Hc, yc, Hd, s = (full[0][c0:c1], full[1][c0:c1], full[2][c0:c1], full[3][c0:c1],
+                               full[4][c0:c1], full[5])
+    to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    Hg, yg, Hcg, ycg, Hdg, sg = to(H), to(y), to(Hc), to(yc), to(Hd), to(s)
     s_hat = torch.empty((UL.N, UL.N_sym, UL.U), dtype=torch.complex64, device=dev)
     hard = torch.empty((UL.N, UL.N_sym, UL.U), dtype=torch.uint8, device=dev)
     x_hat = torch.empty_like(s_hat)
@@ -295,25 +434,33 @@ def main():
         flush.fill_(k & 0xFF)
         torch.sum(flush.view(torch.int64), dim=0, out=flush_sink)
 
-    def solver(name, T, st=None):
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def mx(v):
+        return max_over_ranks(v, world, dist, dev)
+
+    def solver(name, T, st=None, c=None):
+        c = ctx if c is None else c
         sp = None if st is None else st.cuda_stream
         if name == "admm_ul":
-            dbp.detect_admm(ctx, Hg, yg, rho=UL.rho, N0=UL.N0, mod=UL.mod, T=T, s_hat=s_hat, hard=hard,
+            dbp.detect_admm(c, Hg, yg, rho=UL.rho, N0=UL.N0, mod=UL.mod, T=T, s_hat=s_hat, hard=hard,
                             ws=ws["admm_ul"], stream=sp)
         elif name == "admm_dl":
-            dbp.beamform_admm(ctx, Hdg, sg, rho=DL.rho, T=T, x=xbf, ws=ws["admm_dl"], stream=sp)
+            dbp.beamform_admm(c, Hdg, sg, rho=DL.rho, T=T, x=xbf, ws=ws["admm_dl"], stream=sp)
         else:
-            dbp.detect_cg(ctx, Hg, yg, rho=UL.N0, mod=UL.mod, T=T, x_hat=x_hat, hard=hard2, ws=ws["cg_ul"],
+            dbp.detect_cg(c, Hcg, ycg, rho=CG.N0, mod=CG.mod, T=T, x_hat=x_hat, hard=hard2, ws=ws["cg_ul"],
                           stream=sp)
 
     # Step schedule.  world == 1: ADMM-UL then ADMM-DL on one stream, CG-UL on a second, so each
-    # kernel's CTAs fill the other's wave tail (the fastest of the six two-lane orders measured,
-    # DESIGN.md section 6).  world > 1: sequential on one stream (every solver issues one NCCL allreduce per round
-    # on the same communicator; two streams could order them differently across ranks).
+    # kernel's CTAs fill the other's wave tail.  world > 1: sequential on one
+    # stream (every solver issues NCCL allreduces on one communicator; two streams could order them
+    # differently across ranks).
     concurrent = world == 1 and not args.sequential
     plan = args.plan or ("admm_ul|admm_dl|cg_ul" if args.streams == 3 else "admm_ul,admm_dl|cg_ul")
     plan = [lane.split(",") for lane in plan.split("|")]
-    assert sorted(sum(plan, [])) == ["admm_dl", "admm_ul", "cg_ul"], "--plan must name each solver once"
+    assert sorted(sum(plan, [])) == sorted(ORDER), "--plan must name each solver once"
     side = tuple(torch.cuda.Stream(dev) for _ in plan) if concurrent else None
     join = (torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event())
 
@@ -340,13 +487,8 @@ def main():
         barrier()
         return sum(e0.elapsed_time(e1) for e0, e1 in ev)   # ms over K steps
 
-    order = ["admm_ul", "admm_dl", "cg_ul"]   # BF between the two uplink passes: no L2 reuse of H
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    def timed_region(K, T, names):
+    def timed_region(K, T, names, fn=None):
+        fn = fn or solver
         ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)] for _ in range(K)]
         barrier()
         torch.cuda.synchronize()
@@ -354,7 +496,7 @@ def main():
             flush_l2(k)
             ev[k][0].record(stream)
             for i, nm in enumerate(names):
-                solver(nm, T)
+                fn(nm, T)
                 ev[k][i + 1].record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -365,7 +507,7 @@ def main():
         return per  # ms summed over K steps, per solver
 
     for _ in range(args.warmup):
-        for nm in order:
+        for nm in ORDER:
             solver(nm, UL.T)
         if concurrent:
             join[3].record(stream)
@@ -378,10 +520,12 @@ def main():
     ctx.set_option(dbp.OPT_KERNEL_TIMING, 1)
     ctx.kernel_times(reset=True)
     st0 = ctx.stats()
-    per = timed_region(args.steps, UL.T, order)        # sequential: per-solver times + kernel timer
+    per = timed_region(args.steps, UL.T, ORDER)        # sequential: per-solver times + kernel timer
     st1 = ctx.stats()
     ktimes = ctx.kernel_times(reset=True)
     ctx.set_option(dbp.OPT_KERNEL_TIMING, 0)
+    kern_ms_rank = sum(v[1] for v in ktimes.values()) / args.steps       # this rank's kernel time per step
+    step_ms_rank = float(np.sum(per)) / args.steps
     conc_ms = None
     if concurrent:                                     # the step as scheduled (headline)
         st0 = ctx.stats()
@@ -392,87 +536,183 @@ def main():
 
     # per-iteration latency: (L(T) - L(1)) / (T - 1), per solver
     K1 = min(args.steps, 200)
-    per1 = timed_region(K1, 1, order)
-
-
-    def mx(v):
-        if world == 1:
-            return np.asarray(v, dtype=np.float64)
-        t = torch.tensor(np.asarray(v, dtype=np.float64), device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return t.cpu().numpy()
-
+    per1 = timed_region(K1, 1, ORDER)
     per = mx(per)
     per1 = mx(per1)
 
-    # centralized baselines (Table I rows MMSE-UL / ZF-DL, the paper's comparison P789-792,
-    # P810): same frames, timed alone; context only, not part of the step
-    xb = torch.empty_like(s_hat)
-    hb = torch.empty_like(hard)
-    xz = torch.empty_like(xbf)
-    wsb = {a: torch.empty(max(1, ctx.workspace_bytes(UL.C, UL.S, UL.U, UL.N, UL.N_sym, a)), dtype=torch.uint8,
-                          device=dev) for a in ("mmse_ul", "zf_dl")}
-    base_fns = {"mmse_ul": lambda: dbp.detect_mmse(ctx, Hg, yg, N0=UL.N0, mod=UL.mod, x_hat=xb, hard=hb,
-                                                   ws=wsb["mmse_ul"]),
-                "zf_dl": lambda: dbp.precode_zf(ctx, Hdg, sg, x=xz, ws=wsb["zf_dl"])}
-    baselines = {}
-    for nm, fn in base_fns.items():
+    def timed_fn(fn, K, flush_k=0):
         for _ in range(3):
             fn()
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K1)]
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
         barrier()
         torch.cuda.synchronize()
         for e0, e1 in evs:
-            flush_l2(0)
+            flush_l2(flush_k)
             e0.record(stream)
             fn()
             e1.record(stream)
         torch.cuda.synchronize()
-        ms = float(mx([sum(e0.elapsed_time(e1) for e0, e1 in evs) / K1])[0])
-        bits = UL.bits_per_frame if nm == "mmse_ul" else DL.bits_per_frame
-        baselines[nm] = {"ms": ms, "gbps": bits / (ms * 1e-3) / 1e9}
+        barrier()
+        return float(mx([sum(e0.elapsed_time(e1) for e0, e1 in evs) / K])[0])
 
-    # the paper's own Table II workload (P803-804: U=16, 64-QAM, N=1200, N_sym=7 per coherence
-    # interval, T=5, B=1024 = 32 x 32) next to its printed K40-cluster cells -- context only
-    table2 = None
-    if not args.no_table2:
-        t2 = UL.scaled(N_sym=7)
-        H7, y7, _ = synth.uplink_frame(t2, c0, c1)
-        Hd7, s7 = synth.downlink_frame(t2.scaled(algo="admm_dl"), c0, c1)
-        H7g, y7g = torch.from_numpy(H7).to(dev), torch.from_numpy(y7).to(dev)
-        Hd7g, s7g = torch.from_numpy(Hd7).to(dev), torch.from_numpy(s7).to(dev)
-        bits7 = t2.U * t2.N * t2.N_sym * 6
-        paper = {"admm_ul": (21.53, 39.95, "P771"), "cg_ul": (13.61, 59.25, "P779"), "admm_dl": (11.11, 77.40, "P787")}
-        fns = {"admm_ul": lambda: dbp.detect_admm(ctx, H7g, y7g, rho=t2.rho, N0=t2.N0, mod="qam64", T=t2.T),
-               "cg_ul": lambda: dbp.detect_cg(ctx, H7g, y7g, rho=t2.N0, mod="qam64", T=t2.T),
-               "admm_dl": lambda: dbp.beamform_admm(ctx, Hd7g, s7g, rho=t2.rho, T=t2.T)}
-        table2 = {"workload": "B=1024 (C=32 x S=32), U=16, 64-QAM, N=1200, N_sym=7, T=5 (PAPER.md P803-804); "
-                              "two-kernel path (the fused kernel takes N_sym = 1)",
-                  "paper_hw": "32 x Tesla K40 + Cray Aries MPI (P685, P799), CPU wall clock"}
-        K2 = 20
-        for nm, fn in fns.items():
-            for _ in range(2):
-                fn()
-            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K2)]
-            barrier()
-            torch.cuda.synchronize()
-            for e0, e1 in evs:
-                flush_l2(1)
-                e0.record(stream)
-                fn()
-                e1.record(stream)
-            torch.cuda.synchronize()
-            ms = float(mx([sum(e0.elapsed_time(e1) for e0, e1 in evs) / K2])[0])
-            pl, pt, cite = paper[nm]
-            table2[nm] = {"ms": ms, "mbps": bits7 / (ms * 1e-3) / 1e6, "paper_ms": pl, "paper_mbps": pt,
-                          "paper_cite": cite}
-        del H7g, y7g, Hd7g, s7g
+    # ---------------------------------------------------------------- world > 1 legs
+    multi = None
+    if world > 1:
+        multi = {"nccl_comm": comm, "modes": {}}
+        ref_outs = (s_hat.cpu().numpy().copy(), x_hat.cpu().numpy().copy(), xbf.cpu().numpy().copy())
+        rows = gather_rows([step_ms_rank, kern_ms_rank, step_ms_rank - kern_ms_rank,
+                            (st1["allreduce_calls"] - st0["allreduce_calls"]) / args.steps], world, dist, dev)
+        multi["per_rank"] = [{"rank": r, "step_ms": v[0], "kernel_ms": v[1], "exposed_comm_ms": v[2],
+                              "allreduce_calls_per_step": v[3]} for r, v in enumerate(rows)]
+
+        def rel(a, b):
+            return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+        # (i) device-side consensus (NEXT-1) on the same step, cross-checked against the NCCL path
+        if not args.no_device_consensus:
+            try:
+                ctx.set_option(dbp.OPT_DEVICE_CONSENSUS, 1)
+                for _ in range(3):
+                    for nm in ORDER:
+                        solver(nm, UL.T)
+                ctx.sync()
+                pdc = mx(timed_region(args.steps, UL.T, ORDER))
+                ctx.sync()
+                dc = (s_hat.cpu().numpy(), x_hat.cpu().numpy(), xbf.cpu().numpy())
+                err = [rel(a, b) for a, b in zip(dc, ref_outs)]
+                ms = float(pdc.sum()) / args.steps
+                multi["modes"]["device_consensus"] = {
+                    "ms_per_step": ms, "value": BITS_PER_STEP / (ms * 1e-3) / 1e9,
+                    "rel_l2_vs_nccl": {"admm_ul": err[0], "cg_ul": err[1], "admm_dl": err[2]},
+                    "solvers_ms": dict(zip(ORDER, (pdc / args.steps).tolist()))}
+            except Exception as e:   # a protocol fault is a bounded timeout (DBP_ERR_CUDA), never a hang
+                multi["modes"]["device_consensus"] = {"error": str(e)[:300]}
+            finally:
+                ctx.set_option(dbp.OPT_DEVICE_CONSENSUS, 0)
+
+        # (ii) world-1 solve of the whole frame on every rank (same GPU): rel-L2 <= 1e-5
+        ctx1 = dbp.Context(device=local, rank=0, world=1)
+        Hf, yf, Hcf, ycf, Hdf, sf = (to(a) for a in full)
+        s1, _ = dbp.detect_admm(ctx1, Hf, yf, rho=UL.rho, N0=UL.N0, mod=UL.mod, T=UL.T)
+        x1, _ = dbp.detect_cg(ctx1, Hcf, ycf, rho=CG.N0, mod=CG.mod, T=CG.T)
+        b1 = dbp.beamform_admm(ctx1, Hdf, sf, rho=DL.rho, T=DL.T)
+        ctx1.sync()
+        e1 = [rel(ref_outs[0], s1.cpu().numpy()), rel(ref_outs[1], x1.cpu().numpy()),
+              rel(ref_outs[2], b1[c0:c1].cpu().numpy())]
+        worst = mx([max(e1)])[0]
+        multi["vs_world1"] = {"rel_l2": {"admm_ul": e1[0], "cg_ul": e1[1], "admm_dl": e1[2]},
+                              "max_over_ranks": float(worst), "ok": bool(worst <= 1e-5)}
+
+        # (iii) subcarrier-sharded control: all clusters of N/G subcarriers per rank, no communication
+        n0, n1 = rank * UL.N // world, (rank + 1) * UL.N // world
+        shard = {k: to(np.ascontiguousarray(a[:, n0:n1] if a.ndim == 4 else a[n0:n1]))
+                 for k, a in zip(("H", "y", "Hc", "yc", "Hd", "s"), full)}
+
+        def ctrl(nm, T):
+            if nm == "admm_ul":
+                dbp.detect_admm(ctx1, shard["H"], shard["y"], rho=UL.rho, N0=UL.N0, mod=UL.mod, T=T)
+            elif nm == "cg_ul":
+                dbp.detect_cg(ctx1, shard["Hc"], shard["yc"], rho=CG.N0, mod=CG.mod, T=T)
+            else:
+                dbp.beamform_admm(ctx1, shard["Hd"], shard["s"], rho=DL.rho, T=T)
+
+        for _ in range(3):
+            for nm in ORDER:
+                ctrl(nm, UL.T)
+        pc = mx(timed_region(args.steps, UL.T, ORDER, fn=ctrl))
+        ms = float(pc.sum()) / args.steps
+        multi["modes"]["control_subcarrier_sharded"] = {
+            "ms_per_step": ms, "value": BITS_PER_STEP / (ms * 1e-3) / 1e9, "scaling": "weak-equivalent",
+            "subcarriers_per_rank": n1 - n0, "solvers_ms": dict(zip(ORDER, (pc / args.steps).tolist()))}
+        del Hf, yf, Hcf, ycf, Hdf, sf, shard
+        ctx1.close()
+
+    # ---------------------------------------------------------------- world == 1 context legs
+    baselines, table2, configs = {}, None, None
+    if world == 1:
+        # centralized baselines (Table I rows MMSE-UL / ZF-DL, the paper's comparison P789-792, P810)
+        xb, hb, xz = torch.empty_like(s_hat), torch.empty_like(hard), torch.empty_like(xbf)
+        wsb = {a: torch.empty(max(1, ctx.workspace_bytes(UL.C, UL.S, UL.U, UL.N, UL.N_sym, a)), dtype=torch.uint8,
+                              device=dev) for a in ("mmse_ul", "zf_dl")}
+        for nm, fn, bits in (("mmse_ul", lambda: dbp.detect_mmse(ctx, Hg, yg, N0=UL.N0, mod=UL.mod, x_hat=xb,
+                                                                  hard=hb, ws=wsb["mmse_ul"]), UL.bits_per_frame),
+                             ("zf_dl", lambda: dbp.precode_zf(ctx, Hdg, sg, x=xz, ws=wsb["zf_dl"]),
+                              DL.bits_per_frame)):
+            ms = timed_fn(fn, K1)
+            baselines[nm] = {"ms": ms, "gbps": bits / (ms * 1e-3) / 1e9}
+
+        # the paper's own Table II workload (P803-804: U=16, 64-QAM, N=1200, N_sym=7 per coherence
+        # interval, T=5, B=1024 = 32 x 32) next to its printed K40-cluster cells -- context only
+        if not args.no_table2:
+            t2 = UL.scaled(N_sym=7)
+            H7, y7 = gen_frame("ul", t2, 0, t2.C, workers=workers)
+            Hd7, s7 = gen_frame("dl", t2.scaled(algo="admm_dl"), 0, t2.C, workers=workers)
+            H7g, y7g, Hd7g, s7g = to(H7), to(y7), to(Hd7), to(s7)
+            bits7 = t2.U * t2.N * t2.N_sym * 6
+            paper = {"admm_ul": (21.53, 39.95, "P771"), "cg_ul": (13.61, 59.25, "P779"),
+                     "admm_dl": (11.11, 77.40, "P787")}
+            fns = {"admm_ul": lambda: dbp.detect_admm(ctx, H7g, y7g, rho=t2.rho, N0=t2.N0, mod="qam64", T=t2.T),
+                   "cg_ul": lambda: dbp.detect_cg(ctx, H7g, y7g, rho=t2.N0, mod="qam64", T=t2.T),
+                   "admm_dl": lambda: dbp.beamform_admm(ctx, Hd7g, s7g, rho=t2.rho, T=t2.T)}
+            table2 = {"workload": "B=1024 (C=32 x S=32), U=16, 64-QAM, N=1200, N_sym=7, T=5 (PAPER.md P803-804)",
+                      "paper_hw": "32 x Tesla K40 + Cray Aries MPI (P685, P799), CPU wall clock"}
+            ctx.set_option(dbp.OPT_KERNEL_TIMING, 1)
+            ctx.kernel_times(reset=True)
+            for nm, fn in fns.items():
+                ms = timed_fn(fn, 20, flush_k=1)
+                pl, pt, cite = paper[nm]
+                table2[nm] = {"ms": ms, "mbps": bits7 / (ms * 1e-3) / 1e6, "paper_ms": pl, "paper_mbps": pt,
+                              "paper_cite": cite}
+            table2["kernels"] = sorted(ctx.kernel_times(reset=True))
+            ctx.set_option(dbp.OPT_KERNEL_TIMING, 0)
+            del H7g, y7g, Hd7g, s7g
+
+        # per-config entries (BASELINE configs; each solver timed alone, L2 flushed)
+        if not args.no_configs:
+            configs = {}
+            cfgA, cfgB, cfgE = synth.CONFIGS["A"], synth.CONFIGS["B"], synth.CONFIGS["E"]
+            HA, yA = gen_frame("ul", cfgA, 0, cfgA.C)
+            HB, yB = gen_frame("ul", cfgB, 0, cfgB.C, workers=workers)
+            HAg, yAg, HBg, yBg = to(HA), to(yA), to(HB), to(yB)
+            entries = [
+                ("A", "admm_ul", cfgA, lambda: dbp.detect_admm(ctx, HAg, yAg, rho=cfgA.rho, N0=cfgA.N0,
+                                                               mod=cfgA.mod, T=cfgA.T)),
+                ("B", "cg_ul", cfgB, lambda: dbp.detect_cg(ctx, HBg, yBg, rho=cfgB.N0, mod=cfgB.mod, T=cfgB.T)),
+                ("C", "admm_ul", UL, lambda: solver("admm_ul", UL.T)),
+                ("C_cg", "cg_ul", CG, lambda: solver("cg_ul", CG.T)),
+                ("D", "admm_dl", DL, lambda: solver("admm_dl", DL.T)),
+            ]
+            for key, algo, cfg, fn in entries:
+                ms = timed_fn(fn, K1)
+                configs[key] = {"algo": algo, "ms": ms, "gbps": cfg.bits_per_frame / (ms * 1e-3) / 1e9,
+                                "shape": f"C={cfg.C} S={cfg.S} U={cfg.U} N={cfg.N} {cfg.mod} T={cfg.T}"}
+            del HAg, yAg, HBg, yBg
+            # config E: one GPU's share at G = 8 (C_loc = 16 of 128 clusters, all 4800 subcarriers); the
+            # compute of the share only -- the allreduce of the 8-GPU run is not included
+            Ce = cfgE.C // 8
+            HE, yE = gen_frame("ul", cfgE, 0, Ce, workers=workers)
+            HEg, yEg = to(HE), to(yE)
+            del HE, yE
+            shareE = cfgE.scaled(C=Ce)
+            for key, algo, fn in (("E_share_admm_ul", "admm_ul",
+                                   lambda: dbp.detect_admm(ctx, HEg, yEg, rho=cfgE.rho, N0=cfgE.N0, mod=cfgE.mod,
+                                                           T=cfgE.T)),
+                                  ("E_share_cg_ul", "cg_ul",
+                                   lambda: dbp.detect_cg(ctx, HEg, yEg, rho=cfgE.N0, mod=cfgE.mod, T=cfgE.T))):
+                ms = timed_fn(fn, 20)
+                configs[key] = {"algo": algo, "ms": ms, "gbps": cfgE.bits_per_frame / (ms * 1e-3) / 1e9,
+                                "shape": f"per-GPU share of E at G=8: C_loc={Ce} (C=128) S=32 U=32 N=4800 "
+                                         f"{cfgE.mod} T={cfgE.T}; gbps = the whole frame's bits / this GPU's "
+                                         f"compute time (no allreduce)"}
+            del HEg, yEg
+            _ = shareE
+
     total_ms = float(per.sum())
     ms_seq = total_ms / args.steps
     ms_step = float(mx([conc_ms])[0]) / args.steps if concurrent else ms_seq
     value = BITS_PER_STEP / (ms_step * 1e-3) / 1e9
     solvers = {}
-    for i, nm in enumerate(order):
+    for i, nm in enumerate(ORDER):
         msT = per[i] / args.steps
         ms1 = per1[i] / K1
         solvers[nm] = {"ms": msT, "gbps": BITS[nm] / (msT * 1e-3) / 1e9, "ms_T1": ms1,
@@ -507,8 +747,8 @@ def main():
     # end to end through the C ABI with pinned host buffers
     e2e = None
     if args.e2e_steps > 0:
-        pin = lambda a: torch.from_numpy(a).pin_memory().numpy()
-        Hh, yh, Hdh, sh = pin(H), pin(y), pin(Hd), pin(s)
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+        Hh, yh, Hch, ych, Hdh, sh = pin(H), pin(y), pin(Hc), pin(yc), pin(Hd), pin(s)
         o1 = torch.empty(tuple(s_hat.shape), dtype=torch.complex64).pin_memory().numpy()
         o2 = torch.empty(tuple(hard.shape), dtype=torch.uint8).pin_memory().numpy()
         o3 = torch.empty(tuple(s_hat.shape), dtype=torch.complex64).pin_memory().numpy()
@@ -518,7 +758,7 @@ def main():
         def e2e_step():
             dbp.detect_admm(ctx, Hh, yh, rho=UL.rho, N0=UL.N0, mod=UL.mod, T=UL.T, s_hat=o1, hard=o2)
             dbp.beamform_admm(ctx, Hdh, sh, rho=DL.rho, T=DL.T, x=o5)
-            dbp.detect_cg(ctx, Hh, yh, rho=UL.N0, mod=UL.mod, T=UL.T, x_hat=o3, hard=o4)
+            dbp.detect_cg(ctx, Hch, ych, rho=CG.N0, mod=CG.mod, T=CG.T, x_hat=o3, hard=o4)
 
         e2e_step()
         barrier()
@@ -527,7 +767,7 @@ def main():
             e2e_step()
         barrier()
         dt = float(mx([time.perf_counter() - t0])[0]) / args.e2e_steps
-        h2d = 2 * (Hh.nbytes + yh.nbytes) + Hdh.nbytes + sh.nbytes
+        h2d = Hh.nbytes + yh.nbytes + Hch.nbytes + ych.nbytes + Hdh.nbytes + sh.nbytes
         d2h = o1.nbytes + o2.nbytes + o3.nbytes + o4.nbytes + o5.nbytes
         e2e = {"value": BITS_PER_STEP / dt / 1e9, "unit": "Gbit/s", "ms_per_step": dt * 1e3,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
@@ -547,7 +787,8 @@ def main():
                 "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Philox-4x32: i.i.d. Rayleigh "
                 "CN(0,1) channels, uniform Gray QAM, AWGN)", "config": workload_config(world),
-                "solvers": solvers, "centralized_baselines": baselines, "paper_table2_context": table2,
+                "solvers": solvers, "configs": configs, "centralized_baselines": baselines or None,
+                "paper_table2_context": table2, "multi_gpu": multi,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "gpu_launches_per_step": launches / args.steps,
                 "consensus_rounds_per_step": (st1["consensus_rounds"] - st0["consensus_rounds"]) / args.steps,

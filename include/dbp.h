@@ -142,6 +142,11 @@ dbp_status dbp_ctx_destroy(dbp_ctx* ctx);
 dbp_status dbp_set_option(dbp_ctx* ctx, int option, int64_t value);
 dbp_status dbp_get_stats(const dbp_ctx* ctx, dbp_stats* out);
 
+/* The context's communicator as NCCL sees it (ncclCommCount / ncclCommUserRank): the number of
+ * ranks the consensus allreduce spans and this rank's position.  world == 1: 1 and 0 (no
+ * communicator).  Errors: NULL arguments -> DBP_ERR_INVALID_ARG; NCCL failure -> DBP_ERR_NCCL. */
+dbp_status dbp_get_comm_info(const dbp_ctx* ctx, int* nranks, int* rank);
+
 /* Thread-local message describing the last non-OK status ("" if none). */
 const char* dbp_last_error(void);
 

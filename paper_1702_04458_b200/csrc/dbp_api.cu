@@ -175,6 +175,18 @@ extern "C" dbp_status dbp_get_stats(const dbp_ctx* c, dbp_stats* s) {
     return DBP_OK;
 }
 
+extern "C" dbp_status dbp_get_comm_info(const dbp_ctx* c, int* nranks, int* rank) {
+    if (!c || !nranks || !rank) return fail(DBP_ERR_INVALID_ARG, "NULL argument");
+    if (!c->comm) {
+        *nranks = 1;
+        *rank = 0;
+        return DBP_OK;
+    }
+    NC(ncclCommCount(c->comm, nranks));
+    NC(ncclCommUserRank(c->comm, rank));
+    return DBP_OK;
+}
+
 // ----------------------------------------------------------------- shapes
 struct Shape {
     int C, C_loc, S, U, UP, N, J;

@@ -29,7 +29,7 @@ OPT_DEVICE_CONSENSUS = 4
 EXPORTS = ["dbp_get_unique_id", "dbp_ctx_create", "dbp_ctx_destroy", "dbp_set_option", "dbp_get_stats",
            "dbp_last_error", "dbp_workspace_bytes", "dbp_detect_admm", "dbp_detect_cg",
            "dbp_beamform_admm", "dbp_slice", "dbp_sync", "dbp_get_kernel_times", "dbp_complexity",
-           "dbp_detect_mmse", "dbp_precode_zf"]
+           "dbp_detect_mmse", "dbp_precode_zf", "dbp_get_comm_info"]
 CPLX_ALGO = {"admm_dl": 0, "admm_ul": 1, "cg_ul": 2, "zf_dl": 3, "mmse_ul": 4}
 CPLX_MODE = {"SxS": 0, "UxU": 1, None: 1}
 CPLX_METRIC = {"TM": 0, "AR": 1}
@@ -84,6 +84,7 @@ def load() -> ctypes.CDLL:
         "dbp_complexity": [I, I, I, I64, I64, I64, I64, P],
         "dbp_detect_mmse": [P, P, P, P, F, F, I, P, P, P, S, P],
         "dbp_precode_zf": [P, P, P, P, P, P, S, P],
+        "dbp_get_comm_info": [P, P, P],
     }
     for name, args in sigs.items():
         fn = getattr(lib, name)
@@ -216,6 +217,12 @@ class Context:
         s = Stats()
         _check(load().dbp_get_stats(self._h, ctypes.byref(s)))
         return {k: getattr(s, k) for k, _ in Stats._fields_}
+
+    def comm_info(self) -> dict:
+        """{'nranks': ncclCommCount, 'rank': ncclCommUserRank} of the consensus communicator."""
+        n, r = ctypes.c_int(), ctypes.c_int()
+        _check(load().dbp_get_comm_info(self._h, ctypes.byref(n), ctypes.byref(r)))
+        return {"nranks": n.value, "rank": r.value}
 
     def workspace_bytes(self, C, S, U, N, N_sym, algo: str) -> int:
         d = Dims(C, S, U, N, N_sym)
