@@ -79,7 +79,7 @@ struct FZ {
 struct FuArgs {
     XArgs xc;
     int S, U, N, C, T, WPS, NPC;
-    int stg, wreg, nkk, nsb, stage_bytes;   // ring stage pitch, per-warp region pitch; TC: K8 steps, DL boxes
+    int stg, wreg, nkk, nsb, stage_bytes, yoff;   // ring stage pitch, per-warp region pitch; TC: K steps, DL boxes, y offset
     float rho, gamma, delta;
     // UL outputs (SOLVER 0, 1)
     float2* s_hat;        // [N][U]
@@ -130,7 +130,10 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     const int ngroups = (a.N + NPC - 1) / NPC;
     const int nitems = blockIdx.x < ngroups ? (ngroups - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const int nch = Z::TC ? PW : (a.S + SC - 1) / SC;  // stages per pass: TC one per pair, else SC antennas
-    const int per_item = DL ? 2 * nch : nch;           // DL: Gram pass + output pass
+#ifndef DBP_EXP_NO_DLOUT
+#define DBP_EXP_NO_DLOUT 0      // experiment only: drop the DL output pass (wrong results; timing the pass)
+#endif
+    const int per_item = DL && !DBP_EXP_NO_DLOUT ? 2 * nch : nch;   // DL: Gram pass + output pass
     const int nseq = nitems * per_item;
 
     // TMA issue cursor (lane 0): the (item, chunk) of the next stage to load, advanced by one
@@ -147,7 +150,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                 for (int sb = 0; sb < a.nsb; ++sb) tma_load4(dst + sb * 2048, &tmH, 16 * sb, 0, n, cb * PW + ch, &bar[st]);
             } else {
                 tma_load4(dst, &tmH, 0, 0, n, cb * PW + ch, &bar[st]);
-                tma_load4(dst + a.nkk * 1024, &tmY, 0, 0, n, cb * PW + ch, &bar[st]);
+                tma_load4(dst + a.yoff, &tmY, 0, 0, n, cb * PW + ch, &bar[st]);
             }
         } else if (DL) {
             tma_load4(dst, &tmH, ch * SC, 0, n, cb * PW, &bar[st]);
@@ -247,9 +250,16 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
             for (int h = 0; h < 2; ++h) {
                 for (int p4 = 0; p4 < 4; ++p4) {
                     mbar_wait(&bar[st], phase);
-                    float acc[5][4];
-                    tc_gram<DL, MF>(acc, wbase + st * a.stg, a.nkk, g, t4);
-                    tc_store<DL, MF>(acc, gtri + p4 * TRI, mfl + p4 * UP, g, t4);
+                    if constexpr (DBP_FZ_TC == 2) {
+                        // fp16 Z + Z^H Gram; the consumed stage doubles as the transpose scratch
+                        unsigned char* sb = wbase + st * a.stg;
+                        tc16_gram_pair<DL, MF>(sb, a.nkk, gtri + p4 * TRI, mfl + p4 * UP,
+                                               reinterpret_cast<float2*>(sb), g, t4, lane);
+                    } else {
+                        float acc[5][4];
+                        tc_gram<DL, MF>(acc, wbase + st * a.stg, a.nkk, g, t4);
+                        tc_store<DL, MF>(acc, gtri + p4 * TRI, mfl + p4 * UP, g, t4);
+                    }
                     next_stage();
                 }
                 __syncwarp();
@@ -565,7 +575,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
             __syncwarp();
             if constexpr (Z::TC) {
                 dl_output_tc(pl - q * F::PLP, F::PLP, n);
-            } else {
+            } else if (!DBP_EXP_NO_DLOUT) {
                 float2 r[UP];
                 read_vec<UP>(pl, r);
                 dl_output(r, n, valid);
@@ -586,19 +596,22 @@ static bool launch_fz_t(const LaunchCtx& L, const float2* H, const float2* y, Fu
     CUtensorMap tmH{}, tmY{};
     // H: UL [C][N][S][U] -> dims (U, S, N, C); DL [C][N][U][S] -> dims (S, U, N, C); y [C][N][1][S]
     if constexpr (Z::TC) {
-        const int S8 = (a.S + 7) / 8 * 8;
+        // TF32 path: K8 steps (S rounded to 8); FP16 path: K16 steps (S rounded to 16)
+        const int S8 = DBP_FZ_TC == 2 ? (a.S + 15) / 16 * 16 : (a.S + 7) / 8 * 8;
         a.nsb = (a.S + 15) / 16;
         if (!Z::DL) {
             if (!make_map4(&tmH, H, a.U, a.S, a.N, a.C, 16, S8, 1, 1, true)) return false;
             if (!make_map4(&tmY, y, a.S, 1, a.N, a.C, S8, 1, 1, 1)) return false;
-            a.nkk = S8 / 8;
+            a.nkk = DBP_FZ_TC == 2 ? S8 / 16 : S8 / 8;
             a.stage_bytes = S8 * 128 + S8 * 8;
+            a.yoff = S8 * 128;
         } else {
             if (!make_map4(&tmH, H, a.S, a.U, a.N, a.C, 16, 16, 1, 1, true)) return false;
-            a.nkk = 2 * a.nsb;
+            a.nkk = DBP_FZ_TC == 2 ? a.nsb : 2 * a.nsb;
             a.stage_bytes = a.nsb * 2048;
         }
-        a.stg = (a.stage_bytes + 1023) / 1024 * 1024;
+        // TC == 2 reuses the consumed stage as the [16][17] float2 transpose scratch (2176 B)
+        a.stg = (std::max(a.stage_bytes, DBP_FZ_TC == 2 ? 16 * 17 * 8 : 0) + 1023) / 1024 * 1024;
         a.wreg = (NST_of<UP, SOLVER>() * a.stg + Z::LOC + 1023) / 1024 * 1024;
     } else {
         if (!Z::DL) {

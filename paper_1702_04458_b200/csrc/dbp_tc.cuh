@@ -149,4 +149,182 @@ __device__ __forceinline__ void tc_store(const float (&acc)[5][4], float2* gtri,
     }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// FP16 variant (DBP_FZ_TC == 2): mma.sync m16n8k16 f16 -> f32 (485 TFLOP/s measured, twice TF32)
+// with two passes instead of three.  The pair is first scaled by an exact power of two so its
+// largest |Re|, |Im| lies in [1, 2) (warp max; fp16 then keeps the split normal down to 2^-14 of
+// it -- scale-free like TF32).  v = hi + lo with hi = v with the low 13 mantissa bits cleared
+// (exactly an fp16 value) and lo = v - hi.  Since G = hi^H hi + hi^H lo + lo^H hi (dropping
+// lo^H lo, ~2^-22) is Z + Z^H with Z = 0.5 hi^H hi + hi^H lo, the tensor cores form Z (A = hi,
+// B = 0.5 hi then B = lo: two passes) and G_rc = Z_rc + conj(Z_cr) is formed through a per-warp
+// [16][17] scratch.  The matched filter H^H y (16 values) runs on the FP32 cores from the same
+// fragments (unscaled), summed over the 4 lanes of a quad.
+//
+// K16 step kk covers antennas 16 kk .. 16 kk + 15 (K index = antenna); lane (g, t) holds
+//   v[uh][kh][e] = h(user g + 8 uh, antenna 16 kk + 8 kh + 2 t + e),
+// the A fragments a0 = {v[0][0][0..1]}, a1 = {v[1][0][..]}, a2 = {v[0][1][..]}, a3 = {v[1][1][..]}
+// (Re and Im parts separately), and -- B of the Re tiles being A^T -- all B fragments.
+__device__ __forceinline__ void mma_f16(float (&d)[4], unsigned a0, unsigned a1, unsigned a2, unsigned a3,
+                                        unsigned b0, unsigned b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ unsigned f16x2(float lo_half, float hi_half) {
+    unsigned r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi_half), "f"(lo_half));
+    return r;
+}
+constexpr unsigned TC_NEG2 = 0x80008000u;
+
+// Stage reads of one K16 step (see the layouts above).
+template <bool DL>
+__device__ __forceinline__ void tc16_load(float2 (&v)[2][2][2], const unsigned char* stage, int kk, int g, int t) {
+    if (DL) {
+#pragma unroll
+        for (int uh = 0; uh < 2; ++uh)
+#pragma unroll
+            for (int kh = 0; kh < 2; ++kh) {
+                const float4 q = *reinterpret_cast<const float4*>(stage + kk * 2048 + (g + 8 * uh) * 128 +
+                                                                  (((4 * kh + t) ^ g) << 4));
+                v[uh][kh][0] = make_float2(q.x, q.y);
+                v[uh][kh][1] = make_float2(q.z, q.w);
+            }
+    } else {
+#pragma unroll
+        for (int kh = 0; kh < 2; ++kh)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int s = 16 * kk + 8 * kh + 2 * t + e;
+#pragma unroll
+                for (int uh = 0; uh < 2; ++uh) {
+                    const int u = g + 8 * uh;
+                    v[uh][kh][e] = *reinterpret_cast<const float2*>(stage + s * 128 + (((u >> 1) ^ (s & 7)) << 4) +
+                                                                    ((u & 1) << 3));
+                }
+            }
+    }
+}
+
+// G (lower triangle, packed) and, UL, H^H y of one pair.  zs: per-warp [16][17] float2 scratch.
+// nk16 = ceil(S / 16) K16 steps (antennas >= S zero-filled by the TMA).
+template <bool DL, bool MF>
+__device__ __forceinline__ void tc16_gram_pair(const unsigned char* stage, int nk16, float2* gtri, float2* mfl,
+                                               float2* zs, int g, int t, int lane) {
+    // pass 0: the pair's scale (exact power of two)
+    float mx = 0.f;
+    for (int kk = 0; kk < nk16; ++kk) {
+        float2 v[2][2][2];
+        tc16_load<DL>(v, stage, kk, g, t);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float2 x = v[i >> 2][(i >> 1) & 1][i & 1];
+            mx = fmaxf(mx, fmaxf(fabsf(x.x), fabsf(x.y)));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const int ex = mx > 0.f ? ((__float_as_int(mx) >> 23) & 0xff) - 127 : 0;
+    const float sc = __int_as_float((127 - ex) << 23);                 // 2^-ex: max -> [1, 2)
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[i][e] = 0.f;
+    f2x mf[2] = {0ull, 0ull};
+    const float2* yv = reinterpret_cast<const float2*>(stage + nk16 * 16 * 128);   // UL: y after H
+    for (int kk = 0; kk < nk16; ++kk) {
+        float2 v[2][2][2];
+        tc16_load<DL>(v, stage, kk, g, t);
+        if (MF) {
+            // conj(h_su) y_s over this lane's 8 (antenna, user) values, FP32, unscaled
+#pragma unroll
+            for (int kh = 0; kh < 2; ++kh) {
+                const float4 yy = *reinterpret_cast<const float4*>(yv + 16 * kk + 8 * kh + 2 * t);
+#pragma unroll
+                for (int uh = 0; uh < 2; ++uh) {
+                    x2_cmac(mf[uh], v[uh][kh][0], yy.x, yy.y);
+                    x2_cmac(mf[uh], v[uh][kh][1], yy.z, yy.w);
+                }
+            }
+        }
+        // fragments: index f = uh + 2 kh  (a0: uh 0 kh 0, a1: uh 1 kh 0, a2: uh 0 kh 1, a3: uh 1 kh 1)
+        unsigned rh[4], ih[4], rq[4], iq[4], rl[4], il[4];
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+            const int uh = f & 1, kh = f >> 1;
+            float hr[2], hi_[2], lr[2], li[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const float xr = v[uh][kh][e].x * sc, xi = v[uh][kh][e].y * sc;
+                hr[e] = __uint_as_float(__float_as_uint(xr) & 0xffffe000u);
+                hi_[e] = __uint_as_float(__float_as_uint(xi) & 0xffffe000u);
+                lr[e] = xr - hr[e];
+                li[e] = xi - hi_[e];
+            }
+            rh[f] = f16x2(hr[0], hr[1]);
+            ih[f] = f16x2(hi_[0], hi_[1]);
+            rq[f] = f16x2(0.5f * hr[0], 0.5f * hr[1]);
+            iq[f] = f16x2(0.5f * hi_[0], 0.5f * hi_[1]);
+            rl[f] = f16x2(lr[0], lr[1]);
+            il[f] = f16x2(li[0], li[1]);
+        }
+        // Z += hi^H (0.5 hi) + hi^H lo: Re tiles A_re B_re + A_im B_im, Im tiles A_re B_im - A_im B_re
+#pragma unroll
+        for (int pass = 0; pass < 2; ++pass) {
+            const unsigned* Br = pass ? rl : rq;
+            const unsigned* Bi = pass ? il : iq;
+            mma_f16(acc[0], rh[0], rh[1], rh[2], rh[3], Br[0], Br[2]);
+            mma_f16(acc[0], ih[0], ih[1], ih[2], ih[3], Bi[0], Bi[2]);
+            mma_f16(acc[1], rh[0], rh[1], rh[2], rh[3], Br[1], Br[3]);
+            mma_f16(acc[1], ih[0], ih[1], ih[2], ih[3], Bi[1], Bi[3]);
+            mma_f16(acc[2], rh[0], rh[1], rh[2], rh[3], Bi[0], Bi[2]);
+            mma_f16(acc[2], ih[0], ih[1], ih[2], ih[3], Br[0] ^ TC_NEG2, Br[2] ^ TC_NEG2);
+            mma_f16(acc[3], rh[0], rh[1], rh[2], rh[3], Bi[1], Bi[3]);
+            mma_f16(acc[3], ih[0], ih[1], ih[2], ih[3], Br[1] ^ TC_NEG2, Br[3] ^ TC_NEG2);
+        }
+    }
+    // G = Z + Z^H through the scratch (row stride 17: the transposed reads are 2-way at most)
+    const float us = __int_as_float((127 + 2 * ex) << 23);                // 2^(2 ex)
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int e1 = 0; e1 < 2; ++e1)
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc)
+                zs[(g + 8 * e1) * 17 + 8 * h + 2 * t + cc] = make_float2(acc[h][2 * e1 + cc], acc[2 + h][2 * e1 + cc]);
+    __syncwarp();
+    const float sg = DL ? -1.f : 1.f;                                     // DL: B = H H^H = conj(UL form)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int e1 = 0; e1 < 2; ++e1)
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+                const int r = g + 8 * e1, c = 8 * h + 2 * t + cc;
+                if (c <= r) {
+                    const float2 zt = zs[c * 17 + r];
+                    gtri[pidx(r, c)] = make_float2((acc[h][2 * e1 + cc] + zt.x) * us,
+                                                   sg * (acc[2 + h][2 * e1 + cc] - zt.y) * us);
+                }
+            }
+    if (MF) {
+#pragma unroll
+        for (int uh = 0; uh < 2; ++uh) {
+            float2 m = upk2(mf[uh]);
+#pragma unroll
+            for (int o = 1; o < 4; o <<= 1) {
+                m.x += __shfl_xor_sync(0xffffffffu, m.x, o);
+                m.y += __shfl_xor_sync(0xffffffffu, m.y, o);
+            }
+            if (t == 0) mfl[g + 8 * uh] = m;
+        }
+    }
+    (void)lane;
+}
+
 }  // namespace dbp

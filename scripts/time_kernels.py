@@ -15,10 +15,16 @@ ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--split", type=int, default=0)
 ap.add_argument("--T", type=int, default=0)
 ap.add_argument("--nofused", type=int, default=0)
+ap.add_argument("--nsym", type=int, default=0)
+ap.add_argument("--N", type=int, default=0)
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
 if a.T:
     cfg = cfg.scaled(T=a.T)
+if a.nsym:
+    cfg = cfg.scaled(N_sym=a.nsym)
+if a.N:
+    cfg = cfg.scaled(N=a.N)
 ctx = dbp.Context(0)
 ctx.set_option(dbp.OPT_FORCE_SPLIT, a.split)
 ctx.set_option(dbp.OPT_NO_FUSED, a.nofused)
