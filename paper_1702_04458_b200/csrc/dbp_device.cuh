@@ -15,6 +15,40 @@
 
 namespace dbp {
 
+// ---------------------------------------------------------- debug: schedule fuzzing
+// compute-sanitizer (racecheck / synccheck) is unavailable on the GPU pool, so a debug build
+// (-DDBP_FUZZ=1, scripts/build_variants.py) stands in for it: every warp / CTA barrier is
+// preceded and followed by a pseudo-random per-thread __nanosleep (0..511 ns) that reorders
+// the threads' arrivals and subsequent shared-memory traffic, and every kernel first fills its
+// dynamic shared memory with NaN, so a missing barrier or a read-before-write turns into a
+// parity failure of the GPU tests (tests/test_gpu_parity.py run with DBP_LIB=<fuzz build>).
+#ifndef DBP_FUZZ
+#define DBP_FUZZ 0
+#endif
+__device__ __forceinline__ void dbp_fuzz_sleep() {
+#if DBP_FUZZ
+    unsigned x = (unsigned)clock() ^ (threadIdx.x * 2654435761u) ^ (blockIdx.x * 40503u);
+    x ^= x >> 13;
+    x *= 0x5bd1e995u;
+    x ^= x >> 15;
+    __nanosleep(x & 511u);
+#endif
+}
+#define DBP_SYNCWARP() do { ::dbp::dbp_fuzz_sleep(); __syncwarp(); ::dbp::dbp_fuzz_sleep(); } while (0)
+#define DBP_SYNCTHREADS() do { ::dbp::dbp_fuzz_sleep(); __syncthreads(); ::dbp::dbp_fuzz_sleep(); } while (0)
+#if DBP_FUZZ
+#define DBP_POISON_SMEM(base)                                                                   \
+    do {                                                                                        \
+        unsigned nb_;                                                                           \
+        asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(nb_));                          \
+        unsigned* w_ = reinterpret_cast<unsigned*>(base);                                       \
+        for (unsigned i_ = threadIdx.x; i_ < nb_ / 4; i_ += blockDim.x) w_[i_] = 0x7fc00001u;   \
+        __syncthreads();                                                                        \
+    } while (0)
+#else
+#define DBP_POISON_SMEM(base) do { } while (0)
+#endif
+
 // ----------------------------------------------------------------- complex
 __device__ __forceinline__ float2 c_add(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 c_sub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }

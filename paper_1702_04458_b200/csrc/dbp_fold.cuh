@@ -152,10 +152,10 @@ __device__ __forceinline__ void fold_jacobi(f2x (&A)[Fold<UP>::NSLOT], f2x (&E)[
     using F = Fold<UP>;
 #pragma unroll
     for (int m = 0; m < 4; ++m) dr[m] = dg[m] > 0.f ? rsqrtf(dg[m]) : 1.f;
-    __syncwarp();
+    DBP_SYNCWARP();
 #pragma unroll
     for (int m = 0; m < 4; ++m) dline[row[m]] = dr[m];
-    __syncwarp();
+    DBP_SYNCWARP();
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
 #pragma unroll
@@ -178,7 +178,7 @@ __device__ __forceinline__ bool fold_sweep(f2x (&A)[Fold<UP>::NSLOT], f2x (&E)[4
     for (int k = 0; k < UP; ++k) {
         const int mk = k / L;
         const int lk = (mk & 1) ? (mk + 1) * L - 1 - k : k - mk * L;   // owner lane of row k
-        __syncwarp();
+        DBP_SYNCWARP();
         // publish column k of the current matrix: c_j = a_jk (rows >= k from
         // every lane's slot k, rows < k as conj of the owner's row k)
         float2* const dump = pl + UP + 1;
@@ -190,7 +190,7 @@ __device__ __forceinline__ bool fold_sweep(f2x (&A)[Fold<UP>::NSLOT], f2x (&E)[4
             for (int t = 0; t < k && t < (mk + 1) * L; ++t) pl[t] = c_conj(upk2(A[F::off(mk) + t]));
             if (BORDER) pl[UP] = upk2(E[mk]);
         }
-        __syncwarp();
+        DBP_SYNCWARP();
         float2 cr[4];
 #pragma unroll
         for (int m = 0; m < 4; ++m) cr[m] = pl[row[m]];
@@ -312,10 +312,10 @@ template <int UP>
 __device__ __forceinline__ void fold_mv(const f2x (&A)[Fold<UP>::NSLOT], const float2 (&v)[4], float2 (&y)[4],
                                         float2* vline, float2* ybuf, const int (&row)[4], int l) {
     using F = Fold<UP>;
-    __syncwarp();
+    DBP_SYNCWARP();
 #pragma unroll
     for (int m = 0; m < 4; ++m) vline[row[m]] = v[m];
-    __syncwarp();
+    DBP_SYNCWARP();
     f2x col[UP];
 #pragma unroll
     for (int t = 0; t < UP; ++t) col[t] = 0ull;
@@ -343,7 +343,7 @@ __device__ __forceinline__ void fold_mv(const f2x (&A)[Fold<UP>::NSLOT], const f
         const float2 c0 = upk2(col[t2]), c1 = upk2(col[t2 + 1]);
         yb[t2 / 2] = make_float4(c0.x, c0.y, c1.x, c1.y);
     }
-    __syncwarp();
+    DBP_SYNCWARP();
 #pragma unroll
     for (int m = 0; m < 4; ++m)
 #pragma unroll

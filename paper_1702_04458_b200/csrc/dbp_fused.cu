@@ -102,6 +102,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     constexpr int L = F::L, PW = F::PW, SC = F::SC, NST = Z::NST, R = F::R, TRI = F::TRI;
     constexpr bool DL = Z::DL, MF = Z::MF;
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    DBP_POISON_SMEM(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     // 1024-aligned base: [4 warp regions][mbarriers + CG queue (128 B)][Wp, Sv, Gp, Gs]
     unsigned char* const base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -164,7 +165,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
         for (int s = 0; s < NST; ++s) mbar_init(&bar[s], 1);
         fence_mbar_init();
     }
-    __syncwarp();
+    DBP_SYNCWARP();
     if (lane == 0)
         for (int s = 0; s < NST && s < nseq; ++s) issue(s);
 
@@ -173,7 +174,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     static_assert(Z::WARPS * NST * 8 <= 96, "mbarriers overlap the CG queue indices");
     int* qsub = reinterpret_cast<int*>(cta + 96);          // CG queue: subcarrier of each slot
     auto next_stage = [&]() {
-        __syncwarp();
+        DBP_SYNCWARP();
         if (lane == 0 && sq + NST < nseq) {
             fence_proxy_async();
             issue(st);
@@ -262,7 +263,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                     }
                     next_stage();
                 }
-                __syncwarp();
+                DBP_SYNCWARP();
                 if ((q >> 2) == h) {
                     const float2* gq = gtri + (q & 3) * TRI;
 #pragma unroll
@@ -274,7 +275,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                         if (MF) E[m] = pk2(mfl[(q & 3) * UP + row[m]]);
                     }
                 }
-                __syncwarp();
+                DBP_SYNCWARP();
             }
         } else {
             for (int ch = 0; ch < nch; ++ch) {
@@ -317,7 +318,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
 #pragma unroll
                 for (int m = 0; m < R; ++m) Wp[warp * UP + row[m]] = upk2(E[m]);
             }
-            __syncthreads();
+            DBP_SYNCTHREADS();
             // the subcarrier sums go to CG queue slots qn..qn+NPC-1 (4 slots, one per warp)
             for (int e = tid; e < NPC * (TRI + UP); e += Z::WARPS * 32) {
                 const int jj = e / (TRI + UP), f = e - jj * (TRI + UP);
@@ -332,7 +333,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
             }
             if (tid < NPC) qsub[qn + tid] = (blockIdx.x + it * gridDim.x) * NPC + tid;
             qn += NPC;
-            __syncthreads();
+            DBP_SYNCTHREADS();
             // exact solve of queue slot w on the warp's UP-lane groups (lane-row Gauss-Jordan,
             // dbp_lanerow.cuh): returns ((G_w + delta I)^{-1} rhs)_u for u = lane % UP
             auto solve = [&](int w, float delta, float2 rhs_u, bool live) {
@@ -358,11 +359,11 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                     const int u = lane % UP;
                     const float2 sv = (u < a.U && nn < a.N) ? a.s[(size_t)nn * a.U + u] : make_float2(0.f, 0.f);
                     const float2 r = solve(warp, 0.f, sv, nn < a.N);
-                    __syncwarp();
+                    DBP_SYNCWARP();
                     if (lane < UP) Sv[warp * UP + u] = r;
                 }
                 qn = 0;
-                __syncthreads();
+                DBP_SYNCTHREADS();
                 if constexpr (Z::TC) {
                     dl_output_tc(Sv + j * UP, 0, n);
                 } else {
@@ -370,7 +371,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                     read_vec<UP>(Sv + j * UP, r);
                     dl_output(r, n, valid);
                 }
-                __syncthreads();                        // Sv / Gs reused by the next item
+                DBP_SYNCTHREADS();                        // Sv / Gs reused by the next item
                 continue;
             } else {
                 if (qn < Z::WARPS && it + 1 < nitems) continue;
@@ -407,9 +408,9 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                         x = make_float2(0.f, 0.f);
                         float rr = group_sum<UP>(c_norm2(r));
                         for (int t = 0; t < a.T; ++t) {
-                            __syncwarp();
+                            DBP_SYNCWARP();
                             P[u] = p;
-                            __syncwarp();
+                            DBP_SYNCWARP();
                             float2 pv[UP];
                             read_vec<UP>(P, pv);
                             float2 w = make_float2(0.f, 0.f);                            // lines 9-11: w = G p
@@ -425,7 +426,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                     }
                 }
                 qn = 0;
-                __syncthreads();                        // queue slots reused
+                DBP_SYNCTHREADS();                        // queue slots reused
                 continue;
             }
         }
@@ -458,7 +459,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
 #pragma unroll
                 for (int m = 0; m < R; ++m) Wp[warp * UP + row[m]] = ps[m];
             }
-            __syncthreads();
+            DBP_SYNCTHREADS();
             if (!a.xc.on) {
                 if (tid < NPC * UP) {
                     const int jj = tid / UP, u = tid - jj * UP;
@@ -489,7 +490,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                     Sv[tid] = do_prox ? prox(sum, a.px) : sum;
                 }
             }
-            __syncthreads();
+            DBP_SYNCTHREADS();
 #pragma unroll
             for (int m = 0; m < R; ++m) out[m] = Sv[j * UP + row[m]];
         };
@@ -569,10 +570,10 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
             float2 rv[R];
             fold_mv<UP>(A, qv, rv, pl, ybuf, row, l);                             // r = B^{-1} q
             // publish r for the pair; every lane takes all UP entries
-            __syncwarp();
+            DBP_SYNCWARP();
 #pragma unroll
             for (int m = 0; m < R; ++m) pl[row[m]] = rv[m];
-            __syncwarp();
+            DBP_SYNCWARP();
             if constexpr (Z::TC) {
                 dl_output_tc(pl - q * F::PLP, F::PLP, n);
             } else if (!DBP_EXP_NO_DLOUT) {

@@ -38,6 +38,7 @@ namespace dbp {
 template <int UP>
 __global__ void __launch_bounds__(512, UP <= 16 ? 2 : 1) k_admm_gj(UlArgs a) {   // 2 CTAs/SM at <= 64 registers (no spills)
     extern __shared__ __align__(16) float2 sm[];
+    DBP_POISON_SMEM(sm);
     const int C = a.C_loc, NT = a.NT;
     float2* pbuf = sm;                                  // [NT*C][UP] per-pair line
     float2* W = pbuf + (size_t)NT * C * UP;             // [NT][C][UP]
@@ -68,12 +69,12 @@ __global__ void __launch_bounds__(512, UP <= 16 ? 2 : 1) k_admm_gj(UlArgs a) {  
                 w = c_add(z, lam);                                   // line 17
             }
             W[((size_t)nl * C + c) * UP + i] = valid ? w : make_float2(0.f, 0.f);
-            __syncthreads();
+            DBP_SYNCTHREADS();
             if (tid < NT * UP) {                                     // line 18 (consensus) + 19 (prox)
                 const int el = tid / UP, uu = tid % UP;
                 Sv[el * UP + uu] = prox(cluster_sum(W, C, UP, el, uu), a.px);
             }
-            __syncthreads();
+            DBP_SYNCTHREADS();
         }
         if (tid < NT * UP) {
             const int el = tid / UP, uu = tid % UP;
@@ -84,7 +85,7 @@ __global__ void __launch_bounds__(512, UP <= 16 ? 2 : 1) k_admm_gj(UlArgs a) {  
                 if (a.hard) a.hard[((size_t)nn * a.J + jj) * a.U + uu] = slice_bits(s, a.md);
             }
         }
-        __syncthreads();
+        DBP_SYNCTHREADS();
     }
 }
 
@@ -120,14 +121,14 @@ __device__ __forceinline__ void warp_tri_row(float2* tb, const float2* __restric
                                              int q0, int CCH, int lane, int qi, int i, float2 (&R)[UP]) {
     constexpr int WB = 32 / UP * tri(UP);
     const int k = c0 / CCH;
-    __syncwarp();                                        // the buffer about to be refilled was read a chunk ago
+    DBP_SYNCWARP();                                        // the buffer about to be refilled was read a chunk ago
     if (c0 + CCH < C) {
         warp_tri_copy<UP>(tb + ((k + 1) & 1) * WB, Gp, C, N, c0 + CCH, n0, q0, CCH, lane);
         cp_async_wait_1();
     } else {
         cp_async_wait_all();
     }
-    __syncwarp();
+    DBP_SYNCWARP();
     load_herm_row_s<UP>(tb + (k & 1) * WB + qi * tri(UP), i, R);
 }
 
@@ -142,6 +143,7 @@ __device__ __forceinline__ void warp_tri_row(float2* tb, const float2* __restric
 template <int UP>
 __global__ void __launch_bounds__(256) k_admm_it(UlArgs a, int CCH) {   // split_cfg: <= 256 threads
     extern __shared__ __align__(16) float2 sm[];
+    DBP_POISON_SMEM(sm);
     const int C = a.C_loc, NT = a.NT, J = a.J;
     float2* pbuf = sm;                                  // [NT*CCH][UP]
     float2* Wp = pbuf + (size_t)NT * CCH * UP;          // [NT][J][CCH][UP] per-slot partial sums
@@ -164,7 +166,7 @@ __global__ void __launch_bounds__(256) k_admm_it(UlArgs a, int CCH) {   // split
     }
     float2* wp = Wp + ((size_t)nl * J * CCH + cl) * UP + i;   // this lane's slot, symbol stride CCH * UP
     for (int jj = 0; jj < J; ++jj) wp[(size_t)jj * CCH * UP] = make_float2(0.f, 0.f);
-    __syncthreads();
+    DBP_SYNCTHREADS();
     for (int c0 = 0; c0 < C; c0 += CCH) {
         const int c = c0 + cl;
         const bool valid = n < a.N && c < C;
@@ -197,7 +199,7 @@ __global__ void __launch_bounds__(256) k_admm_it(UlArgs a, int CCH) {   // split
             }
         }
     }
-    __syncthreads();
+    DBP_SYNCTHREADS();
     for (int e = tid; e < NT * J * UP; e += blockDim.x)      // e = (el J + jj) UP + u
         if (n0 + e / (J * UP) < a.N) a.wbuf[(size_t)n0 * J * UP + e] = cluster_sum(Wp, CCH, UP, e / UP, e % UP);
 }
@@ -210,7 +212,7 @@ template <int UP>
 __device__ __forceinline__ void bf_output(const float2* __restrict__ Hd, float2* buf, int i, float2 ri, int U, int S,
                                           float2* __restrict__ xo, bool valid) {
     buf[i] = ri;
-    __syncwarp();
+    DBP_SYNCWARP();
     // UP = 32: r_u by broadcast LDS (a register copy of r next to the caller's row spills)
     constexpr bool RR = UP <= DBP_BFOUT_REG_MAX_UP;
     float2 r[RR ? UP : 1];
@@ -222,7 +224,7 @@ __device__ __forceinline__ void bf_output(const float2* __restrict__ Hd, float2*
             if (u < U) c_fmac(acc, __ldg(Hd + (size_t)u * S + s), RR ? r[RR ? u : 0] : buf[u]);
         if (valid) xo[s] = acc;
     }
-    __syncwarp();
+    DBP_SYNCWARP();
 }
 
 // Fused (world == 1): B^{-1} in registers; init, T-1 consensus iterations of
@@ -233,6 +235,7 @@ __device__ __forceinline__ void bf_output(const float2* __restrict__ Hd, float2*
 template <int UP, int MINB>
 __global__ void __launch_bounds__(512, MINB) k_bf_gj(DlArgs a) {
     extern __shared__ __align__(16) float2 sm[];
+    DBP_POISON_SMEM(sm);
     const int C = a.C_loc, NT = a.NT;
     float2* pbuf = sm;
     float2* W = pbuf + (size_t)NT * C * UP;
@@ -266,15 +269,15 @@ __global__ void __launch_bounds__(512, MINB) k_bf_gj(DlArgs a) {
             const float2 m = c_sub(qv, c_scale(bq, a.rho_inv));          // line 11 (m-form)
             const float2 w = c_sub(m, lam);                              // line 12
             W[((size_t)nl * C + c) * UP + i] = valid ? w : make_float2(0.f, 0.f);
-            __syncthreads();
+            DBP_SYNCTHREADS();
             if (tid < NT * UP) Ws[tid] = cluster_sum(W, C, UP, tid / UP, tid % UP);   // line 13
-            __syncthreads();
+            DBP_SYNCTHREADS();
             const float2 d = c_sub(sv, Ws[nl * UP + i]);
             const float f = lemma2_scale(group_sum<UP>(c_norm2(d)), a.eps, a.inv_c);
             const float2 z = c_add(w, c_scale(d, f));                                // line 14 (Lemma 2)
             lam = c_sub(lam, c_scale(c_sub(m, z), a.gamma));                         // line 15
             qv = c_add(z, lam);
-            __syncthreads();
+            DBP_SYNCTHREADS();
         }
         const float2 r = row_apply<UP>(R, buf, i, qv);                  // B^{-1} q
         if (a.J == 1) {
@@ -287,7 +290,7 @@ __global__ void __launch_bounds__(512, MINB) k_bf_gj(DlArgs a) {
     if (a.J > 1) {
         // x_c[j] = H_c^H r_j for every symbol j from ONE pass over H_c: lane i takes antennas
         // i, i+UP, ..., loads the antenna's column of H_c once and reuses it for all J symbols
-        __syncwarp();
+        DBP_SYNCWARP();
         const float2* Hp = a.Hd + pair * (size_t)a.U * a.S;
         const float2* rp = a.m + pair * a.J * UP;
         for (int s = i; s < a.S; s += UP) {
@@ -310,6 +313,7 @@ __global__ void __launch_bounds__(512, MINB) k_bf_gj(DlArgs a) {
 template <int UP>
 __global__ void __launch_bounds__(256, UP >= 32 ? 2 : 3) k_bf_it(DlArgs a, int CCH) {   // split_cfg: <= 256 threads
     extern __shared__ __align__(16) float2 sm[];
+    DBP_POISON_SMEM(sm);
     const int C = a.C_loc, NT = a.NT, J = a.J;
     float2* pbuf = sm;                                  // [NT*CCH][UP]
     float2* Wp = pbuf + (size_t)NT * CCH * UP;          // [NT][J][CCH][UP] per-slot partial sums
@@ -343,7 +347,7 @@ __global__ void __launch_bounds__(256, UP >= 32 ? 2 : 3) k_bf_it(DlArgs a, int C
     }
     float2* wp = Wp + ((size_t)nl * J * CCH + cl) * UP + i;   // this lane's slot, symbol stride CCH * UP
     for (int jj = 0; jj < J; ++jj) wp[(size_t)jj * CCH * UP] = make_float2(0.f, 0.f);
-    __syncthreads();
+    DBP_SYNCTHREADS();
     for (int c0 = 0; c0 < C; c0 += CCH) {
         const int c = c0 + cl;
         const bool valid = n < a.N && c < C;
@@ -382,7 +386,7 @@ __global__ void __launch_bounds__(256, UP >= 32 ? 2 : 3) k_bf_it(DlArgs a, int C
         }
     }
     if (fin) return;
-    __syncthreads();
+    DBP_SYNCTHREADS();
     for (int e = tid; e < NT * J * UP; e += blockDim.x)      // e = (el J + jj) UP + u
         if (n0 + e / (J * UP) < a.N) a.wbuf[(size_t)n0 * J * UP + e] = cluster_sum(Wp, CCH, UP, e / UP, e % UP);
 }

@@ -66,6 +66,7 @@ __global__ void k_cg_gsum(const float2* __restrict__ Gp, const float2* __restric
 template <int UP, bool FUSED>
 __global__ void k_cg_it(CgArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    DBP_POISON_SMEM(smem_raw);
     constexpr int GPB = 256 / UP;                      // (n, j) groups per CTA
     float2* Gs = reinterpret_cast<float2*>(smem_raw);  // [GPB][tri]
     float2* Ps = Gs + (size_t)GPB * tri(UP);           // [GPB][UP]
@@ -96,9 +97,9 @@ __global__ void k_cg_it(CgArgs a) {
     }
     const int iters = FUSED ? a.T : (a.step < a.T ? 1 : 0);
     for (int it = 0; it < iters; ++it) {
-        __syncwarp();
+        DBP_SYNCWARP();
         P[u] = p;
-        __syncwarp();
+        DBP_SYNCWARP();
         float2 w = herm_mv_row<UP>(G, P, u);               // lines 9-11, w = G p
         if (FUSED) cg_update<UP>(x, r, p, rr, w, a.rho);
         else if (valid) a.wbuf[o] = w;

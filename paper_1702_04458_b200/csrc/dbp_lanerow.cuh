@@ -61,7 +61,7 @@ __device__ __forceinline__ bool gj_invert(float2 (&r)[UP], float2* prow, int i) 
 #pragma unroll
             for (int q = 0; q < UP / 2; ++q) p[q] = make_float4(r[2 * q].x, r[2 * q].y, r[2 * q + 1].x, r[2 * q + 1].y);
         }
-        __syncwarp();
+        DBP_SYNCWARP();
         float2 pr[UP];
         read_vec<UP>(prow, pr);
         // pivot (real and positive for HPD input), then one divergence-free
@@ -82,7 +82,7 @@ __device__ __forceinline__ bool gj_invert(float2 (&r)[UP], float2* prow, int i) 
             r[j].y = fmaf(-fs.x, pr[j].y, fmaf(-fs.y, pr[j].x, m * r[j].y));
         }
         r[k] = make_float2(-fs.x, -fs.y);
-        __syncwarp();
+        DBP_SYNCWARP();
     }
     return ok;
 }
@@ -91,13 +91,13 @@ __device__ __forceinline__ bool gj_invert(float2 (&r)[UP], float2* prow, int i) 
 template <int UP>
 __device__ __forceinline__ float2 row_apply(const float2 (&R)[UP], float2* buf, int i, float2 vi) {
     buf[i] = vi;
-    __syncwarp();
+    DBP_SYNCWARP();
     float2 v[UP];
     read_vec<UP>(buf, v);
     float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
     for (int j = 0; j < UP; ++j) c_fma(acc, R[j], v[j]);
-    __syncwarp();
+    DBP_SYNCWARP();
     return acc;
 }
 

@@ -82,6 +82,7 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
     // MODE 0 Gram + b, 1 inverse + y^reg, 2 inverse (DL), 4 Gram only (UL, N_sym > 1), 5 inverse only (UL)
     constexpr bool MF = !DL && (MODE == 0 || MODE == 1), INV = MODE == 1 || MODE == 2 || MODE == 5;
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    DBP_POISON_SMEM(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw) + warp * NST;
     unsigned char* wbase = smem_raw + 128 + (size_t)warp * Q::WREG;
@@ -120,7 +121,7 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
         for (int s = 0; s < NST; ++s) mbar_init(&bar[s], 1);
         fence_mbar_init();
     }
-    __syncwarp();
+    DBP_SYNCWARP();
     if (lane == 0)
         for (int s = 0; s < NST && s < nseq; ++s) issue(s);
 
@@ -142,7 +143,7 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
             const float2* stage = reinterpret_cast<const float2*>(wbase + st * G::STG);
             if (DL) fold_gram_dl<UP>(A, stage, q, row);
             else fold_gram_ul<UP, MF>(A, E, stage, q, row);
-            __syncwarp();
+            DBP_SYNCWARP();
             if (lane == 0 && sq + NST < nseq) {
                 fence_proxy_async();
                 issue(st);

@@ -72,6 +72,7 @@ k_prelr(const __grid_constant__ CUtensorMap tmH, LrArgs a) {
     constexpr int PPC = C::PPC, NST = C::NST, TRI = tri(UP);
     constexpr bool UL = !DL;
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    DBP_POISON_SMEM(smem_raw);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
     int* done = reinterpret_cast<int*>(smem_raw + 32);
     const int S = a.S, U = a.U, J = a.J;
@@ -111,7 +112,7 @@ k_prelr(const __grid_constant__ CUtensorMap tmH, LrArgs a) {
         for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); done[s] = 0; }
         fence_mbar_init();
     }
-    __syncthreads();
+    DBP_SYNCTHREADS();
     if (bulk && tid == 0)
         for (int s = 0; s < NST && s < nitems; ++s) issue(s, s);
 
@@ -124,7 +125,7 @@ k_prelr(const __grid_constant__ CUtensorMap tmH, LrArgs a) {
         if (bulk) {
             mbar_wait(&full[st], (uint32_t)((it / NST) & 1));
         } else {
-            __syncthreads();
+            DBP_SYNCTHREADS();
             float2* hw = const_cast<float2*>(hsl);
             float2* yw = const_cast<float2*>(ysm);
             for (int k = 0; k < nv; ++k) {
@@ -139,7 +140,7 @@ k_prelr(const __grid_constant__ CUtensorMap tmH, LrArgs a) {
                     }
                 }
             }
-            __syncthreads();
+            DBP_SYNCTHREADS();
         }
         const bool valid = q < nv;
         const long p = p0 + (valid ? q : 0);
@@ -193,7 +194,7 @@ k_prelr(const __grid_constant__ CUtensorMap tmH, LrArgs a) {
         }
         // stage consumed: release it (the last warp re-arms it for the group NST ahead)
         if (bulk) {
-            __syncwarp();
+            DBP_SYNCWARP();
             if (lane == 0 && atomicAdd(&done[st], 1) == C::THREADS / 32 - 1) {
                 done[st] = 0;
                 if (it + NST < nitems) {

@@ -289,7 +289,7 @@ __device__ __forceinline__ void tc16_gram_pair(const unsigned char* stage, int n
     }
     // G = Z + Z^H through the scratch (row stride 17: the transposed reads are 2-way at most)
     const float us = __int_as_float((127 + 2 * ex) << 23);                // 2^(2 ex)
-    __syncwarp();
+    DBP_SYNCWARP();
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -297,7 +297,7 @@ __device__ __forceinline__ void tc16_gram_pair(const unsigned char* stage, int n
 #pragma unroll
             for (int cc = 0; cc < 2; ++cc)
                 zs[(g + 8 * e1) * 17 + 8 * h + 2 * t + cc] = make_float2(acc[h][2 * e1 + cc], acc[2 + h][2 * e1 + cc]);
-    __syncwarp();
+    DBP_SYNCWARP();
     const float sg = DL ? -1.f : 1.f;                                     // DL: B = H H^H = conj(UL form)
 #pragma unroll
     for (int h = 0; h < 2; ++h)

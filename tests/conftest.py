@@ -29,3 +29,6 @@ def pytest_terminal_summary(terminalreporter):
         terminalreporter.write_line(
             f"parity worst: rel-L2 {worst['rel_l2']:.3e}, max per-subcarrier rel-L2 {worst['max_subcarrier']:.3e} "
             f"(bar 1e-4)")
+    dbp = sys.modules.get("paper_1702_04458_b200.dbp")
+    if dbp is not None and getattr(dbp, "_lib", None) is not None:
+        terminalreporter.write_line(f"libdbp loaded from {dbp.LIB_PATH}")
