@@ -120,7 +120,16 @@ typedef enum {
      * NCCL path on every rank (the decision depends only on the dims).  Round ids are consecutive
      * within and across calls (ADMM-UL T, CG-UL T + 1, ADMM-DL T - 1 rounds).
      * Unverified across GPUs (single-GPU environment). */
-    DBP_OPT_DEVICE_CONSENSUS = 4
+    DBP_OPT_DEVICE_CONSENSUS = 4,
+    /* Per-cluster inverse of Alg. 1 / Alg. 3 (P275-280, P290, P482-488, P500).  0 (default): the
+     * paper's choice made strict -- S < U uses the S x S form (A_c = H_c H_c^H + rho I_S uplink,
+     * A_c = H_c^H H_c + rho^{-1} I_S downlink; three mat-vecs per round), S >= U the U x U form
+     * (B_c; at S == U the two have equal size and U x U needs one mat-vec per round, Table I).
+     * 1: always U x U.  2: always S x S (S <= 32).  The two forms give the same iterates up to
+     * rounding (Woodbury).  The S x S form runs on one warp per cluster pair with one launch per
+     * consensus round (and the NCCL allreduce in between at world > 1); it affects the workspace
+     * size, so set it before dbp_workspace_bytes.  CG (Alg. 2) has a single form. */
+    DBP_OPT_MODE = 5
 } dbp_option;
 
 /* Per-kernel device time accumulated under DBP_OPT_KERNEL_TIMING. */

@@ -26,6 +26,7 @@ struct dbp_ctx {
     int64_t allreduce_calls = 0, allreduce_bytes = 0, consensus_rounds = 0;
     int force_split = 0;
     int no_fused = 0;
+    int mode = 0;                // DBP_OPT_MODE: 0 paper rule (S < U -> S x S), 1 U x U, 2 S x S
     // device-side consensus (DBP_OPT_DEVICE_CONSENSUS): symmetric buffer, peer mappings
     int xcons = 0;
     void* xbuf = nullptr;
@@ -157,6 +158,11 @@ extern "C" dbp_status dbp_set_option(dbp_ctx* c, int option, int64_t value) {
     if (option == DBP_OPT_FORCE_SPLIT) { c->force_split = value ? 1 : 0; return DBP_OK; }
     if (option == DBP_OPT_KERNEL_TIMING) { c->timing = value ? 1 : 0; return DBP_OK; }
     if (option == DBP_OPT_NO_FUSED) { c->no_fused = value ? 1 : 0; return DBP_OK; }
+    if (option == DBP_OPT_MODE) {
+        if (value < 0 || value > 2) return fail(DBP_ERR_INVALID_ARG, "mode %lld (0 auto, 1 UxU, 2 SxS)", (long long)value);
+        c->mode = (int)value;
+        return DBP_OK;
+    }
     if (option == DBP_OPT_DEVICE_CONSENSUS) {
         if (value < 0 || value > 2) return fail(DBP_ERR_INVALID_ARG, "device consensus mode %lld", (long long)value);
         if (value && c->world > 8) return fail(DBP_ERR_UNSUPPORTED, "device consensus supports world <= 8");
@@ -190,6 +196,7 @@ extern "C" dbp_status dbp_get_comm_info(const dbp_ctx* c, int* nranks, int* rank
 // ----------------------------------------------------------------- shapes
 struct Shape {
     int C, C_loc, S, U, UP, N, J;
+    int ss, SP;                  // S x S form (DBP_OPT_MODE) and S padded to 4/8/16/32
     long pairs() const { return (long)C_loc * N; }
 };
 
@@ -209,6 +216,9 @@ static dbp_status check_dims(const dbp_ctx* c, const dbp_dims* d, Shape* sh) {
     sh->UP = pad_users(d->U);
     sh->N = d->N;
     sh->J = d->N_sym;
+    sh->ss = c->mode == 2 || (c->mode == 0 && d->S < d->U);
+    sh->SP = pad_users(d->S);
+    if (sh->ss && d->S > 32) return fail(DBP_ERR_UNSUPPORTED, "the S x S form supports S <= 32 (got S=%d)", d->S);
     if ((long)sh->C_loc * sh->N > (1L << 31) - 1) return fail(DBP_ERR_UNSUPPORTED, "too many pairs");
     return DBP_OK;
 }
@@ -220,7 +230,8 @@ struct Layout {
 };
 
 static Layout layout(const Shape& sh, int algo) {
-    const size_t T = (size_t)sh.UP * (sh.UP + 1) / 2;
+    // per-pair packed inverse: U x U, or the S x S form's A_c^{-1} (the larger of the two when forced)
+    const size_t T = std::max((size_t)sh.UP * (sh.UP + 1) / 2, sh.ss ? (size_t)sh.SP * (sh.SP + 1) / 2 : (size_t)0);
     const size_t P = (size_t)sh.pairs();
     const size_t vecp = P * sh.J * sh.UP * 8;      // per pair per symbol vectors
     const size_t vecn = (size_t)sh.N * sh.J * sh.UP * 8;
@@ -494,6 +505,31 @@ extern "C" dbp_status dbp_detect_admm(dbp_ctx* c, const dbp_dims* d, const dbp_c
     float2* mf = reinterpret_cast<float2*>(k.ws + Lw.off[1]);
     LaunchCtx L{s, c->d_flag, &c->launches};
 
+    if (sh.ss) {
+        // S x S form (Alg. 1 lines 3-5, 13; eq. (4)): A_c^{-1}, y^reg = H^H A^{-1} y, then one launch
+        // per round with the allreduce in between (T rounds), s_hat = prox of the last sum
+        SsArgs a{};
+        a.H = dH; a.y = dy;
+        a.Ainv = G;
+        a.yreg = reinterpret_cast<float2*>(k.ws + Lw.off[2]);
+        a.lam = reinterpret_cast<float2*>(k.ws + Lw.off[3]);
+        a.st = reinterpret_cast<float2*>(k.ws + Lw.off[4]);
+        a.wbuf = reinterpret_cast<float2*>(k.ws + Lw.off[5]);
+        a.flag = c->d_flag;
+        a.C_loc = sh.C_loc; a.N = sh.N; a.J = sh.J; a.S = sh.S; a.U = sh.U; a.UPW = sh.UP; a.T = T;
+        a.delta = rho; a.rho = rho; a.gamma = gamma;
+        a.px = make_prox(reg, mod, sh.C, rho, N0, Es);
+        KT("pre_ss_ul", launch_ss_pre(L, false, a));
+        const size_t nw = (size_t)sh.N * sh.J * sh.UP;
+        for (int t = 1; t <= T; ++t) {
+            a.step = t;
+            KT("ss_ul_step", launch_ss_it(L, false, a));                          // lines 12-17 (t = 1: 10)
+            if ((st = allreduce(c, a.wbuf, nw, s))) return st;                  // line 18 consensus
+        }
+        KT("prox_out", launch_prox_out(L, sh.UP, a.wbuf, sh.N, sh.J, sh.U, a.px, modem_of(mod),
+                                       static_cast<float2*>(k.io[2].dev), static_cast<uint8_t*>(k.io[3].dev)));
+        return end_call(c, k, s);
+    }
     const bool xc_on = xcons_active(c) && T < 250;
     if ((c->world == 1 || xc_on) && !c->force_split && !c->no_fused &&
         fused_ok(sh.UP, sh.C_loc, sh.N, sh.J, sh.S, sh.U)) {
@@ -675,6 +711,28 @@ extern "C" dbp_status dbp_beamform_admm(dbp_ctx* c, const dbp_dims* d, const dbp
     a.inv_c = (float)(1.0 / sh.C);
     a.eps = eps;
 
+    if (sh.ss) {
+        // S x S form (Alg. 3 lines 3-4, 9, 17): A_c^{-1} = (H_c^H H_c + rho^{-1} I_S)^{-1}; one launch per
+        // round, T - 1 allreduces (the first iteration is local, P811)
+        SsArgs b{};
+        b.H = a.Hd; b.s = a.s; b.x = a.x;
+        b.Ainv = G;
+        b.st = a.m; b.lam = a.lam; b.wbuf = a.wbuf;
+        b.flag = c->d_flag;
+        b.C_loc = sh.C_loc; b.N = sh.N; b.J = sh.J; b.S = sh.S; b.U = sh.U; b.UPW = sh.UP; b.T = T;
+        b.delta = a.rho_inv; b.gamma = gamma; b.a0 = a.a0; b.inv_c = a.inv_c; b.eps = eps;
+        KT("pre_ss_dl", launch_ss_pre(L, true, b));
+        const size_t nw = (size_t)sh.N * sh.J * sh.UP;
+        b.step = 0;
+        KT("ss_dl_step", launch_ss_it(L, true, b));                                // lines 8-9 (+ 11-12)
+        if (T > 1 && (st = allreduce(c, b.wbuf, nw, s))) return st;
+        for (int t = 2; t <= T; ++t) {
+            b.step = t;
+            KT("ss_dl_step", launch_ss_it(L, true, b));                            // lines 14-17 (+ 11-12)
+            if (t < T && (st = allreduce(c, b.wbuf, nw, s))) return st;          // line 13 consensus
+        }
+        return end_call(c, k, s);
+    }
     const bool xc_on = xcons_active(c) && T < 250;
     if ((c->world == 1 || xc_on) && !c->force_split && !c->no_fused &&
         fused_ok(sh.UP, sh.C_loc, sh.N, sh.J, sh.S, sh.U)) {

@@ -136,4 +136,24 @@ cudaError_t launch_zf_out(const LaunchCtx& L, int UP, const float2* Hd, const fl
                           long npairs, float2* x);
 cudaError_t launch_bf_it(const LaunchCtx& L, int UP, DlArgs a, int CCH);
 
+// S x S forms of Alg. 1 / Alg. 3 (dbp_ss.cu, NEXT-2): one warp per pair, one launch per round
+struct SsArgs {
+    const float2* H;      // UL [C_loc][N][S][U]; DL [C_loc][N][U][S]
+    const float2* y;      // UL [C_loc][N][J][S]
+    const float2* s;      // DL [N][J][U]
+    float2* Ainv;         // [C_loc][N][tri(SP)]
+    float2* yreg;         // UL [C_loc][N][J][UPW]
+    float2* lam;          // [C_loc][N][J][UPW]
+    float2* st;           // UL: z; DL: m   [C_loc][N][J][UPW]
+    float2* wbuf;         // [N][J][UPW] consensus partial sums (UPW = the API's UP)
+    float2* x;            // DL output [C_loc][N][J][S]
+    int* flag;
+    int C_loc, N, J, S, U, UPW, T, step;   // step: UL 1..T; DL 0 = init, t = 2..T
+    float delta, rho, gamma, a0, inv_c, eps;
+    Prox px;
+};
+
+cudaError_t launch_ss_pre(const LaunchCtx& L, bool dl, SsArgs a);
+cudaError_t launch_ss_it(const LaunchCtx& L, bool dl, SsArgs a);
+
 }  // namespace dbp

@@ -592,3 +592,76 @@ def test_empty_frame(env, host):
     with pytest.raises(dbp.DbpError) as ei:
         dbp.detect_admm(ctx, H, y, rho=0.0, mod="qpsk")
     assert ei.value.status == 1
+
+
+# ---------------------------------------------------------------- S x S forms (NEXT-2)
+SS_SHAPES = [
+    synth.Config("s<u", "admm_ul", C=4, S=4, U=12, N=6, mod="qpsk", snr_db=15),
+    synth.Config("s<u-b", "admm_ul", C=6, S=8, U=16, N=13, mod="qam16", snr_db=20),
+    synth.Config("s<u-odd", "admm_ul", C=3, S=5, U=9, N=7, N_sym=3, mod="qam64", snr_db=25),
+    synth.Config("s>u", "admm_ul", C=2, S=16, U=4, N=16, mod="qpsk", snr_db=10),        # forced S x S
+    synth.Config("s32", "admm_ul", C=4, S=32, U=16, N=9, mod="qam64", snr_db=25),       # forced, SP = 32
+]
+
+
+def set_mode(env, mode):
+    dbp, ctx = env[0], env[1]
+    ctx.set_option(dbp.OPT_MODE, mode)
+
+
+@pytest.mark.parametrize("cfg", SS_SHAPES, ids=lambda c: f"{c.name}-C{c.C}S{c.S}U{c.U}N{c.N}J{c.N_sym}")
+@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("reg,T", [("mmse", 5), ("mmse", 1), ("zf", 3), ("box", 4)])
+def test_admm_ss_mode(env, cfg, mode, reg, T):
+    """Alg. 1 with the S x S inverse (eq. (4), lines 3-5 and 13; P275-280, P290) against the oracle
+    (whose U x U and S x S forms agree to 1e-9): mode 0 = the paper's rule (S < U -> S x S),
+    1 = U x U, 2 = S x S forced."""
+    if mode == 0 and cfg.S >= cfg.U:
+        pytest.skip("auto mode picks U x U here (covered by the other tests)")
+    set_mode(env, mode)
+    try:
+        s, hard, s_ref, hard_ref = run_admm(env, cfg, "fused", reg=reg, T=T)
+    finally:
+        set_mode(env, 0)
+    assert rel(s, s_ref) < TOL
+    check_hard(hard, hard_ref, s_ref, cfg.mod)
+
+
+@pytest.mark.parametrize("cfg", [c.scaled(algo="admm_dl") for c in SS_SHAPES],
+                         ids=lambda c: f"{c.name}-C{c.C}S{c.S}U{c.U}N{c.N}J{c.N_sym}")
+@pytest.mark.parametrize("mode", [0, 2])
+@pytest.mark.parametrize("T,eps", [(5, 0.0), (1, 0.0), (2, 0.0), (4, 0.3)])
+def test_bf_ss_mode(env, cfg, mode, T, eps):
+    """Alg. 3 with A_c^{-1} = (H_c^H H_c + rho^{-1} I_S)^{-1} (lines 3-4, 9, 17; P480-488, P500),
+    Lemma 2 for eps > 0, against the oracle."""
+    if mode == 0 and cfg.S >= cfg.U:
+        pytest.skip("auto mode picks U x U here")
+    dbp, ctx, oracle, torch = env
+    Hd, s = synth.downlink_frame(cfg)
+    set_mode(env, mode)
+    try:
+        x = dbp.beamform_admm(ctx, torch.from_numpy(Hd).cuda(), torch.from_numpy(s).cuda(), rho=cfg.rho, T=T,
+                              eps=eps)
+        ctx.sync()
+    finally:
+        set_mode(env, 0)
+    x_ref = oracle.beamform_admm(Hd, s, rho=cfg.rho, T=T, eps=eps)
+    assert rel(x.cpu().numpy(), x_ref) < TOL
+
+
+def test_ss_round_counts(env):
+    """The S x S forms keep the paper's consensus counts: ADMM-UL T rounds, ADMM-DL T - 1."""
+    dbp, ctx, oracle, torch = env
+    cfg = SS_SHAPES[0]
+    H, y, _ = synth.uplink_frame(cfg)
+    Hd, s = synth.downlink_frame(cfg)
+    for T in (1, 3):
+        st0 = ctx.stats()
+        dbp.detect_admm(ctx, torch.from_numpy(H).cuda(), torch.from_numpy(y).cuda(), rho=1.0, N0=cfg.N0,
+                        mod=cfg.mod, T=T)
+        st1 = ctx.stats()
+        dbp.beamform_admm(ctx, torch.from_numpy(Hd).cuda(), torch.from_numpy(s).cuda(), rho=1.0, T=T)
+        st2 = ctx.stats()
+        ctx.sync()
+        assert st1["consensus_rounds"] - st0["consensus_rounds"] == T
+        assert st2["consensus_rounds"] - st1["consensus_rounds"] == T - 1
