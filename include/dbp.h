@@ -89,6 +89,7 @@ typedef struct {
     int64_t kernel_launches;   /* libdbp kernels enqueued                              */
     int64_t consensus_rounds;  /* algorithmic consensus rounds: ADMM-UL T, CG T+1,
                                   ADMM-DL T-1 per call (SPEC S389-390), any world     */
+    int64_t graph_replays;     /* schedules replayed from a cached CUDA graph (DBP_OPT_GRAPHS) */
 } dbp_stats;
 
 /* Options for dbp_set_option(). */
@@ -129,7 +130,13 @@ typedef enum {
      * rounding (Woodbury).  The S x S form runs on one warp per cluster pair with one launch per
      * consensus round (and the NCCL allreduce in between at world > 1); it affects the workspace
      * size, so set it before dbp_workspace_bytes.  CG (Alg. 2) has a single form. */
-    DBP_OPT_MODE = 5
+    DBP_OPT_MODE = 5,
+    /* 1 (default): the multi-launch schedules (per-pair preprocessing, the per-round kernels and
+     * the NCCL allreduces between them -- the world > 1 path, or FORCE_SPLIT / NO_FUSED) are
+     * captured into a CUDA graph on first use and replayed while the call's dims, scalars and
+     * device pointers repeat (host-pointer calls and KERNEL_TIMING never use graphs).  0: plain
+     * launches.  Results are identical either way. */
+    DBP_OPT_GRAPHS = 6
 } dbp_option;
 
 /* Per-kernel device time accumulated under DBP_OPT_KERNEL_TIMING. */

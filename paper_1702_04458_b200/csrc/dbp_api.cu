@@ -27,6 +27,18 @@ struct dbp_ctx {
     int force_split = 0;
     int no_fused = 0;
     int mode = 0;                // DBP_OPT_MODE: 0 paper rule (S < U -> S x S), 1 U x U, 2 S x S
+    // CUDA graphs of the multi-launch schedules (DBP_OPT_GRAPHS): key -> instantiated graph
+    int graphs = 1;
+    cudaStream_t cap = nullptr;
+    struct GraphEnt {
+        std::vector<uint64_t> key;
+        cudaGraphExec_t exec;
+        int64_t launches, ar_calls, ar_bytes, rounds;
+        uint64_t used;
+    };
+    std::vector<GraphEnt> gcache;
+    uint64_t gclock = 0;
+    int64_t graph_replays = 0;
     // device-side consensus (DBP_OPT_DEVICE_CONSENSUS): symmetric buffer, peer mappings
     int xcons = 0;
     void* xbuf = nullptr;
@@ -147,6 +159,8 @@ extern "C" dbp_status dbp_ctx_destroy(dbp_ctx* c) {
     cudaFree(c->d_flag);
     if (c->stage) cudaFree(c->stage);
     if (c->iws) cudaFree(c->iws);
+    for (auto& g : c->gcache) cudaGraphExecDestroy(g.exec);
+    if (c->cap) cudaStreamDestroy(c->cap);
     for (auto& p : c->pending) { cudaEventDestroy(p.e0); cudaEventDestroy(p.e1); }
     for (auto e : c->pool) cudaEventDestroy(e);
     delete c;
@@ -158,6 +172,7 @@ extern "C" dbp_status dbp_set_option(dbp_ctx* c, int option, int64_t value) {
     if (option == DBP_OPT_FORCE_SPLIT) { c->force_split = value ? 1 : 0; return DBP_OK; }
     if (option == DBP_OPT_KERNEL_TIMING) { c->timing = value ? 1 : 0; return DBP_OK; }
     if (option == DBP_OPT_NO_FUSED) { c->no_fused = value ? 1 : 0; return DBP_OK; }
+    if (option == DBP_OPT_GRAPHS) { c->graphs = value ? 1 : 0; return DBP_OK; }
     if (option == DBP_OPT_MODE) {
         if (value < 0 || value > 2) return fail(DBP_ERR_INVALID_ARG, "mode %lld (0 auto, 1 UxU, 2 SxS)", (long long)value);
         c->mode = (int)value;
@@ -178,6 +193,7 @@ extern "C" dbp_status dbp_get_stats(const dbp_ctx* c, dbp_stats* s) {
     s->allreduce_bytes = c->allreduce_bytes;
     s->kernel_launches = c->launches;
     s->consensus_rounds = c->consensus_rounds;
+    s->graph_replays = c->graph_replays;
     return DBP_OK;
 }
 
@@ -375,6 +391,60 @@ static dbp_status allreduce(dbp_ctx* c, float2* buf, size_t nfloat2, cudaStream_
     return DBP_OK;
 }
 
+// Multi-launch schedules (preprocessing + per-round kernels + the NCCL allreduces between them)
+// are captured once per (solver, shape, scalars, pointers) into a CUDA graph and replayed: one
+// cudaGraphLaunch instead of T + 2 kernel launches and T collectives issued from the host
+// (SURVEY 5 "capture the NCCL calls in a CUDA graph").  Capture runs on a library stream (the
+// caller's may be the legacy default stream, which cannot be captured); the graph is launched
+// on the caller's stream.  Not used for host-pointer calls (their staging is outside) or under
+// DBP_OPT_KERNEL_TIMING (per-kernel events).  Counters (launches, allreduces, rounds) advance on
+// every replay by the amounts the captured schedule issued.
+template <class F>
+static dbp_status graphed(dbp_ctx* c, bool host, cudaStream_t s, const std::vector<uint64_t>& key, F&& body) {
+    if (!c->graphs || host || c->timing) return body(s);
+    ++c->gclock;
+    for (auto& g : c->gcache) {
+        if (g.key != key) continue;
+        g.used = c->gclock;
+        CU(cudaGraphLaunch(g.exec, s));
+        c->launches += g.launches;
+        c->allreduce_calls += g.ar_calls;
+        c->allreduce_bytes += g.ar_bytes;
+        c->consensus_rounds += g.rounds;
+        ++c->graph_replays;
+        return DBP_OK;
+    }
+    if (!c->cap) CU(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
+    const int64_t l0 = c->launches, a0 = c->allreduce_calls, b0 = c->allreduce_bytes, r0 = c->consensus_rounds;
+    CU(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeRelaxed));
+    dbp_status st = body(c->cap);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(c->cap, &graph);
+    if (st || e != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        return st ? st : fail(DBP_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+    }
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) return fail(DBP_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ei));
+    if (c->gcache.size() >= 16) {                      // evict the least recently used
+        size_t v = 0;
+        for (size_t i = 1; i < c->gcache.size(); ++i)
+            if (c->gcache[i].used < c->gcache[v].used) v = i;
+        cudaGraphExecDestroy(c->gcache[v].exec);
+        c->gcache.erase(c->gcache.begin() + (long)v);
+    }
+    c->gcache.push_back({key, exec, c->launches - l0, c->allreduce_calls - a0, c->allreduce_bytes - b0,
+                         c->consensus_rounds - r0, c->gclock});
+    CU(cudaGraphLaunch(exec, s));
+    return DBP_OK;
+}
+
+static uint64_t fbits(float f) { uint32_t u; memcpy(&u, &f, 4); return u; }
+static uint64_t pbits(const void* p) { return reinterpret_cast<uintptr_t>(p); }
+
 #define KL(call)                                                                               \
     do {                                                                                       \
         cudaError_t e_ = (call);                                                               \
@@ -519,15 +589,24 @@ extern "C" dbp_status dbp_detect_admm(dbp_ctx* c, const dbp_dims* d, const dbp_c
         a.C_loc = sh.C_loc; a.N = sh.N; a.J = sh.J; a.S = sh.S; a.U = sh.U; a.UPW = sh.UP; a.T = T;
         a.delta = rho; a.rho = rho; a.gamma = gamma;
         a.px = make_prox(reg, mod, sh.C, rho, N0, Es);
-        KT("pre_ss_ul", launch_ss_pre(L, false, a));
-        const size_t nw = (size_t)sh.N * sh.J * sh.UP;
-        for (int t = 1; t <= T; ++t) {
-            a.step = t;
-            KT("ss_ul_step", launch_ss_it(L, false, a));                          // lines 12-17 (t = 1: 10)
-            if ((st = allreduce(c, a.wbuf, nw, s))) return st;                  // line 18 consensus
-        }
-        KT("prox_out", launch_prox_out(L, sh.UP, a.wbuf, sh.N, sh.J, sh.U, a.px, modem_of(mod),
-                                       static_cast<float2*>(k.io[2].dev), static_cast<uint8_t*>(k.io[3].dev)));
+        const std::vector<uint64_t> key{10, (uint64_t)sh.C, (uint64_t)sh.S, (uint64_t)sh.U, (uint64_t)sh.N, (uint64_t)sh.J, (uint64_t)T, (uint64_t)sh.ss, (uint64_t)c->force_split, (uint64_t)c->no_fused, (uint64_t)reg, (uint64_t)mod, fbits(rho), fbits(gamma),
+                                        fbits(N0), fbits(Es), pbits(dH), pbits(dy), pbits(k.io[2].dev),
+                                        pbits(k.io[3].dev), pbits(k.ws)};
+        st = graphed(c, k.host, s, key, [&](cudaStream_t s) -> dbp_status {
+            LaunchCtx L{s, c->d_flag, &c->launches};
+            dbp_status st;
+            KT("pre_ss_ul", launch_ss_pre(L, false, a));
+            const size_t nw = (size_t)sh.N * sh.J * sh.UP;
+            for (int t = 1; t <= T; ++t) {
+                a.step = t;
+                KT("ss_ul_step", launch_ss_it(L, false, a));                      // lines 12-17 (t = 1: 10)
+                if ((st = allreduce(c, a.wbuf, nw, s))) return st;              // line 18 consensus
+            }
+            KT("prox_out", launch_prox_out(L, sh.UP, a.wbuf, sh.N, sh.J, sh.U, a.px, modem_of(mod),
+                                           static_cast<float2*>(k.io[2].dev), static_cast<uint8_t*>(k.io[3].dev)));
+            return DBP_OK;
+        });
+        if (st) return st;
         return end_call(c, k, s);
     }
     const bool xc_on = xcons_active(c) && T < 250;
@@ -553,6 +632,12 @@ extern "C" dbp_status dbp_detect_admm(dbp_ctx* c, const dbp_dims* d, const dbp_c
         if (xc_on) return fail(DBP_ERR_CUDA, "fused ADMM-UL launch with device consensus failed (rank %d)", c->rank);
     }
     float2* yreg = reinterpret_cast<float2*>(k.ws + Lw.off[2]);
+    const std::vector<uint64_t> key{11, (uint64_t)sh.C, (uint64_t)sh.S, (uint64_t)sh.U, (uint64_t)sh.N, (uint64_t)sh.J, (uint64_t)T, (uint64_t)sh.ss, (uint64_t)c->force_split, (uint64_t)c->no_fused, (uint64_t)reg, (uint64_t)mod, fbits(rho), fbits(gamma), fbits(N0),
+                                    fbits(Es), pbits(dH), pbits(dy), pbits(k.io[2].dev), pbits(k.io[3].dev),
+                                    pbits(k.ws)};
+    st = graphed(c, k.host, s, key, [&](cudaStream_t s) -> dbp_status {
+    LaunchCtx L{s, c->d_flag, &c->launches};
+    dbp_status st;
     // a1-a3: G_c = H_c^H H_c + rho I, B_c^{-1} and y^reg = B_c^{-1} H_c^H y_c (Alg. 1 lines 7-8)
     KT("pre_ul", launch_prelr(L, sh.UP, 1, dH, dy, sh.S, sh.U, sh.J, sh.pairs(), rho, G, yreg));
 
@@ -586,6 +671,9 @@ extern "C" dbp_status dbp_detect_admm(dbp_ctx* c, const dbp_dims* d, const dbp_c
         }
         KT("prox_out", launch_prox_out(L, sh.UP, a.wbuf, sh.N, sh.J, sh.U, a.px, a.md, a.s_hat, a.hard));  // line 19
     }
+    return DBP_OK;
+    });
+    if (st) return st;
     return end_call(c, k, s);
 }
 
@@ -649,6 +737,11 @@ extern "C" dbp_status dbp_detect_cg(dbp_ctx* c, const dbp_dims* d, const dbp_cf3
         }
         if (xc_on) return fail(DBP_ERR_CUDA, "fused CG launch with device consensus failed (rank %d)", c->rank);
     }
+    const std::vector<uint64_t> key{12, (uint64_t)sh.C, (uint64_t)sh.S, (uint64_t)sh.U, (uint64_t)sh.N, (uint64_t)sh.J, (uint64_t)T, (uint64_t)sh.ss, (uint64_t)c->force_split, (uint64_t)c->no_fused, (uint64_t)mod, fbits(rho), pbits(k.io[0].dev), pbits(k.io[1].dev),
+                                    pbits(k.io[2].dev), pbits(k.io[3].dev), pbits(k.ws)};
+    st = graphed(c, k.host, s, key, [&](cudaStream_t s) -> dbp_status {
+    LaunchCtx L{s, c->d_flag, &c->launches};
+    dbp_status st;
     // b1: per-pair Gram H_c^H H_c and matched filter H_c^H y_c, then the
     // per-GPU sums (G_loc, local y^MRC) in fixed cluster order.
     KT("pre_cg", launch_prelr(L, sh.UP, 0, static_cast<const float2*>(k.io[0].dev),
@@ -666,6 +759,9 @@ extern "C" dbp_status dbp_detect_cg(dbp_ctx* c, const dbp_dims* d, const dbp_cf3
             if (t < T && (st = allreduce(c, a.wbuf, nw, s))) return st;   // line 11 consensus
         }
     }
+    return DBP_OK;
+    });
+    if (st) return st;
     return end_call(c, k, s);
 }
 
@@ -721,16 +817,24 @@ extern "C" dbp_status dbp_beamform_admm(dbp_ctx* c, const dbp_dims* d, const dbp
         b.flag = c->d_flag;
         b.C_loc = sh.C_loc; b.N = sh.N; b.J = sh.J; b.S = sh.S; b.U = sh.U; b.UPW = sh.UP; b.T = T;
         b.delta = a.rho_inv; b.gamma = gamma; b.a0 = a.a0; b.inv_c = a.inv_c; b.eps = eps;
-        KT("pre_ss_dl", launch_ss_pre(L, true, b));
-        const size_t nw = (size_t)sh.N * sh.J * sh.UP;
-        b.step = 0;
-        KT("ss_dl_step", launch_ss_it(L, true, b));                                // lines 8-9 (+ 11-12)
-        if (T > 1 && (st = allreduce(c, b.wbuf, nw, s))) return st;
-        for (int t = 2; t <= T; ++t) {
-            b.step = t;
-            KT("ss_dl_step", launch_ss_it(L, true, b));                            // lines 14-17 (+ 11-12)
-            if (t < T && (st = allreduce(c, b.wbuf, nw, s))) return st;          // line 13 consensus
-        }
+        const std::vector<uint64_t> key{13, (uint64_t)sh.C, (uint64_t)sh.S, (uint64_t)sh.U, (uint64_t)sh.N, (uint64_t)sh.J, (uint64_t)T, (uint64_t)sh.ss, (uint64_t)c->force_split, (uint64_t)c->no_fused, fbits(rho), fbits(gamma), fbits(eps), pbits(a.Hd), pbits(a.s),
+                                        pbits(a.x), pbits(k.ws)};
+        st = graphed(c, k.host, s, key, [&](cudaStream_t s) -> dbp_status {
+            LaunchCtx L{s, c->d_flag, &c->launches};
+            dbp_status st;
+            KT("pre_ss_dl", launch_ss_pre(L, true, b));
+            const size_t nw = (size_t)sh.N * sh.J * sh.UP;
+            b.step = 0;
+            KT("ss_dl_step", launch_ss_it(L, true, b));                            // lines 8-9 (+ 11-12)
+            if (T > 1 && (st = allreduce(c, b.wbuf, nw, s))) return st;
+            for (int t = 2; t <= T; ++t) {
+                b.step = t;
+                KT("ss_dl_step", launch_ss_it(L, true, b));                        // lines 14-17 (+ 11-12)
+                if (t < T && (st = allreduce(c, b.wbuf, nw, s))) return st;      // line 13 consensus
+            }
+            return DBP_OK;
+        });
+        if (st) return st;
         return end_call(c, k, s);
     }
     const bool xc_on = xcons_active(c) && T < 250;
@@ -753,6 +857,11 @@ extern "C" dbp_status dbp_beamform_admm(dbp_ctx* c, const dbp_dims* d, const dbp
         }
         if (xc_on) return fail(DBP_ERR_CUDA, "fused ADMM-DL launch with device consensus failed (rank %d)", c->rank);
     }
+    const std::vector<uint64_t> key{14, (uint64_t)sh.C, (uint64_t)sh.S, (uint64_t)sh.U, (uint64_t)sh.N, (uint64_t)sh.J, (uint64_t)T, (uint64_t)sh.ss, (uint64_t)c->force_split, (uint64_t)c->no_fused, fbits(rho), fbits(gamma), fbits(eps), pbits(a.Hd), pbits(a.s),
+                                    pbits(a.x), pbits(k.ws)};
+    st = graphed(c, k.host, s, key, [&](cudaStream_t s) -> dbp_status {
+    LaunchCtx L{s, c->d_flag, &c->launches};
+    dbp_status st;
     // c1: B_c = H_c H_c^H + rho^{-1} I_U and its inverse (Alg. 3 lines 5-6)
     KT("pre_dl", launch_prelr(L, sh.UP, 2, a.Hd, nullptr, sh.S, sh.U, sh.J, sh.pairs(), a.rho_inv, G, nullptr));
     int NT, CCH;
@@ -772,6 +881,9 @@ extern "C" dbp_status dbp_beamform_admm(dbp_ctx* c, const dbp_dims* d, const dbp
         a.step = T + 1;
         KT("bf_final", launch_bf_it(L, sh.UP, a, CCH));                    // output x_c^(T) (P525)
     }
+    return DBP_OK;
+    });
+    if (st) return st;
     return end_call(c, k, s);
 }
 

@@ -26,6 +26,7 @@ OPT_KERNEL_TIMING = 2
 OPT_NO_FUSED = 3
 OPT_DEVICE_CONSENSUS = 4
 OPT_MODE = 5
+OPT_GRAPHS = 6
 
 EXPORTS = ["dbp_get_unique_id", "dbp_ctx_create", "dbp_ctx_destroy", "dbp_set_option", "dbp_get_stats",
            "dbp_last_error", "dbp_workspace_bytes", "dbp_detect_admm", "dbp_detect_cg",
@@ -49,7 +50,8 @@ class Dims(ctypes.Structure):
 
 class Stats(ctypes.Structure):
     _fields_ = [("allreduce_calls", ctypes.c_int64), ("allreduce_bytes", ctypes.c_int64),
-                ("kernel_launches", ctypes.c_int64), ("consensus_rounds", ctypes.c_int64)]
+                ("kernel_launches", ctypes.c_int64), ("consensus_rounds", ctypes.c_int64),
+                ("graph_replays", ctypes.c_int64)]
 
 
 class KernelTime(ctypes.Structure):

@@ -24,12 +24,17 @@ for G in (int(g) for g in a.gs.split(",")):
     H, y, _ = synth.uplink_frame(loc)
     Hd, s = synth.downlink_frame(loc.scaled(algo="admm_dl"))
     H, y, Hd, s = (torch.from_numpy(v).cuda() for v in (H, y, Hd, s))
-    runs = {"admm_ul": lambda: dbp.detect_admm(ctx, H, y, N0=cfg.N0, mod=cfg.mod, T=cfg.T),
-            "cg_ul": lambda: dbp.detect_cg(ctx, H, y, rho=cfg.N0, mod=cfg.mod, T=cfg.T),
-            "admm_dl": lambda: dbp.beamform_admm(ctx, Hd, s, T=cfg.T)}
+    o1, h1 = torch.empty((cfg.N, 1, cfg.U), dtype=torch.complex64, device="cuda"), \
+        torch.empty((cfg.N, 1, cfg.U), dtype=torch.uint8, device="cuda")
+    o2, h2 = torch.empty_like(o1), torch.empty_like(h1)
+    o3 = torch.empty((loc.C, cfg.N, 1, cfg.S), dtype=torch.complex64, device="cuda")
+    runs = {"admm_ul": lambda: dbp.detect_admm(ctx, H, y, N0=cfg.N0, mod=cfg.mod, T=cfg.T, s_hat=o1, hard=h1),
+            "cg_ul": lambda: dbp.detect_cg(ctx, H, y, rho=cfg.N0, mod=cfg.mod, T=cfg.T, x_hat=o2, hard=h2),
+            "admm_dl": lambda: dbp.beamform_admm(ctx, Hd, s, T=cfg.T, x=o3)}
     out = {}
-    for split in (0, 1):
-        ctx.set_option(dbp.OPT_FORCE_SPLIT, split)
+    for split in (0, 1, 2):                      # fused; split (graphs); split, plain launches
+        ctx.set_option(dbp.OPT_FORCE_SPLIT, int(split > 0))
+        ctx.set_option(dbp.OPT_GRAPHS, int(split != 2))
         for nm, fn in runs.items():
             fn()
             ctx.sync()
@@ -42,5 +47,6 @@ for G in (int(g) for g in a.gs.split(",")):
             torch.cuda.synchronize()
             out[(nm, split)] = sum(e0.elapsed_time(e1) for e0, e1 in ev) / a.reps * 1e3
     ctx.set_option(dbp.OPT_FORCE_SPLIT, 0)
-    print(f"G={G} C_loc={loc.C}: " + ", ".join(f"{nm} fused {out[(nm, 0)]:.1f} split {out[(nm, 1)]:.1f} us"
-                                               for nm in runs))
+    ctx.set_option(dbp.OPT_GRAPHS, 1)
+    print(f"G={G} C_loc={loc.C}: " + ", ".join(f"{nm} fused {out[(nm, 0)]:.1f} split+graphs {out[(nm, 1)]:.1f} "
+                                               f"split {out[(nm, 2)]:.1f} us" for nm in runs), flush=True)

@@ -665,3 +665,49 @@ def test_ss_round_counts(env):
         ctx.sync()
         assert st1["consensus_rounds"] - st0["consensus_rounds"] == T
         assert st2["consensus_rounds"] - st1["consensus_rounds"] == T - 1
+
+
+def test_split_graphs_replay_bitwise(env):
+    """DBP_OPT_GRAPHS: the multi-launch schedules (here the forced split path: per-pair
+    preprocessing, T per-round kernels and the allreduce slots, the final kernel) are captured
+    once and replayed; replays give bitwise the results of plain launches, and the counters
+    (launches, rounds) advance as if the schedule had been issued."""
+    dbp, ctx, oracle, torch = env
+    cfg = synth.CONFIGS["C"].scaled(N=24)
+    H, y, _ = synth.uplink_frame(cfg)
+    Hd, s = synth.downlink_frame(cfg.scaled(algo="admm_dl"))
+    Hg, yg, Hdg, sg = (torch.from_numpy(a).cuda() for a in (H, y, Hd, s))
+    outs = {}
+    bufs = {"sa": torch.empty((cfg.N, 1, cfg.U), dtype=torch.complex64, device="cuda"),
+            "ha": torch.empty((cfg.N, 1, cfg.U), dtype=torch.uint8, device="cuda"),
+            "xc": torch.empty((cfg.N, 1, cfg.U), dtype=torch.complex64, device="cuda"),
+            "hc": torch.empty((cfg.N, 1, cfg.U), dtype=torch.uint8, device="cuda"),
+            "xb": torch.empty((cfg.C, cfg.N, 1, cfg.S), dtype=torch.complex64, device="cuda")}
+    for graphs in (0, 1):
+        ctx.set_option(dbp.OPT_GRAPHS, graphs)
+        ctx.set_option(dbp.OPT_FORCE_SPLIT, 1)
+        try:
+            res = []
+            for rep in range(3):
+                st0 = ctx.stats()
+                dbp.detect_admm(ctx, Hg, yg, rho=1.0, N0=cfg.N0, mod=cfg.mod, T=5, s_hat=bufs["sa"], hard=bufs["ha"])
+                dbp.detect_cg(ctx, Hg, yg, rho=cfg.N0, mod=cfg.mod, T=5, x_hat=bufs["xc"], hard=bufs["hc"])
+                dbp.beamform_admm(ctx, Hdg, sg, rho=1.0, T=5, x=bufs["xb"])
+                ctx.sync()
+                st1 = ctx.stats()
+                res.append(tuple(bufs[k].cpu().numpy().copy() for k in ("sa", "ha", "xc", "hc", "xb")) +
+                           (st1["consensus_rounds"] - st0["consensus_rounds"],
+                            st1["kernel_launches"] - st0["kernel_launches"],
+                            st1["graph_replays"] - st0["graph_replays"]))
+                for b in bufs.values():
+                    b.zero_()
+        finally:
+            ctx.set_option(dbp.OPT_FORCE_SPLIT, 0)
+            ctx.set_option(dbp.OPT_GRAPHS, 1)
+        outs[graphs] = res
+    for r0, r1 in zip(outs[0], outs[1]):
+        for u, v in zip(r0[:5], r1[:5]):
+            assert np.array_equal(u, v)
+        assert r0[5] == r1[5] == 5 + 6 + 4 and r0[6] == r1[6]
+    assert [r[7] for r in outs[0]] == [0, 0, 0]
+    assert [r[7] for r in outs[1]] == [0, 3, 3]               # captured on first use, then replayed
