@@ -652,6 +652,7 @@ extern "C" dbp_status dbp_detect_admm(dbp_ctx* c, const dbp_dims* d, const dbp_c
     a.flag = c->d_flag;
     a.C_loc = sh.C_loc; a.N = sh.N; a.J = sh.J; a.U = sh.U; a.T = T;
     a.rho = rho; a.gamma = gamma;
+    a.wonly = gamma == 1.f;                 // split rounds: w-only state (5504 -> 4992 B per pair at UP = 32)
     a.px = make_prox(reg, mod, sh.C, rho, N0, Es);
     a.md = modem_of(mod);
     int NT, CCH;

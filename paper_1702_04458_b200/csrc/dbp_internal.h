@@ -104,6 +104,7 @@ struct UlArgs {
     uint8_t* hard;
     int* flag;
     int C_loc, N, J, U, T, NT, init;
+    int wonly;            // split: gamma == 1 -> carry only w_c = z_c + lambda_c between rounds
     float rho, gamma;
     Prox px;
     Modem md;

@@ -186,6 +186,12 @@ __global__ void __launch_bounds__(256) k_admm_it(UlArgs a, int CCH) {   // split
                 lam = make_float2(0.f, 0.f);
                 z = yreg;
                 w = yreg;
+            } else if (a.wonly) {
+                // gamma = 1: lambda' = w - s, so z' + lambda' = y^reg + rho B^{-1} (2 s - w) + w - s
+                // (lines 12, 15, 17 with lambda and z eliminated): only w_c is carried between rounds
+                const float2 s = Sv[((size_t)nl * J + jj) * UP + i];
+                const float2 w0 = a.z[o];
+                w = c_add(c_add(yreg, row_apply<UP>(R, buf, i, c_sub(c_scale(s, 2.f), w0))), c_sub(w0, s));
             } else {
                 const float2 s = Sv[((size_t)nl * J + jj) * UP + i];
                 lam = c_add(a.lam[o], c_scale(c_sub(a.z[o], s), a.gamma));   // line 12
@@ -193,8 +199,12 @@ __global__ void __launch_bounds__(256) k_admm_it(UlArgs a, int CCH) {   // split
                 w = c_add(z, lam);                                           // line 17
             }
             if (valid) {
-                a.lam[o] = lam;
-                a.z[o] = z;
+                if (a.wonly) {
+                    a.z[o] = w;                                              // the z buffer holds w_c
+                } else {
+                    a.lam[o] = lam;
+                    a.z[o] = z;
+                }
                 wp[(size_t)jj * CCH * UP] = c_add(wp[(size_t)jj * CCH * UP], w);
             }
         }

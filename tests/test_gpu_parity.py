@@ -711,3 +711,23 @@ def test_split_graphs_replay_bitwise(env):
         assert r0[5] == r1[5] == 5 + 6 + 4 and r0[6] == r1[6]
     assert [r[7] for r in outs[0]] == [0, 0, 0]
     assert [r[7] for r in outs[1]] == [0, 3, 3]               # captured on first use, then replayed
+
+
+@pytest.mark.parametrize("gamma", [1.0, 0.7, 1.6])
+@pytest.mark.parametrize("path", PATHS)
+def test_admm_gamma(env, gamma, path):
+    """The ADMM step gamma (P245) on every path; gamma = 1 takes the split path's w-only
+    state (lambda and z eliminated), other gammas the lambda / z state."""
+    dbp, ctx, oracle, torch = env
+    cfg = synth.Config("g", "admm_ul", C=6, S=12, U=8, N=20, mod="qam16", snr_db=12)
+    H, y, _ = synth.uplink_frame(cfg)
+    set_path(env, path)
+    try:
+        s, hard = dbp.detect_admm(ctx, torch.from_numpy(H).cuda(), torch.from_numpy(y).cuda(), rho=0.8,
+                                  gamma=gamma, N0=cfg.N0, mod=cfg.mod, T=6)
+        ctx.sync()
+    finally:
+        set_path(env, "fused")
+    s_ref, hard_ref = oracle.detect_admm(H, y, rho=0.8, gamma=gamma, N0=cfg.N0, mod=cfg.mod, T=6)
+    assert rel(s.cpu().numpy(), s_ref) < TOL
+    check_hard(hard.cpu().numpy(), hard_ref, s_ref, cfg.mod)
