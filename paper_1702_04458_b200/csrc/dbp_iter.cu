@@ -294,7 +294,8 @@ __global__ void __launch_bounds__(512, MINB) k_bf_gj(DlArgs a) {
             bf_output<UP>(a.Hd + pair * (size_t)a.U * a.S, buf, i, r, a.U, a.S,
                           a.x + (pair * a.J + jj) * a.S, valid);        // line 20 / output
         } else {
-            a.m[(pair * a.J + jj) * UP + i] = r;                        // all symbols' r, then one H_c pass
+            if (valid) a.m[(pair * a.J + jj) * UP + i] = r;             // all symbols' r, then one H_c pass
+                                                                        // (padding lanes alias pair N - 1)
         }
     }
     if (a.J > 1) {

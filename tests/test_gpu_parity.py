@@ -731,3 +731,26 @@ def test_admm_gamma(env, gamma, path):
     s_ref, hard_ref = oracle.detect_admm(H, y, rho=0.8, gamma=gamma, N0=cfg.N0, mod=cfg.mod, T=6)
     assert rel(s.cpu().numpy(), s_ref) < TOL
     check_hard(hard.cpu().numpy(), hard_ref, s_ref, cfg.mod)
+
+
+@pytest.mark.parametrize("cfg", [synth.CONFIGS["C"].scaled(N=7, N_sym=7),                      # Table II shape
+                                 synth.Config("j10", "admm_ul", C=8, S=32, U=16, N=9, N_sym=10, mod="qam16",
+                                              snr_db=20),                                    # two batches
+                                 synth.Config("j2u5", "admm_ul", C=3, S=10, U=5, N=11, N_sym=2, mod="qpsk",
+                                              snr_db=10)],
+                         ids=lambda c: f"{c.name}-C{c.C}S{c.S}U{c.U}N{c.N}J{c.N_sym}")
+@pytest.mark.parametrize("reg", ["mmse", "box"])
+def test_nsym_paths(env, cfg, reg):
+    """N_sym > 1 at world 1 (k_prefold / k_mf_yreg + the lane-row iteration kernels; padding
+    subcarriers of a partial CTA must not store) against the oracle, uplink and downlink
+    (eps > 0 too)."""
+    dbp, ctx, oracle, torch = env
+    s, hard, s_ref, hard_ref = run_admm(env, cfg, "fused", reg=reg)
+    assert rel(s, s_ref) < TOL
+    check_hard(hard, hard_ref, s_ref, cfg.mod)
+    Hd, sv = synth.downlink_frame(cfg.scaled(algo="admm_dl"))
+    for eps in (0.0, 0.2):
+        x = dbp.beamform_admm(ctx, torch.from_numpy(Hd).cuda(), torch.from_numpy(sv).cuda(), rho=cfg.rho, T=cfg.T,
+                              eps=eps)
+        ctx.sync()
+        assert rel(x.cpu().numpy(), oracle.beamform_admm(Hd, sv, rho=cfg.rho, T=cfg.T, eps=eps)) < TOL
