@@ -94,7 +94,10 @@ struct FuArgs {
 };
 
 template <int UP, int SOLVER>
-__global__ void __launch_bounds__(128, 3)
+#ifndef DBP_FZ_MINB
+#define DBP_FZ_MINB 3
+#endif
+__global__ void __launch_bounds__(128, DBP_FZ_MINB)
 k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmY, FuArgs a) {
     using Z = FZ<UP, SOLVER>;
     using F = Fold<UP>;
