@@ -152,8 +152,21 @@ dbp_status dbp_get_unique_id(uint8_t id[128]);
 
 /* Create a context bound to CUDA `device` for `rank` of `world`.  `id` is the
  * rank-0 unique id (ignored and may be NULL when world == 1).  Collective
- * over all ranks when world > 1 (ncclCommInitRank). */
+ * over all ranks when world > 1 (ncclCommInitRank).  world > 1 with id == NULL
+ * creates a context without an NCCL communicator whose consensus exchange is a
+ * host hook (dbp_set_allreduce_hook, which must be set before any solver call). */
 dbp_status dbp_ctx_create(dbp_ctx** ctx, int device, int rank, int world, const uint8_t* id);
+
+/* Host-side consensus exchange for a context created without a communicator (world > 1,
+ * id == NULL): instead of ncclAllReduce, each round's partial sums (n_floats fp32 values,
+ * complex interleaved) are copied to a pinned host buffer, `fn(host_buf, n_floats, user)` must
+ * replace them in place by their sum over all ranks (in the same rank order everywhere) and
+ * return 0, and the result is copied back -- the same dataflow over any transport (e.g. gloo;
+ * the test suite uses it to run two ranks of the real library on one GPU).  Slow by design;
+ * never used by the NCCL path.  Graphs and device-side consensus are off for such a context.
+ * A non-zero return from fn makes the solver call return DBP_ERR_NCCL. */
+typedef int (*dbp_allreduce_fn)(float* host_buf, int64_t n_floats, void* user);
+dbp_status dbp_set_allreduce_hook(dbp_ctx* ctx, dbp_allreduce_fn fn, void* user);
 dbp_status dbp_ctx_destroy(dbp_ctx* ctx);
 dbp_status dbp_set_option(dbp_ctx* ctx, int option, int64_t value);
 dbp_status dbp_get_stats(const dbp_ctx* ctx, dbp_stats* out);

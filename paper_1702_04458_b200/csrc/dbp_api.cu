@@ -27,6 +27,11 @@ struct dbp_ctx {
     int force_split = 0;
     int no_fused = 0;
     int mode = 0;                // DBP_OPT_MODE: 0 paper rule (S < U -> S x S), 1 U x U, 2 S x S
+    // host allreduce hook (world > 1 without a communicator)
+    dbp_allreduce_fn hook = nullptr;
+    void* hook_user = nullptr;
+    float* hbuf = nullptr;
+    size_t hbuf_bytes = 0;
     // CUDA graphs of the multi-launch schedules (DBP_OPT_GRAPHS): key -> instantiated graph
     int graphs = 1;
     cudaStream_t cap = nullptr;
@@ -118,7 +123,6 @@ extern "C" dbp_status dbp_ctx_create(dbp_ctx** out, int device, int rank, int wo
     if (!out) return fail(DBP_ERR_INVALID_ARG, "ctx out-pointer is NULL");
     *out = nullptr;
     if (world < 1 || rank < 0 || rank >= world) return fail(DBP_ERR_INVALID_ARG, "bad rank %d / world %d", rank, world);
-    if (world > 1 && !id) return fail(DBP_ERR_INVALID_ARG, "world > 1 needs the rank-0 unique id");
     int ndev = 0;
     CU(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return fail(DBP_ERR_INVALID_ARG, "device %d of %d", device, ndev);
@@ -134,7 +138,7 @@ extern "C" dbp_status dbp_ctx_create(dbp_ctx** out, int device, int rank, int wo
         delete c;
         return fail(DBP_ERR_CUDA, "context setup: %s", cudaGetErrorString(e));
     }
-    if (world > 1) {
+    if (world > 1 && id) {
         ncclUniqueId u;
         memcpy(&u, id, 128);
         ncclResult_t r = ncclCommInitRank(&c->comm, world, u, rank);
@@ -159,6 +163,7 @@ extern "C" dbp_status dbp_ctx_destroy(dbp_ctx* c) {
     cudaFree(c->d_flag);
     if (c->stage) cudaFree(c->stage);
     if (c->iws) cudaFree(c->iws);
+    if (c->hbuf) cudaFreeHost(c->hbuf);
     for (auto& g : c->gcache) cudaGraphExecDestroy(g.exec);
     if (c->cap) cudaStreamDestroy(c->cap);
     for (auto& p : c->pending) { cudaEventDestroy(p.e0); cudaEventDestroy(p.e1); }
@@ -197,11 +202,19 @@ extern "C" dbp_status dbp_get_stats(const dbp_ctx* c, dbp_stats* s) {
     return DBP_OK;
 }
 
+extern "C" dbp_status dbp_set_allreduce_hook(dbp_ctx* c, dbp_allreduce_fn fn, void* user) {
+    if (!c) return fail(DBP_ERR_INVALID_ARG, "ctx is NULL");
+    if (c->comm) return fail(DBP_ERR_INVALID_ARG, "the context has an NCCL communicator");
+    c->hook = fn;
+    c->hook_user = user;
+    return DBP_OK;
+}
+
 extern "C" dbp_status dbp_get_comm_info(const dbp_ctx* c, int* nranks, int* rank) {
     if (!c || !nranks || !rank) return fail(DBP_ERR_INVALID_ARG, "NULL argument");
-    if (!c->comm) {
-        *nranks = 1;
-        *rank = 0;
+    if (!c->comm) {                       // world 1, or a host-hook context: the context's own view
+        *nranks = c->world;
+        *rank = c->rank;
         return DBP_OK;
     }
     NC(ncclCommCount(c->comm, nranks));
@@ -385,6 +398,26 @@ static dbp_status end_call(dbp_ctx*, Call& k, cudaStream_t st) {
 static dbp_status allreduce(dbp_ctx* c, float2* buf, size_t nfloat2, cudaStream_t st, bool round = true) {
     if (round) c->consensus_rounds += 1;
     if (c->world == 1) return DBP_OK;
+    if (!c->comm) {
+        // host hook (dbp_set_allreduce_hook): D2H, sum over ranks on the host, H2D
+        if (!c->hook) return fail(DBP_ERR_NCCL, "world %d context without a communicator or allreduce hook", c->world);
+        const size_t bytes = nfloat2 * 8;
+        if (c->hbuf_bytes < bytes) {
+            if (c->hbuf) cudaFreeHost(c->hbuf);
+            c->hbuf = nullptr;
+            c->hbuf_bytes = 0;
+            CU(cudaMallocHost(&c->hbuf, bytes));
+            c->hbuf_bytes = bytes;
+        }
+        CU(cudaMemcpyAsync(c->hbuf, buf, bytes, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        if (c->hook(c->hbuf, (int64_t)(nfloat2 * 2), c->hook_user) != 0)
+            return fail(DBP_ERR_NCCL, "allreduce hook failed (rank %d)", c->rank);
+        CU(cudaMemcpyAsync(buf, c->hbuf, bytes, cudaMemcpyHostToDevice, st));
+        c->allreduce_calls += 1;
+        c->allreduce_bytes += (int64_t)bytes;
+        return DBP_OK;
+    }
     NC(ncclAllReduce(buf, buf, nfloat2 * 2, ncclFloat32, ncclSum, c->comm, st));
     c->allreduce_calls += 1;
     c->allreduce_bytes += (int64_t)(nfloat2 * 8);
@@ -401,7 +434,7 @@ static dbp_status allreduce(dbp_ctx* c, float2* buf, size_t nfloat2, cudaStream_
 // every replay by the amounts the captured schedule issued.
 template <class F>
 static dbp_status graphed(dbp_ctx* c, bool host, cudaStream_t s, const std::vector<uint64_t>& key, F&& body) {
-    if (!c->graphs || host || c->timing) return body(s);
+    if (!c->graphs || host || c->timing || (c->world > 1 && !c->comm)) return body(s);
     ++c->gclock;
     for (auto& g : c->gcache) {
         if (g.key != key) continue;
@@ -518,7 +551,9 @@ static dbp_status xbuf_ensure(dbp_ctx* c, int N, cudaStream_t s) {
 }
 
 // Consensus-exchange arguments for one call with `rounds` rounds (nullptr: not in use).
-static bool xcons_active(const dbp_ctx* c) { return c->xcons == 2 || (c->xcons == 1 && c->world > 1); }
+static bool xcons_active(const dbp_ctx* c) {
+    return c->xcons == 2 || (c->xcons == 1 && c->world > 1 && c->comm);
+}
 
 static XArgs xargs_for(dbp_ctx* c, int rounds) {
     XArgs x{};

@@ -31,7 +31,7 @@ OPT_GRAPHS = 6
 EXPORTS = ["dbp_get_unique_id", "dbp_ctx_create", "dbp_ctx_destroy", "dbp_set_option", "dbp_get_stats",
            "dbp_last_error", "dbp_workspace_bytes", "dbp_detect_admm", "dbp_detect_cg",
            "dbp_beamform_admm", "dbp_slice", "dbp_sync", "dbp_get_kernel_times", "dbp_complexity",
-           "dbp_detect_mmse", "dbp_precode_zf", "dbp_get_comm_info"]
+           "dbp_detect_mmse", "dbp_precode_zf", "dbp_get_comm_info", "dbp_set_allreduce_hook"]
 CPLX_ALGO = {"admm_dl": 0, "admm_ul": 1, "cg_ul": 2, "zf_dl": 3, "mmse_ul": 4}
 CPLX_MODE = {"SxS": 0, "UxU": 1, None: 1}
 CPLX_METRIC = {"TM": 0, "AR": 1}
@@ -88,6 +88,7 @@ def load() -> ctypes.CDLL:
         "dbp_detect_mmse": [P, P, P, P, F, F, I, P, P, P, S, P],
         "dbp_precode_zf": [P, P, P, P, P, P, S, P],
         "dbp_get_comm_info": [P, P, P],
+        "dbp_set_allreduce_hook": [P, P, P],
     }
     for name, args in sigs.items():
         fn = getattr(lib, name)
@@ -190,6 +191,9 @@ def _dim(x, i, name):
     return int(x.shape[i])
 
 
+HOOK_T = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_float), ctypes.c_int64, ctypes.c_void_p)
+
+
 class Context:
     """One libdbp context (one per rank); NCCL communicator when world > 1."""
 
@@ -220,6 +224,19 @@ class Context:
         s = Stats()
         _check(load().dbp_get_stats(self._h, ctypes.byref(s)))
         return {k: getattr(s, k) for k, _ in Stats._fields_}
+
+    def set_allreduce_hook(self, fn):
+        """Host consensus exchange for a context created with world > 1 and no unique id:
+        fn(arr) receives the round's partial sums as a float32 numpy array (a view of the
+        library's pinned buffer) and must replace them in place by their sum over all ranks."""
+        def _cb(ptr, n, user):
+            try:
+                fn(np.ctypeslib.as_array(ptr, shape=(int(n),)))
+                return 0
+            except Exception:                       # noqa: BLE001 -- reported as DBP_ERR_NCCL
+                return 1
+        self._hook = HOOK_T(_cb)                    # keep the trampoline alive with the context
+        _check(load().dbp_set_allreduce_hook(self._h, self._hook, None))
 
     def comm_info(self) -> dict:
         """{'nranks': ncclCommCount, 'rank': ncclCommUserRank} of the consensus communicator."""
