@@ -568,16 +568,39 @@ def main():
         def rel(a, b):
             return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
-        # (i) device-side consensus (NEXT-1) on the same step, cross-checked against the NCCL path
+        # (i) device-side consensus (NEXT-1) on the same step, cross-checked against the NCCL path.  Every
+        # rank runs the same sequence of collectives whatever happens locally: solver errors are caught per
+        # call, and the ranks agree (MIN over ranks) on success before any result is reduced.
         if not args.no_device_consensus:
-            try:
-                ctx.set_option(dbp.OPT_DEVICE_CONSENSUS, 1)
-                for _ in range(3):
-                    for nm in ORDER:
-                        solver(nm, UL.T)
-                ctx.sync()
-                pdc = mx(timed_region(args.steps, UL.T, ORDER))
-                ctx.sync()
+            errs = []
+
+            def dc_solver(nm, T):
+                try:
+                    solver(nm, T)
+                except Exception as e:   # noqa: BLE001 -- a bounded timeout or launch error, never a hang
+                    errs.append(str(e)[:300])
+
+            def agree(ok):
+                return bool(max_over_ranks([0.0 if ok else 1.0], world, dist, dev)[0] == 0.0)
+
+            def synced():
+                try:
+                    ctx.sync()
+                except Exception as e:   # noqa: BLE001
+                    errs.append(str(e)[:300])
+                return not errs
+
+            ctx.set_option(dbp.OPT_DEVICE_CONSENSUS, 1)
+            for _ in range(3):
+                for nm in ORDER:
+                    dc_solver(nm, UL.T)
+            ok = agree(synced())
+            pdc = None
+            if ok:
+                pdc = mx(timed_region(args.steps, UL.T, ORDER, fn=dc_solver))
+                ok = agree(synced())
+            ctx.set_option(dbp.OPT_DEVICE_CONSENSUS, 0)
+            if ok:
                 dc = (s_hat.cpu().numpy(), x_hat.cpu().numpy(), xbf.cpu().numpy())
                 err = [rel(a, b) for a, b in zip(dc, ref_outs)]
                 ms = float(pdc.sum()) / args.steps
@@ -585,10 +608,8 @@ def main():
                     "ms_per_step": ms, "value": BITS_PER_STEP / (ms * 1e-3) / 1e9,
                     "rel_l2_vs_nccl": {"admm_ul": err[0], "cg_ul": err[1], "admm_dl": err[2]},
                     "solvers_ms": dict(zip(ORDER, (pdc / args.steps).tolist()))}
-            except Exception as e:   # a protocol fault is a bounded timeout (DBP_ERR_CUDA), never a hang
-                multi["modes"]["device_consensus"] = {"error": str(e)[:300]}
-            finally:
-                ctx.set_option(dbp.OPT_DEVICE_CONSENSUS, 0)
+            else:
+                multi["modes"]["device_consensus"] = {"error": (errs[0] if errs else "failed on another rank")}
 
         # (ii) world-1 solve of the whole frame on every rank (same GPU): rel-L2 <= 1e-5
         ctx1 = dbp.Context(device=local, rank=0, world=1)
