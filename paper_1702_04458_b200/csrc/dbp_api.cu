@@ -453,15 +453,21 @@ static dbp_status graphed(dbp_ctx* c, bool host, cudaStream_t s, const std::vect
     dbp_status st = body(c->cap);
     cudaGraph_t graph = nullptr;
     const cudaError_t e = cudaStreamEndCapture(c->cap, &graph);
-    if (st || e != cudaSuccess) {
-        if (graph) cudaGraphDestroy(graph);
-        cudaGetLastError();
-        return st ? st : fail(DBP_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
-    }
     cudaGraphExec_t exec = nullptr;
-    const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
-    cudaGraphDestroy(graph);
-    if (ei != cudaSuccess) return fail(DBP_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ei));
+    cudaError_t ei = cudaErrorUnknown;
+    if (!st && e == cudaSuccess) ei = cudaGraphInstantiate(&exec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    if (st || e != cudaSuccess || ei != cudaSuccess) {
+        // nothing ran during the capture: undo its bookkeeping, stop capturing on this context and
+        // issue the schedule with plain launches (an argument error simply recurs there)
+        cudaGetLastError();
+        c->launches = l0;
+        c->allreduce_calls = a0;
+        c->allreduce_bytes = b0;
+        c->consensus_rounds = r0;
+        c->graphs = 0;
+        return body(s);
+    }
     if (c->gcache.size() >= 16) {                      // evict the least recently used
         size_t v = 0;
         for (size_t i = 1; i < c->gcache.size(); ++i)
