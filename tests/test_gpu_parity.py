@@ -601,6 +601,9 @@ SS_SHAPES = [
     synth.Config("s<u-odd", "admm_ul", C=3, S=5, U=9, N=7, N_sym=3, mod="qam64", snr_db=25),
     synth.Config("s>u", "admm_ul", C=2, S=16, U=4, N=16, mod="qpsk", snr_db=10),        # forced S x S
     synth.Config("s32", "admm_ul", C=4, S=32, U=16, N=9, mod="qam64", snr_db=25),       # forced, SP = 32
+    synth.Config("s1", "admm_ul", C=1, S=1, U=3, N=1, mod="qpsk", snr_db=10),            # edge: one antenna, C = 1
+    synth.Config("u32", "admm_ul", C=5, S=3, U=32, N=4, mod="qam16", snr_db=20),         # U = 32, SP = 4
+    synth.Config("s31", "admm_ul", C=2, S=31, U=32, N=3, N_sym=2, mod="qpsk", snr_db=15),  # SP = 32, S < U
 ]
 
 
