@@ -135,6 +135,18 @@ def _gen(args):
     return synth.downlink_frame(cfg, c0, c1, n0, n1)
 
 
+_POOL = {}
+
+
+def _pool(workers: int):
+    """One process pool for all frame generation, started with 'spawn' (the bench process already
+    holds CUDA / NCCL threads, which a fork would copy in an undefined state)."""
+    if workers not in _POOL:
+        import multiprocessing as mp
+        _POOL[workers] = ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("spawn"))
+    return _POOL[workers]
+
+
 def gen_frame(kind: str, cfg, c0: int, c1: int, n0: int = 0, n1: int | None = None, workers: int = 1):
     """synth frame of clusters [c0, c1), subcarriers [n0, n1), generated per cluster in parallel
     (the values do not depend on the split: counter-based Philox)."""
@@ -143,8 +155,7 @@ def gen_frame(kind: str, cfg, c0: int, c1: int, n0: int = 0, n1: int | None = No
     if workers <= 1 or len(jobs) == 1:
         parts = [_gen(j) for j in jobs]
     else:
-        with ProcessPoolExecutor(max_workers=min(workers, len(jobs))) as ex:
-            parts = list(ex.map(_gen, jobs))
+        parts = list(_pool(workers).map(_gen, jobs))
     if kind == "ul":
         return np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts])
     return np.concatenate([p[0] for p in parts]), parts[0][1]
@@ -825,6 +836,8 @@ def main():
                 "kernels": kern, "clocks": clocks}
         print(json.dumps(line), flush=True)
     ctx.close()
+    for ex in _POOL.values():
+        ex.shutdown(wait=False, cancel_futures=True)
     if world > 1:
         dist.destroy_process_group()
 
