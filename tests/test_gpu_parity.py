@@ -757,3 +757,21 @@ def test_nsym_paths(env, cfg, reg):
                               eps=eps)
         ctx.sync()
         assert rel(x.cpu().numpy(), oracle.beamform_admm(Hd, sv, rho=cfg.rho, T=cfg.T, eps=eps)) < TOL
+
+
+@pytest.mark.parametrize("cfg", [synth.CONFIGS["C"].scaled(N=13, N_sym=7),
+                                 synth.Config("j2", "admm_ul", C=5, S=12, U=8, N=9, N_sym=2, mod="qam16", snr_db=15),
+                                 synth.Config("j5", "admm_ul", C=12, S=16, U=14, N=7, N_sym=5, mod="qam64", snr_db=25),
+                                 synth.Config("j3u4", "admm_ul", C=3, S=8, U=4, N=11, N_sym=3, mod="qpsk", snr_db=10)],
+                         ids=lambda c: f"{c.name}-C{c.C}S{c.S}U{c.U}N{c.N}J{c.N_sym}")
+@pytest.mark.parametrize("reg,T", [("mmse", 5), ("mmse", 1), ("zf", 3), ("box", 6)])
+def test_admm_fused_nsym(env, cfg, reg, T):
+    """k_fusedj: ADMM-UL with N_sym = 2..7 in one kernel (Gram + inverse once, the matched filters as
+    border columns of the sweep, all symbols through every round, w-only state at gamma = 1)."""
+    dbp, ctx, oracle, torch = env
+    st0 = ctx.stats()
+    s, hard, s_ref, hard_ref = run_admm(env, cfg, "fused", reg=reg, T=T)
+    st1 = ctx.stats()
+    assert rel(s, s_ref) < TOL
+    check_hard(hard, hard_ref, s_ref, cfg.mod)
+    assert st1["kernel_launches"] - st0["kernel_launches"] == 1         # the single fused kernel
