@@ -653,7 +653,7 @@ extern "C" dbp_status dbp_detect_admm(dbp_ctx* c, const dbp_dims* d, const dbp_c
     if (c->world == 1 && !c->force_split && !c->no_fused && sh.J > 1 && gamma == 1.f) {
         // N_sym > 1 in one per-subcarrier kernel (the Gram and B_c^{-1} serve all symbols, P706-709)
         bool launched = false;
-        KT("fused_ulj", (launched = launch_fused_ulj(L, sh.UP, dH, dy, sh.C_loc, sh.N, sh.S, sh.U, sh.J, T, rho,
+        KT("fused_ulj", (launched = launch_fused_ulj(L, sh.UP, false, dH, dy, sh.C_loc, sh.N, sh.S, sh.U, sh.J, T, rho,
                                                      make_prox(reg, mod, sh.C, rho, N0, Es), modem_of(mod),
                                                      static_cast<float2*>(k.io[2].dev),
                                                      static_cast<uint8_t*>(k.io[3].dev)),
@@ -770,6 +770,18 @@ extern "C" dbp_status dbp_detect_cg(dbp_ctx* c, const dbp_dims* d, const dbp_cf3
     a.N = sh.N; a.J = sh.J; a.U = sh.U; a.T = T; a.rho = rho;
     a.md = modem_of(mod);
 
+    if (c->world == 1 && !c->force_split && !c->no_fused && sh.J > 1) {
+        // N_sym > 1 in one per-subcarrier kernel (G and the J matched filters summed once, J CG solves)
+        bool launched = false;
+        KT("fused_cgj", (launched = launch_fused_ulj(L, sh.UP, true, static_cast<const float2*>(k.io[0].dev),
+                                                     static_cast<const float2*>(k.io[1].dev), sh.C_loc, sh.N, sh.S,
+                                                     sh.U, sh.J, T, rho, Prox{}, modem_of(mod), a.x_hat, a.hard),
+                         cudaGetLastError()));
+        if (launched) {
+            c->consensus_rounds += T + 1;
+            return end_call(c, k, s);
+        }
+    }
     const bool xc_on = xcons_active(c) && T < 250;
     if ((c->world == 1 || xc_on) && !c->force_split && !c->no_fused &&
         fused_ok(sh.UP, sh.C_loc, sh.N, sh.J, sh.S, sh.U)) {

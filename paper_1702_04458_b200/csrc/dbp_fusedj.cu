@@ -25,11 +25,13 @@
 #include "dbp_fold.cuh"
 #include "dbp_internal.h"
 
+#pragma nv_diag_suppress 128   // SOLVER 0 continues before the ADMM rounds: "loop is not reachable"
+
 namespace dbp {
 
 constexpr int FJ_JM = 7;          // symbols per kernel instance (N_sym = 2..7; 2 CTAs/SM fit up to 7)
 
-template <int UP>
+template <int UP, int SOLVER>
 struct FZJ {
     using F = Fold<UP>;
     static constexpr int JM = FJ_JM;
@@ -42,9 +44,11 @@ struct FZJ {
     static constexpr int PWL = F::PW * PLPJ;
     static constexpr int DLN = F::PW * UP;
     static constexpr int YB = F::PW * fold_ybuf_pair<UP>();
-    static constexpr int YRG = 32 * 4 * JM;                            // y^reg [m][j][lane]
+    static constexpr int TRI = F::TRI;
+    static constexpr int YRG = SOLVER == 1 ? 32 * 4 * JM : 0;          // ADMM: y^reg [m][j][lane]
     static constexpr int WREG = (NST * STG + PWL * 8 + DLN * 4 + YB * 8 + YRG * 8 + 127) / 128 * 128;
-    static constexpr int CBUF = 2 * WARPS * JM * UP * 8;               // Wp [warp][j][u] + Sv [sub][j][u]
+    // Wp [warp][j][u] + Sv [sub][j][u]; CG also Gp [warp][TRI] (partial Gram sums) + Gs [sub][TRI]
+    static constexpr int CBUF = 2 * WARPS * JM * UP * 8 + (SOLVER == 0 ? 2 * WARPS * TRI * 8 : 0);
     static constexpr size_t SMEM = 128 + (size_t)WARPS * WREG + CBUF;
 };
 
@@ -63,7 +67,7 @@ template <int UP>
 __device__ __forceinline__ void foldj_gram(f2x (&A)[Fold<UP>::NSLOT], f2x (&E)[4][FJ_JM], const float2* stage, int q,
                                            const int (&row)[4], int J) {
     using F = Fold<UP>;
-    using Z = FZJ<UP>;
+    using Z = FZJ<UP, 1>;
     const float2* hq = stage + q * F::SC * Z::HL;
     const float2* yq = stage + Z::HSZ + q * J * F::SC;
 #pragma unroll 2
@@ -154,10 +158,10 @@ __device__ __forceinline__ bool foldj_sweep(f2x (&A)[Fold<UP>::NSLOT], f2x (&E)[
     return ok;
 }
 
-template <int UP>
+template <int UP, int SOLVER>
 __global__ void __launch_bounds__(128, 2)
 k_fusedj(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmY, FuJArgs a) {
-    using Z = FZJ<UP>;
+    using Z = FZJ<UP, SOLVER>;
     using F = Fold<UP>;
     constexpr int L = F::L, PW = F::PW, SC = F::SC, NST = Z::NST, R = F::R, JM = Z::JM;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -174,6 +178,8 @@ k_fusedj(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtens
     float2* yrs = reinterpret_cast<float2*>(wloc + Z::PWL * 8 + Z::DLN * 4 + Z::YB * 8) + lane;
     float2* Wp = reinterpret_cast<float2*>(smem_raw + 128 + (size_t)Z::WARPS * Z::WREG);   // [warp][j][u]
     float2* Sv = Wp + Z::WARPS * JM * UP;                                                  // [sub][j][u]
+    float2* Gp = Sv + Z::WARPS * JM * UP;                                                  // CG: [warp][TRI]
+    float2* Gs = Gp + Z::WARPS * Z::TRI;                                                   // CG: [sub][TRI]
 
     int row[R];
 #pragma unroll
@@ -226,6 +232,90 @@ k_fusedj(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtens
             }
             ++sq;
             if (++st == NST) { st = 0; phase ^= 1u; }
+        }
+        if constexpr (SOLVER == 0) {
+            // ------------------------------------------ CG-UL (Alg. 2), N_sym > 1: the cluster sums
+            // G = sum_c G_c (footnote P416) and y^MRC_j = sum_c H_c^H y_cj (line 3) once, then one CG per
+            // (subcarrier, symbol) on the CTA's UP-lane groups (T iterations, P404-409, P715)
+            float dg[R];
+            fold_diag<UP>(A, row, 0.f, dg);
+#pragma unroll
+            for (int e = 0; e < F::NSLOT; ++e) {
+                float2 v = valid ? upk2(A[e]) : make_float2(0.f, 0.f);
+#pragma unroll
+                for (int o = L; o < 32; o <<= 1) {
+                    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+                    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+                }
+                A[e] = pk2(v);
+            }
+#pragma unroll
+            for (int jj = 0; jj < JM; ++jj) {
+                if (jj < J) {
+#pragma unroll
+                    for (int m = 0; m < R; ++m) {
+                        float2 v = valid ? upk2(E[m][jj]) : make_float2(0.f, 0.f);
+#pragma unroll
+                        for (int o = L; o < 32; o <<= 1) {
+                            v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+                            v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+                        }
+                        if (lane < L) Wp[(warp * JM + jj) * UP + row[m]] = v;
+                    }
+                }
+            }
+            if (lane < L) fold_store<UP>(Gp + warp * Z::TRI, A, row);
+            DBP_SYNCTHREADS();
+            for (int e = tid; e < NPC * (Z::TRI + J * UP); e += blockDim.x) {       // fixed warp order
+                const int jsub = e / (Z::TRI + J * UP), f = e - jsub * (Z::TRI + J * UP);
+                float2 acc = make_float2(0.f, 0.f);
+                if (f < Z::TRI) {
+                    for (int w2 = 0; w2 < WPS; ++w2) acc = c_add(acc, Gp[(jsub * WPS + w2) * Z::TRI + f]);
+                    Gs[jsub * Z::TRI + f] = acc;
+                } else {
+                    const int jj = (f - Z::TRI) / UP, u = (f - Z::TRI) % UP;
+                    for (int w2 = 0; w2 < WPS; ++w2) acc = c_add(acc, Wp[((jsub * WPS + w2) * JM + jj) * UP + u]);
+                    Sv[(jsub * JM + jj) * UP + u] = acc;
+                }
+            }
+            DBP_SYNCTHREADS();
+            constexpr int GPW = 32 / UP;                   // UP-lane groups per warp
+            const int u = lane % UP;
+            float2* P = pl - q * Z::PLPJ + (lane / UP) * Z::PLPJ;               // the group's vector line
+            // warp-uniform trip count: every lane of the warp stays in the loop (the CG's warp barriers and
+            // shuffles take the full mask); a group without a problem solves a clamped copy, unstored
+            for (int pb = warp * GPW; pb < NPC * J; pb += Z::WARPS * GPW) {
+                const bool live = pb + lane / UP < NPC * J;
+                const int prob = live ? pb + lane / UP : pb;
+                const int jsub = prob / J, jj = prob % J;
+                const int nn = (blockIdx.x + it * gridDim.x) * NPC + jsub;
+                const float2* Gj = Gs + jsub * Z::TRI;
+                float2 grow[UP];                                                 // row u of G
+#pragma unroll
+                for (int jc = 0; jc < UP; ++jc)
+                    grow[jc] = jc <= u ? Gj[(u * (u + 1)) / 2 + jc] : c_conj(Gj[(jc * (jc + 1)) / 2 + u]);
+                float2 r = Sv[(jsub * JM + jj) * UP + u];                        // line 6: r = y^MRC, p = r
+                float2 p = r, x = make_float2(0.f, 0.f);
+                float rr = group_sum<UP>(c_norm2(r));
+                for (int t = 0; t < a.T; ++t) {
+                    DBP_SYNCWARP();
+                    P[u] = p;
+                    DBP_SYNCWARP();
+                    float2 pv[UP];
+                    read_vec<UP>(P, pv);
+                    float2 w = make_float2(0.f, 0.f);                            // lines 9-11: w = G p
+#pragma unroll
+                    for (int jc = 0; jc < UP; ++jc) c_fma(w, grow[jc], pv[jc]);
+                    cg_update<UP>(x, r, p, rr, w, a.rho);                        // lines 13-18
+                }
+                if (live && u < a.U && nn < a.N) {
+                    const size_t o = ((size_t)nn * J + jj) * a.U + u;
+                    a.s_hat[o] = x;
+                    if (a.hard) a.hard[o] = slice_bits(x, a.md);
+                }
+            }
+            DBP_SYNCTHREADS();                                                  // Gs / Sv reused
+            continue;
         }
         // B_c^{-1} and y^reg_j (lines 7-8): diagonal + rho, Jacobi scaling, bordered sweep, un-scaling
         float dg[R], dr[R];
@@ -308,9 +398,9 @@ k_fusedj(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtens
 
 static int g_sms_fj = 0;
 
-template <int UP>
+template <int UP, int SOLVER>
 static bool launch_fj_t(const LaunchCtx& L, const float2* H, const float2* y, FuJArgs a) {
-    using Z = FZJ<UP>;
+    using Z = FZJ<UP, SOLVER>;
     using F = Fold<UP>;
     CUtensorMap tmH{}, tmY{};
     if (!make_map4(&tmH, H, a.U, a.S, a.N, a.C, UP + 2, F::SC, 1, F::PW)) return false;
@@ -321,7 +411,7 @@ static bool launch_fj_t(const LaunchCtx& L, const float2* H, const float2* y, Fu
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_sms_fj, cudaDevAttrMultiProcessorCount, dev);
     }
-    auto k = k_fusedj<UP>;
+    auto k = k_fusedj<UP, SOLVER>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z::SMEM) != cudaSuccess) {
         cudaGetLastError();
         return false;
@@ -332,9 +422,10 @@ static bool launch_fj_t(const LaunchCtx& L, const float2* H, const float2* y, Fu
     return true;
 }
 
-// ADMM-UL, N_sym = 2..8, gamma == 1, world == 1: one kernel (false: shape not taken -> caller falls back)
-bool launch_fused_ulj(const LaunchCtx& L, int UP, const float2* H, const float2* y, int C, int N, int S, int U, int J,
-                      int T, float rho, Prox px, Modem md, float2* s_hat, uint8_t* hard) {
+// ADMM-UL (cg = false; gamma == 1) or CG-UL (cg = true; rho = N0/Es), N_sym = 2..7, world == 1: one kernel
+// (false: shape not taken -> the caller falls back to the two-kernel path)
+bool launch_fused_ulj(const LaunchCtx& L, int UP, bool cg, const float2* H, const float2* y, int C, int N, int S, int U,
+                      int J, int T, float rho, Prox px, Modem md, float2* s_hat, uint8_t* hard) {
     if (J < 2 || J > FJ_JM || UP > 16 || N <= 0 || C <= 0 || (U % 2) || (S % 2)) return false;
     const int PW = 32 / (UP / 4);
     if (C > 4 * PW) return false;
@@ -345,9 +436,9 @@ bool launch_fused_ulj(const LaunchCtx& L, int UP, const float2* H, const float2*
     a.WPS = need <= 1 ? 1 : need <= 2 ? 2 : 4;
     a.NPC = 4 / a.WPS;
     switch (UP) {
-        case 4: return launch_fj_t<4>(L, H, y, a);
-        case 8: return launch_fj_t<8>(L, H, y, a);
-        case 16: return launch_fj_t<16>(L, H, y, a);
+        case 4: return cg ? launch_fj_t<4, 0>(L, H, y, a) : launch_fj_t<4, 1>(L, H, y, a);
+        case 8: return cg ? launch_fj_t<8, 0>(L, H, y, a) : launch_fj_t<8, 1>(L, H, y, a);
+        case 16: return cg ? launch_fj_t<16, 0>(L, H, y, a) : launch_fj_t<16, 1>(L, H, y, a);
         default: return false;
     }
 }

@@ -77,8 +77,9 @@ bool launch_fused_central(const LaunchCtx& L, int UP, bool dl, const float2* H, 
 bool launch_fused_dl(const LaunchCtx& L, int UP, const float2* Hd, const float2* s, int C, int C_glob, int N, int S,
                      int U, int T, float rho, float gamma, float a0, float eps, float2* x, const XArgs* xc = nullptr);
 // ADMM-UL with N_sym = 2..7 symbols per subcarrier, gamma == 1, world == 1 (dbp_fusedj.cu)
-bool launch_fused_ulj(const LaunchCtx& L, int UP, const float2* H, const float2* y, int C, int N, int S, int U, int J,
-                      int T, float rho, Prox px, Modem md, float2* s_hat, uint8_t* hard);
+// (cg: CG-UL with N_sym = 2..7, rho = N0/Es)
+bool launch_fused_ulj(const LaunchCtx& L, int UP, bool cg, const float2* H, const float2* y, int C, int N, int S, int U,
+                      int J, int T, float rho, Prox px, Modem md, float2* s_hat, uint8_t* hard);
 size_t prelr_smem(int UP, int S, int U, int J, bool ul);
 bool launch_prefold(const LaunchCtx& L, int UP, int mode, const float2* H, const float2* y, int S, int U, int J,
                     long npairs, float delta, float2* Gout, float2* vout);

@@ -775,3 +775,24 @@ def test_admm_fused_nsym(env, cfg, reg, T):
     assert rel(s, s_ref) < TOL
     check_hard(hard, hard_ref, s_ref, cfg.mod)
     assert st1["kernel_launches"] - st0["kernel_launches"] == 1         # the single fused kernel
+
+
+@pytest.mark.parametrize("cfg", [synth.CONFIGS["C"].scaled(N=13, N_sym=7),
+                                 synth.Config("cj2", "cg_ul", C=5, S=12, U=8, N=9, N_sym=2, mod="qam16", snr_db=15),
+                                 synth.Config("cj5", "cg_ul", C=12, S=16, U=14, N=7, N_sym=5, mod="qam64", snr_db=25),
+                                 synth.Config("cj3u4", "cg_ul", C=3, S=8, U=4, N=11, N_sym=3, mod="qpsk", snr_db=10)],
+                         ids=lambda c: f"{c.name}-C{c.C}S{c.S}U{c.U}N{c.N}J{c.N_sym}")
+@pytest.mark.parametrize("T", [1, 3, 5, 16])
+def test_cg_fused_nsym(env, cfg, T):
+    """k_fusedj<., 0>: CG-UL with N_sym = 2..7 in one kernel (G = sum_c G_c and the J matched filters
+    summed once per subcarrier, J CG solves on the CTA's lane groups)."""
+    dbp, ctx, oracle, torch = env
+    H, y, _ = synth.uplink_frame(cfg)
+    st0 = ctx.stats()
+    x, hard = dbp.detect_cg(ctx, torch.from_numpy(H).cuda(), torch.from_numpy(y).cuda(), rho=cfg.N0, mod=cfg.mod, T=T)
+    ctx.sync()
+    st1 = ctx.stats()
+    x_ref, hard_ref = oracle.detect_cg(H, y, rho=cfg.N0, mod=cfg.mod, T=T)
+    assert rel(x.cpu().numpy(), x_ref) < TOL
+    check_hard(hard.cpu().numpy(), hard_ref, x_ref, cfg.mod)
+    assert st1["kernel_launches"] - st0["kernel_launches"] == 1
