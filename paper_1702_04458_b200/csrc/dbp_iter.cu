@@ -287,7 +287,8 @@ __global__ void __launch_bounds__(512, MINB) k_bf_gj(DlArgs a) {
             const float2 z = c_add(w, c_scale(d, f));                                // line 14 (Lemma 2)
             lam = c_sub(lam, c_scale(c_sub(m, z), a.gamma));                         // line 15
             qv = c_add(z, lam);
-            DBP_SYNCTHREADS();
+            // (no third barrier: the next round's W / Ws writes come after its first barrier, which
+            // every thread reaches only once it has read this round's Ws)
         }
         const float2 r = row_apply<UP>(R, buf, i, qv);                  // B^{-1} q
         if (a.J == 1) {
