@@ -292,7 +292,7 @@ def relaunch(args) -> int | None:
     never silently measured on fewer GPUs."""
     if "RANK" in os.environ or args.gpus <= 1:
         return None
-    if not args.plumbing_check:
+    if not args.plumbing_check and not args.host_comm:
         import torch
         have = torch.cuda.device_count()
         if have < args.gpus:
@@ -314,11 +314,16 @@ def rank_env(args):
     return rank, world, local
 
 
+def _coll_device(dist, device):
+    """Collectives of the bench's own bookkeeping run on the process group's device (CPU for gloo)."""
+    return device if dist.get_backend() == "nccl" else None
+
+
 def max_over_ranks(vals, world, dist, device=None):
     if world == 1:
         return np.asarray(vals, dtype=np.float64)
     import torch
-    t = torch.tensor(np.asarray(vals, dtype=np.float64), device=device)
+    t = torch.tensor(np.asarray(vals, dtype=np.float64), device=_coll_device(dist, device))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t.cpu().numpy()
 
@@ -328,7 +333,7 @@ def gather_rows(row, world, dist, device=None):
     if world == 1:
         return [list(row)]
     import torch
-    t = torch.tensor(np.asarray(row, dtype=np.float64), device=device)
+    t = torch.tensor(np.asarray(row, dtype=np.float64), device=_coll_device(dist, device))
     out = [torch.empty_like(t) for _ in range(world)]
     dist.all_gather(out, t)
     return [o.cpu().numpy().tolist() for o in out]
@@ -381,6 +386,7 @@ def main():
                          "'admm_ul,cg_ul|admm_dl' (overrides --streams)")
     ap.add_argument("--ref-subcarriers", type=int, default=60)
     ap.add_argument("--plumbing-check", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--host-comm", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
 
     rc = relaunch(args)
@@ -398,15 +404,27 @@ def main():
     import torch.distributed as dist
     from paper_1702_04458_b200 import dbp
 
+    if args.host_comm:
+        # test mode: ranks may share a GPU; the consensus exchange is the library's host allreduce hook
+        # over gloo instead of NCCL (which refuses two ranks on one device) -- everything else is the
+        # world > 1 path of this script
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     uid = None
-    if world > 1:
+    if world > 1 and args.host_comm:
+        dist.init_process_group("gloo")
+    elif world > 1:
         dist.init_process_group("nccl", device_id=dev)
         obj = [dbp.get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     ctx = dbp.Context(device=local, rank=rank, world=world, unique_id=uid)
+    if world > 1 and args.host_comm:
+        def _hook(arr):
+            t = torch.from_numpy(arr)
+            dist.all_reduce(t)
+        ctx.set_allreduce_hook(_hook)
     comm = ctx.comm_info()
     if comm["nranks"] != world or comm["rank"] != rank:
         raise SystemExit(f"bench.py: NCCL communicator {comm} does not match rank {rank} / world {world}")
@@ -577,6 +595,9 @@ def main():
     multi = None
     if world > 1:
         multi = {"nccl_comm": comm, "modes": {}}
+        for nm in ORDER:                                  # the T = 1 region ran last: redo the T-round step
+            solver(nm, UL.T)
+        ctx.sync()
         ref_outs = (s_hat.cpu().numpy().copy(), x_hat.cpu().numpy().copy(), xbf.cpu().numpy().copy())
         rows = gather_rows([step_ms_rank, kern_ms_rank, step_ms_rank - kern_ms_rank,
                             (comm_stats[1]["allreduce_calls"] - comm_stats[0]["allreduce_calls"]) / args.steps],
