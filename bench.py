@@ -263,6 +263,8 @@ def algorithmic(kernel: str, C_loc: int):
         "bf_fused": P * (tri + S * U + J * S) * c8 + N * J * U * c8,
         "cg_gsum": P * (tri + J * U) * c8 + N * (tri + J * U) * c8,
         "cg_fused": N * (tri + J * U) * c8 + N * J * U * (c8 + 1),
+        # tensor-core CG (world 1): read H_c and y_c once, write x_hat (+ hard bits)
+        "cg_tc": P * (S * U + S * J) * c8 + N * J * U * (c8 + 1),
     }
     return "hbm", float(table.get(kernel, 0.0))
 

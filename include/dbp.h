@@ -136,7 +136,13 @@ typedef enum {
      * captured into a CUDA graph on first use and replayed while the call's dims, scalars and
      * device pointers repeat (host-pointer calls and KERNEL_TIMING never use graphs).  0: plain
      * launches.  Results are identical either way. */
-    DBP_OPT_GRAPHS = 6
+    DBP_OPT_GRAPHS = 6,
+    /* 1 (default): dbp_detect_cg at world == 1 with N_sym == 1, 9 <= U <= 16, S <= 64 (and no
+     * FORCE_SPLIT / NO_FUSED / DEVICE_CONSENSUS) forms the cluster-summed Gram sum_c H_c^H H_c and
+     * y^MRC on the tensor cores (k_cg_tc: fp16 mma.sync on an exact power-of-two-scaled hi/lo split,
+     * FP32 accumulation; error ~2^-22 relative to the Gram, within the 1e-4 parity bar).  0: the
+     * FP32 single-kernel path (k_fused).  The two agree to rounding, not bitwise. */
+    DBP_OPT_CG_TENSOR = 7
 } dbp_option;
 
 /* Per-kernel device time accumulated under DBP_OPT_KERNEL_TIMING. */

@@ -27,6 +27,7 @@ struct dbp_ctx {
     int force_split = 0;
     int no_fused = 0;
     int mode = 0;                // DBP_OPT_MODE: 0 paper rule (S < U -> S x S), 1 U x U, 2 S x S
+    int cg_tc = 1;               // DBP_OPT_CG_TENSOR: world-1 CG-UL Gram on the tensor cores
     // host allreduce hook (world > 1 without a communicator)
     dbp_allreduce_fn hook = nullptr;
     void* hook_user = nullptr;
@@ -178,6 +179,7 @@ extern "C" dbp_status dbp_set_option(dbp_ctx* c, int option, int64_t value) {
     if (option == DBP_OPT_KERNEL_TIMING) { c->timing = value ? 1 : 0; return DBP_OK; }
     if (option == DBP_OPT_NO_FUSED) { c->no_fused = value ? 1 : 0; return DBP_OK; }
     if (option == DBP_OPT_GRAPHS) { c->graphs = value ? 1 : 0; return DBP_OK; }
+    if (option == DBP_OPT_CG_TENSOR) { c->cg_tc = value ? 1 : 0; return DBP_OK; }
     if (option == DBP_OPT_MODE) {
         if (value < 0 || value > 2) return fail(DBP_ERR_INVALID_ARG, "mode %lld (0 auto, 1 UxU, 2 SxS)", (long long)value);
         c->mode = (int)value;
@@ -770,6 +772,17 @@ extern "C" dbp_status dbp_detect_cg(dbp_ctx* c, const dbp_dims* d, const dbp_cf3
     a.N = sh.N; a.J = sh.J; a.U = sh.U; a.T = T; a.rho = rho;
     a.md = modem_of(mod);
 
+    if (c->cg_tc && c->world == 1 && !c->force_split && !c->no_fused && sh.J == 1 && !xcons_active(c)) {
+        // b1-b5 with the cluster-summed Gram on the tensor cores (long K = C * S): one kernel
+        bool launched = false;
+        KT("cg_tc", (launched = launch_cg_tc(L, sh.UP, static_cast<const float2*>(k.io[0].dev),
+                                             static_cast<const float2*>(k.io[1].dev), sh.C_loc, sh.N, sh.S, sh.U,
+                                             sh.J, T, rho, modem_of(mod), a.x_hat, a.hard), cudaGetLastError()));
+        if (launched) {
+            c->consensus_rounds += T + 1;
+            return end_call(c, k, s);
+        }
+    }
     if (c->world == 1 && !c->force_split && !c->no_fused && sh.J > 1) {
         // N_sym > 1 in one per-subcarrier kernel (G and the J matched filters summed once, J CG solves)
         bool launched = false;

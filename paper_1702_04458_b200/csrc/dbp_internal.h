@@ -80,6 +80,9 @@ bool launch_fused_dl(const LaunchCtx& L, int UP, const float2* Hd, const float2*
 // (cg: CG-UL with N_sym = 2..7, rho = N0/Es)
 bool launch_fused_ulj(const LaunchCtx& L, int UP, bool cg, const float2* H, const float2* y, int C, int N, int S, int U,
                       int J, int T, float rho, Prox px, Modem md, float2* s_hat, uint8_t* hard);
+// CG-UL at world 1, N_sym = 1, UP = 16: the cluster-summed Gram on the tensor cores (dbp_cgtc.cu)
+bool launch_cg_tc(const LaunchCtx& L, int UP, const float2* H, const float2* y, int C, int N, int S, int U, int J,
+                  int T, float rho, Modem md, float2* x_hat, uint8_t* hard);
 size_t prelr_smem(int UP, int S, int U, int J, bool ul);
 bool launch_prefold(const LaunchCtx& L, int UP, int mode, const float2* H, const float2* y, int S, int U, int J,
                     long npairs, float delta, float2* Gout, float2* vout);

@@ -51,15 +51,22 @@ constexpr unsigned TC_NEG = 0x80000000u;
 // Gram (+ matched filter) of one pair from its TMA stage; acc[0..1] Re tiles (columns
 // 0-7, 8-15), acc[2..3] Im tiles, acc[4] matched filter (columns 0 = Re, 1 = Im).
 // nkk = number of K8 steps (ceil(S / 8)); antennas >= S are zero-filled by the TMA.
+// (kk0, kk1: the K8 steps to take, accumulate: add to acc instead of starting from zero, yoff: byte
+// offset of y in the stage -- a longer K, e.g. several clusters' antennas stacked as rows, is the
+// same loop; see dbp_cgtc.cu)
 template <bool DL, bool MF>
-__device__ __forceinline__ void tc_gram(float (&acc)[5][4], const unsigned char* stage, int nkk, int g, int t) {
+__device__ __forceinline__ void tc_gram(float (&acc)[5][4], const unsigned char* stage, int nkk, int g, int t,
+                                        int kk0 = 0, int kk1 = -1, bool accumulate = false, int yoff = -1) {
+    if (!accumulate) {
 #pragma unroll
-    for (int i = 0; i < 5; ++i)
+        for (int i = 0; i < 5; ++i)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) acc[i][e] = 0.f;
-    const float2* yv = reinterpret_cast<const float2*>(stage + nkk * 8 * 128);   // UL: y after H
+            for (int e = 0; e < 4; ++e) acc[i][e] = 0.f;
+    }
+    if (kk1 < 0) kk1 = nkk;
+    const float2* yv = reinterpret_cast<const float2*>(stage + (yoff >= 0 ? yoff : nkk * 8 * 128));   // UL: y after H
 #pragma unroll 2
-    for (int kk = 0; kk < nkk; ++kk) {
+    for (int kk = kk0; kk < kk1; ++kk) {
         float2 v[2][2];
         if (DL) {
             // box kk/2, row u, the 16-B chunk holding antennas 8(kk&1) + 2t, +1

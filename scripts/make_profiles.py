@@ -25,7 +25,7 @@ NAMES = [(r"k_fused<\d+, 3>", "fused_mmse"), (r"k_fused<\d+, 4>", "fused_zf"), (
          (r"k_gram<\d+, 0, 1", "gram_ul"), (r"k_gram<\d+, 1,", "gram_dl"), (r"k_inv_ul", "inv_ul"),
          (r"k_inv_dl", "inv_dl"), (r"k_admm_gj", "admm_fused"), (r"k_bf_gj", "bf_fused"),
          (r"k_admm_it", "admm_step"), (r"k_bf_it", "bf_step"), (r"k_cg_gsum", "cg_gsum"),
-         (r"k_cg_it<\d+, 1", "cg_fused"), (r"k_cg_it<\d+, 0", "cg_step"), (r"k_prox_out", "prox_out"),
+         (r"k_cg_it<\d+, 1", "cg_fused"), (r"k_cg_tc", "cg_tc"), (r"k_cg_it<\d+, 0", "cg_step"), (r"k_prox_out", "prox_out"),
          (r"k_mf", "mf"), (r"k_slice", "slice")]
 
 

@@ -74,12 +74,14 @@ def check_hard(hard_gpu, hard_ref, soft_ref, mod):
 
 
 PATHS = ["fused", "twokernel", "split"]   # k_fused / preprocessing + iteration kernels / per-round split path
+CG_PATHS = PATHS + ["fp32"]                # CG "fused" = k_cg_tc where it applies; "fp32" = k_fused
 
 
 def set_path(env, path):
     dbp, ctx = env[0], env[1]
     ctx.set_option(dbp.OPT_FORCE_SPLIT, int(path == "split"))
     ctx.set_option(dbp.OPT_NO_FUSED, int(path == "twokernel"))
+    ctx.set_option(dbp.OPT_CG_TENSOR, int(path != "fp32"))
 
 
 def run_admm(env, cfg, split=False, reg="mmse", T=None, host=False):
@@ -184,11 +186,17 @@ SMALL_CG = [
     synth.Config("nsym", "cg_ul", C=2, S=16, U=8, N=10, N_sym=4, mod="qam64", snr_db=30),
     synth.Config("c20", "cg_ul", C=20, S=12, U=14, N=13, mod="qam16", snr_db=22),
     synth.Config("c5", "cg_ul", C=5, S=8, U=6, N=10, mod="qpsk", snr_db=12),
+    # world-1 tensor-core CG (k_cg_tc, 9 <= U <= 16): 32-row stages of two clusters with an odd C,
+    # S padded to 32 / 64 rows, a single stage (one K-split warp idle)
+    synth.Config("tc13", "cg_ul", C=7, S=13, U=11, N=10, mod="qam16", snr_db=20),
+    synth.Config("tc40", "cg_ul", C=3, S=40, U=12, N=9, mod="qam64", snr_db=25),
+    synth.Config("tc64", "cg_ul", C=5, S=64, U=16, N=7, mod="qam16", snr_db=20),
+    synth.Config("tc1", "cg_ul", C=1, S=32, U=16, N=5, mod="qpsk", snr_db=15),
 ]
 
 
 @pytest.mark.parametrize("cfg", SMALL_CG, ids=lambda c: f"{c.name}-C{c.C}S{c.S}U{c.U}N{c.N}J{c.N_sym}")
-@pytest.mark.parametrize("split", PATHS)
+@pytest.mark.parametrize("split", CG_PATHS)
 def test_cg_parity(env, cfg, split):
     x, hard, x_ref, hard_ref = run_cg(env, cfg, split)
     assert rel(x, x_ref) < TOL
@@ -198,9 +206,32 @@ def test_cg_parity(env, cfg, split):
 @pytest.mark.parametrize("T", [1, 2, 16])
 def test_cg_iteration_counts(env, T):
     cfg = synth.CONFIGS["B"].scaled(N=20)
-    for split in PATHS:
+    for split in CG_PATHS:
         x, _, x_ref, _ = run_cg(env, cfg, split, T=T)
         assert rel(x, x_ref) < TOL
+
+
+@pytest.mark.parametrize("spread", [-40, 24])
+def test_cg_cluster_scales(env, spread):
+    """Clusters at powers of two apart (2^(spread * c / C), the largest at 1 so that the FP32 CG
+    recursion itself stays in range): the tensor-core Gram's per-group fp16 scaling must hold the
+    paper's 1e-4 bar whatever the dynamic range across clusters -- small clusters first (24) or
+    last (-40)."""
+    dbp, ctx, oracle, torch = env
+    cfg = synth.CONFIGS["C"].scaled(N=11, C=8)
+    H, y, _ = synth.uplink_frame(cfg)
+    f = np.float32(2.0) ** (spread * np.arange(cfg.C) / cfg.C)
+    f = f / f.max()
+    H = (H * f[:, None, None, None]).astype(np.complex64)
+    y = (y * f[:, None, None, None]).astype(np.complex64)
+    for path in CG_PATHS:
+        set_path(env, path)
+        x, _ = dbp.detect_cg(ctx, torch.from_numpy(H).cuda(), torch.from_numpy(y).cuda(), rho=cfg.N0, mod=cfg.mod,
+                             T=cfg.T)
+        ctx.sync()
+        x_ref, _ = oracle.detect_cg(H, y, rho=cfg.N0, mod=cfg.mod, T=cfg.T)
+        assert rel(x.cpu().numpy(), x_ref) < TOL, path
+    set_path(env, "fused")
 
 
 def test_cg_zero_input(env):
@@ -521,7 +552,9 @@ def test_device_consensus_self_peer(env):
         Hdg, sg = torch.from_numpy(Hd).cuda(), torch.from_numpy(s).cuda()
         ref_s, ref_h = dbp.detect_admm(ctx, Hg, yg, N0=cfg.N0, mod=cfg.mod, T=cfg.T)
         ref_x = dbp.beamform_admm(ctx, Hdg, sg, T=cfg.T, eps=0.2)
+        ctx.set_option(dbp.OPT_CG_TENSOR, 0)                 # device consensus runs CG in k_fused
         ref_c, ref_ch = dbp.detect_cg(ctx, Hg, yg, rho=cfg.N0, mod=cfg.mod, T=cfg.T)
+        ctx.set_option(dbp.OPT_CG_TENSOR, 1)
         ctx.sync()
         ctx.set_option(dbp.OPT_DEVICE_CONSENSUS, 2)
         try:
