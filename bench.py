@@ -29,9 +29,10 @@ NCCL communicator size.
 Timing: W untimed warm-up steps; then exactly K steps, each bracketed by CUDA
 events on the launch stream, with an untimed 256 MiB L2-flush write between
 steps; barrier + synchronize on both sides; max over ranks.  At world = 1
-the step runs ADMM-UL then ADMM-DL on one stream concurrently with CG-UL on a
-second (forked from and joined to the launch stream inside the event
-bracket); a separate sequential region (all three back to back) gives the
+the step runs ADMM-UL, ADMM-DL and CG-UL back to back on one stream (forked
+from and joined to the launch stream inside the event bracket), each solver
+launched with DBP_OPT_OVERLAP_PREV so its CTAs fill its predecessor's last wave
+(the three frames are independent); a separate sequential region (all three back to back) gives the
 per-solver times, per-iteration latencies and the kernel-timer shares the
 roofline uses.  At world > 1 the step is sequential (one communicator, one
 collective order).  `e2e` calls the same C ABI with pinned HOST buffers, so
@@ -380,12 +381,16 @@ def main():
                     help="world = 1: time the step with the three solvers back to back on one stream")
     ap.add_argument("--no-device-consensus", action="store_true",
                     help="world > 1: skip the device-side consensus leg (DBP_OPT_DEVICE_CONSENSUS)")
-    ap.add_argument("--streams", type=int, default=2, choices=[2, 3],
-                    help="world-1 concurrent schedule: 2 = ADMM-UL then ADMM-DL on one stream, CG-UL on another; "
-                         "3 = every solver on its own stream")
+    ap.add_argument("--streams", type=int, default=1, choices=[1, 2, 3],
+                    help="world-1 step schedule: 1 = ADMM-UL, ADMM-DL, CG-UL on one stream (overlapped launches); "
+                         "2 = ADMM-UL then ADMM-DL on one stream, CG-UL on another; 3 = every solver on its own "
+                         "stream")
     ap.add_argument("--plan", default=None,
                     help="world-1 concurrent schedule as solver lists per stream, e.g. "
                          "'admm_ul,cg_ul|admm_dl' (overrides --streams)")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="world-1 concurrent schedule without DBP_OPT_OVERLAP_PREV (a solver following another on "
+                         "its stream then waits for it to drain instead of filling its last wave)")
     ap.add_argument("--ref-subcarriers", type=int, default=60)
     ap.add_argument("--plumbing-check", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--host-comm", action="store_true", help=argparse.SUPPRESS)
@@ -484,12 +489,13 @@ def main():
             dbp.detect_cg(c, Hcg, ycg, rho=CG.N0, mod=CG.mod, T=T, x_hat=x_hat, hard=hard2, ws=ws["cg_ul"],
                           stream=sp)
 
-    # Step schedule.  world == 1: ADMM-UL then ADMM-DL on one stream, CG-UL on a second, so each
-    # kernel's CTAs fill the other's wave tail.  world > 1: sequential on one
+    # Step schedule.  world == 1: the three solvers back to back on one stream, each launched with
+    # DBP_OPT_OVERLAP_PREV so its CTAs fill the previous kernel's last wave (209.5 vs 211.9 us for the
+    # two-stream plan admm_ul,admm_dl|cg_ul).  world > 1: sequential on one
     # stream (every solver issues NCCL allreduces on one communicator; two streams could order them
     # differently across ranks).
     concurrent = world == 1 and not args.sequential
-    plan = args.plan or ("admm_ul|admm_dl|cg_ul" if args.streams == 3 else "admm_ul,admm_dl|cg_ul")
+    plan = args.plan or {1: "admm_ul,admm_dl,cg_ul", 2: "admm_ul,admm_dl|cg_ul", 3: "admm_ul|admm_dl|cg_ul"}[args.streams]
     plan = [lane.split(",") for lane in plan.split("|")]
     assert sorted(sum(plan, [])) == sorted(ORDER), "--plan must name each solver once"
     side = tuple(torch.cuda.Stream(dev) for _ in plan) if concurrent else None
@@ -558,11 +564,18 @@ def main():
     kern_ms_rank = sum(v[1] for v in ktimes.values()) / args.steps       # this rank's kernel time per step
     step_ms_rank = float(np.sum(per)) / args.steps
     conc_ms = None
+    overlap = False
     comm_stats = (st0, st1)                            # the timed-kernel region's counters (per-rank comm)
     if concurrent:                                     # the step as scheduled (headline)
+        # consecutive solvers on a lane are independent frames: each may start in its predecessor's
+        # last wave (programmatic dependent launch; outputs still ordered, include/dbp.h)
+        overlap = not args.no_overlap
+        ctx.set_option(dbp.OPT_OVERLAP_PREV, int(overlap))
+        step_concurrent(UL.T, join[3])                 # warm the overlapped launch path
         st0 = ctx.stats()
         conc_ms = timed_concurrent(args.steps, UL.T)
         st1 = ctx.stats()
+        ctx.set_option(dbp.OPT_OVERLAP_PREV, 0)
     else:
         # world > 1: the headline is the sequential step WITHOUT the per-kernel event timer (which brackets
         # every launch and disables graph replay); the timed-kernel region above gives the breakdown
@@ -846,6 +859,8 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_step_sequential": ms_seq,
                 "schedule": ("concurrent, one stream per lane: " + " | ".join(" then ".join(l) for l in plan)
+                             + ("; a solver may start in its lane predecessor's last wave (DBP_OPT_OVERLAP_PREV)"
+                                if overlap else "")
                              if concurrent else "sequential on one stream"),
                 "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Philox-4x32: i.i.d. Rayleigh "

@@ -142,7 +142,16 @@ typedef enum {
      * y^MRC on the tensor cores (k_cg_tc: fp16 mma.sync on an exact power-of-two-scaled hi/lo split,
      * FP32 accumulation; error ~2^-22 relative to the Gram, within the 1e-4 parity bar).  0: the
      * FP32 single-kernel path (k_fused).  The two agree to rounding, not bitwise. */
-    DBP_OPT_CG_TENSOR = 7
+    DBP_OPT_CG_TENSOR = 7,
+    /* 0 (default): ordinary stream order.  1: the single-kernel solver paths (world == 1 fused
+     * ADMM-UL / CG-UL / ADMM-DL) are launched with programmatic stream serialization: the solver's
+     * CTAs may start while the kernel before it on the stream is finishing (its last wave), filling
+     * the SMs that kernel's tail leaves idle.  The solver reads H / y / s WITHOUT waiting for that
+     * kernel, so the caller must not have it produce them (e.g. ADMM-UL of one frame followed by
+     * ADMM-DL of another); every global store waits for it (griddepcontrol.wait), so outputs stay in
+     * stream order.  Ignored with device consensus, host pointers make it moot (the H2D copy sits in
+     * between).  Our own fused kernels let the next kernel start once their last wave is running. */
+    DBP_OPT_OVERLAP_PREV = 8
 } dbp_option;
 
 /* Per-kernel device time accumulated under DBP_OPT_KERNEL_TIMING. */

@@ -28,6 +28,7 @@ struct dbp_ctx {
     int no_fused = 0;
     int mode = 0;                // DBP_OPT_MODE: 0 paper rule (S < U -> S x S), 1 U x U, 2 S x S
     int cg_tc = 1;               // DBP_OPT_CG_TENSOR: world-1 CG-UL Gram on the tensor cores
+    int pdl = 0;                 // DBP_OPT_OVERLAP_PREV: single-kernel solvers overlap the previous kernel
     // host allreduce hook (world > 1 without a communicator)
     dbp_allreduce_fn hook = nullptr;
     void* hook_user = nullptr;
@@ -180,6 +181,7 @@ extern "C" dbp_status dbp_set_option(dbp_ctx* c, int option, int64_t value) {
     if (option == DBP_OPT_NO_FUSED) { c->no_fused = value ? 1 : 0; return DBP_OK; }
     if (option == DBP_OPT_GRAPHS) { c->graphs = value ? 1 : 0; return DBP_OK; }
     if (option == DBP_OPT_CG_TENSOR) { c->cg_tc = value ? 1 : 0; return DBP_OK; }
+    if (option == DBP_OPT_OVERLAP_PREV) { c->pdl = value ? 1 : 0; return DBP_OK; }
     if (option == DBP_OPT_MODE) {
         if (value < 0 || value > 2) return fail(DBP_ERR_INVALID_ARG, "mode %lld (0 auto, 1 UxU, 2 SxS)", (long long)value);
         c->mode = (int)value;
@@ -676,6 +678,7 @@ extern "C" dbp_status dbp_detect_admm(dbp_ctx* c, const dbp_dims* d, const dbp_c
             xa = xargs_for(c, T);
         }
         bool launched = false;
+        L.pdl = c->pdl && !xc_on;
         KT("fused_ul", (launched = launch_fused_ul(L, sh.UP, false, dH, dy, sh.C_loc, sh.N, sh.S, sh.U, T, rho, gamma,
                                                    make_prox(reg, mod, sh.C, rho, N0, Es), modem_of(mod),
                                                    static_cast<float2*>(k.io[2].dev),
@@ -775,6 +778,7 @@ extern "C" dbp_status dbp_detect_cg(dbp_ctx* c, const dbp_dims* d, const dbp_cf3
     if (c->cg_tc && c->world == 1 && !c->force_split && !c->no_fused && sh.J == 1 && !xcons_active(c)) {
         // b1-b5 with the cluster-summed Gram on the tensor cores (long K = C * S): one kernel
         bool launched = false;
+        L.pdl = c->pdl;
         KT("cg_tc", (launched = launch_cg_tc(L, sh.UP, static_cast<const float2*>(k.io[0].dev),
                                              static_cast<const float2*>(k.io[1].dev), sh.C_loc, sh.N, sh.S, sh.U,
                                              sh.J, T, rho, modem_of(mod), a.x_hat, a.hard), cudaGetLastError()));
@@ -806,6 +810,7 @@ extern "C" dbp_status dbp_detect_cg(dbp_ctx* c, const dbp_dims* d, const dbp_cf3
             xa = xargs_for(c, T + 1);
         }
         bool launched = false;
+        L.pdl = c->pdl && !xc_on;
         KT("fused_cg", (launched = launch_fused_ul(L, sh.UP, true, static_cast<const float2*>(k.io[0].dev),
                                                    static_cast<const float2*>(k.io[1].dev), sh.C_loc, sh.N, sh.S,
                                                    sh.U, T, rho, 1.f, Prox{}, modem_of(mod), a.x_hat, a.hard,
@@ -928,6 +933,7 @@ extern "C" dbp_status dbp_beamform_admm(dbp_ctx* c, const dbp_dims* d, const dbp
             xa = xargs_for(c, T - 1);               // Alg. 3: T - 1 consensus rounds (P811)
         }
         bool launched = false;
+        L.pdl = c->pdl && !xc_on;
         KT("fused_dl", (launched = launch_fused_dl(L, sh.UP, a.Hd, a.s, sh.C_loc, sh.C, sh.N, sh.S, sh.U, T, rho,
                                                    gamma, a.a0, eps, a.x, xc_on ? &xa : nullptr),
                         cudaGetLastError()));

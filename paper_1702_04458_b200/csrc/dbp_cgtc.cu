@@ -151,6 +151,7 @@ k_cg_tc(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     constexpr int UP = 16;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     DBP_POISON_SMEM(smem_raw);
+    griddep_launch();
     unsigned char* const base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t4 = lane & 3;
@@ -260,6 +261,7 @@ k_cg_tc(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
         for (int jc = 0; jc < UP; ++jc) c_fma(w, grow[jc], pv[jc]);
         cg_update<UP>(x, r, p, rr, w, a.rho);
     }
+    griddep_wait();
     if (lane < UP && u < a.U) {
         a.x_hat[(size_t)n * a.U + u] = x;
         if (a.hard) a.hard[(size_t)n * a.U + u] = slice_bits(x, a.md);
@@ -284,7 +286,7 @@ bool launch_cg_tc(const LaunchCtx& L, int UP, const float2* H, const float2* y, 
         cudaGetLastError();
         return false;
     }
-    k_cg_tc<<<N, CGT_KS * 32, smem, L.stream>>>(tmH, tmY, a);
+    if (!launch_pdl(k_cg_tc, N, CGT_KS * 32, smem, L, tmH, tmY, a)) return false;
     L.count(1);
     return true;
 }

@@ -225,6 +225,14 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// Programmatic dependent launch (DBP_OPT_OVERLAP_PREV).  griddep_launch: this CTA lets the next
+// kernel on the stream start (it launches once every CTA of this grid has issued it or exited).
+// griddep_wait: block until the kernel before this one on the stream has completed and its memory
+// is visible -- issued before a solver's first global store, so outputs stay in stream order.
+// Both are no-ops for a kernel launched without the attribute.
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------------------ constellation
 // Gray QAM with Es = 1 (reading 17): per-axis levels
 // (2k - (m-1)) / sqrt(norm).  The decision is taken in fp32 with explicit

@@ -106,6 +106,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     constexpr bool DL = Z::DL, MF = Z::MF;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     DBP_POISON_SMEM(smem_raw);
+    griddep_launch();
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     // 1024-aligned base: [4 warp regions][mbarriers + CG queue (128 B)][Wp, Sv, Gp, Gs]
     unsigned char* const base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -193,6 +194,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     // takes antennas s, s + 32 (128B-swizzled [16 users][16 antennas] boxes); r of pair p is the
     // UP-line rl + p * rstride (ADMM-DL: the pair's pivot line; ZF-DL: the subcarrier's solution).
     auto dl_output_tc = [&](const float2* rl, int rstride, int n) {
+        griddep_wait();
         for (int p = 0; p < PW; ++p) {
             mbar_wait(&bar[st], phase);
             const unsigned char* hs = wbase + st * a.stg;
@@ -216,6 +218,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     auto dl_output = [&](const float2 (&r)[UP], int n, bool valid) {
         using GD = FoldStage<UP, true, false>;
         float2* xo = a.x + ((size_t)c * a.N + n) * a.S;
+        griddep_wait();
         for (int ch = 0; ch < nch; ++ch) {
             mbar_wait(&bar[st], phase);
             const float2* hq = reinterpret_cast<const float2*>(wbase + st * a.stg) + q * GD::NL * GD::HL;
@@ -423,6 +426,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                             cg_update<UP>(x, r, p, rr, w, a.rho);                        // lines 13-18
                         }
                     }
+                    griddep_wait();
                     if (lane < UP && u < a.U && nn < a.N) {
                         a.s_hat[(size_t)nn * a.U + u] = x;
                         if (a.hard) a.hard[(size_t)nn * a.U + u] = slice_bits(x, a.md);
@@ -526,6 +530,7 @@ k_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
                 }
                 consensus(t, w, true, sc);                                        // lines 18-19
             }
+            griddep_wait();
             if (warp == j * WPS && lane < UP) {
                 const int u = lane;
                 if (u < a.U && n < a.N) {
@@ -672,7 +677,7 @@ static bool launch_fz_t(const LaunchCtx& L, const float2* H, const float2* y, Fu
         return true;
     }
     const int grid = (persist >> SOLVER) & 1 ? std::min(ngroups, g_sms_fz * std::max(per_sm, 1)) : ngroups;
-    k<<<grid, Z::WARPS * 32, SMEM, L.stream>>>(tmH, tmY, a);
+    if (!launch_pdl(k, grid, Z::WARPS * 32, SMEM, L, tmH, tmY, a)) return false;
     L.count(1);
     return true;
 }

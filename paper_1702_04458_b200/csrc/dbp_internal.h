@@ -23,10 +23,35 @@ struct LaunchCtx {
     cudaStream_t stream;
     int* flag;              // device error flag (Cholesky pivot)
     int64_t* launches;      // host counter
+    int pdl = 0;            // launch with programmatic stream serialization (DBP_OPT_OVERLAP_PREV)
     void count(int n) const { if (launches) *launches += n; }
 };
 
 enum { PRE_ADMM_ = 0, PRE_BF_ = 1, PRE_CG_ = 2 };
+
+// <<<grid, block, smem, L.stream>>>, with programmatic stream serialization when L.pdl
+template <typename K, typename... Args>
+static inline bool launch_pdl(K kernel, int grid, int block, size_t smem, const LaunchCtx& L, Args... args) {
+    if (!L.pdl) {
+        kernel<<<grid, block, smem, L.stream>>>(args...);
+        return true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = L.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kernel, args...) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return true;
+}
 
 struct CgArgs {
     const float2* Gloc;   // [N][tri(UP)]

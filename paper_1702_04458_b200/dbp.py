@@ -28,6 +28,7 @@ OPT_DEVICE_CONSENSUS = 4
 OPT_MODE = 5
 OPT_GRAPHS = 6
 OPT_CG_TENSOR = 7
+OPT_OVERLAP_PREV = 8
 
 EXPORTS = ["dbp_get_unique_id", "dbp_ctx_create", "dbp_ctx_destroy", "dbp_set_option", "dbp_get_stats",
            "dbp_last_error", "dbp_workspace_bytes", "dbp_detect_admm", "dbp_detect_cg",

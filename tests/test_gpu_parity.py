@@ -592,11 +592,53 @@ def test_two_stream_schedule_matches_sequential(env):
     main = torch.cuda.current_stream()
     seq = run(main, main)
     conc = run(torch.cuda.Stream(), torch.cuda.Stream())
-    for a, b in zip(seq, conc):
-        for u, v in zip(a if isinstance(a, tuple) else (a,), b if isinstance(b, tuple) else (b,)):
-            assert torch.equal(u, v)
+    ctx.set_option(dbp.OPT_OVERLAP_PREV, 1)            # bench.py's default: one stream, overlapped launches
+    try:
+        ov = run(main, main)
+    finally:
+        ctx.set_option(dbp.OPT_OVERLAP_PREV, 0)
+    for other in (conc, ov):
+        for a, b in zip(seq, other):
+            for u, v in zip(a if isinstance(a, tuple) else (a,), b if isinstance(b, tuple) else (b,)):
+                assert torch.equal(u, v)
     x_ref = oracle.beamform_admm(Hd, s, rho=dl.rho, T=dl.T)
     assert rel(conc[1].cpu().numpy(), x_ref) < TOL
+
+
+def test_overlap_prev_keeps_store_order(env):
+    """DBP_OPT_OVERLAP_PREV: a solver may start inside its predecessor's last wave, but its stores
+    wait for it -- two overlapped calls into the same output buffers leave the second call's result
+    (write-after-write order kept), for every single-kernel solver."""
+    dbp, ctx, oracle, torch = env
+    cfg = synth.CONFIGS["C"].scaled(N=600)
+    frames = [synth.uplink_frame(cfg.scaled(seed=cfg.seed + k))[:2] for k in range(2)]
+    (Ha, ya), (Hb, yb) = [(torch.from_numpy(H).cuda(), torch.from_numpy(y).cuda()) for H, y in frames]
+    dl = synth.CONFIGS["D"].scaled(N=600)
+    dfr = [synth.downlink_frame(dl.scaled(seed=dl.seed + k)) for k in range(2)]
+    (Hda, sa), (Hdb, sb) = [(torch.from_numpy(H).cuda(), torch.from_numpy(s).cuda()) for H, s in dfr]
+    set_path(env, "fused")
+    ref_ul = dbp.detect_admm(ctx, Hb, yb, rho=cfg.rho, N0=cfg.N0, mod=cfg.mod, T=cfg.T)
+    ref_cg = dbp.detect_cg(ctx, Hb, yb, rho=cfg.N0, mod=cfg.mod, T=cfg.T)
+    ref_dl = dbp.beamform_admm(ctx, Hdb, sb, rho=dl.rho, T=dl.T)
+    ctx.sync()
+    s_hat, hard = torch.empty_like(ref_ul[0]), torch.empty_like(ref_ul[1])
+    x_hat, hard2 = torch.empty_like(ref_cg[0]), torch.empty_like(ref_cg[1])
+    xbf = torch.empty_like(ref_dl)
+    ctx.set_option(dbp.OPT_OVERLAP_PREV, 1)
+    try:
+        for _ in range(3):
+            dbp.detect_admm(ctx, Ha, ya, rho=cfg.rho, N0=cfg.N0, mod=cfg.mod, T=cfg.T, s_hat=s_hat, hard=hard)
+            dbp.detect_admm(ctx, Hb, yb, rho=cfg.rho, N0=cfg.N0, mod=cfg.mod, T=cfg.T, s_hat=s_hat, hard=hard)
+            dbp.detect_cg(ctx, Ha, ya, rho=cfg.N0, mod=cfg.mod, T=cfg.T, x_hat=x_hat, hard=hard2)
+            dbp.detect_cg(ctx, Hb, yb, rho=cfg.N0, mod=cfg.mod, T=cfg.T, x_hat=x_hat, hard=hard2)
+            dbp.beamform_admm(ctx, Hda, sa, rho=dl.rho, T=dl.T, x=xbf)
+            dbp.beamform_admm(ctx, Hdb, sb, rho=dl.rho, T=dl.T, x=xbf)
+            ctx.sync()
+            assert torch.equal(s_hat, ref_ul[0]) and torch.equal(hard, ref_ul[1])
+            assert torch.equal(x_hat, ref_cg[0]) and torch.equal(hard2, ref_cg[1])
+            assert torch.equal(xbf, ref_dl)
+    finally:
+        ctx.set_option(dbp.OPT_OVERLAP_PREV, 0)
 
 
 @pytest.mark.parametrize("host", [False, True])
