@@ -775,7 +775,8 @@ extern "C" dbp_status dbp_detect_cg(dbp_ctx* c, const dbp_dims* d, const dbp_cf3
     a.N = sh.N; a.J = sh.J; a.U = sh.U; a.T = T; a.rho = rho;
     a.md = modem_of(mod);
 
-    if (c->cg_tc && c->world == 1 && !c->force_split && !c->no_fused && sh.J == 1 && !xcons_active(c)) {
+    if (c->cg_tc && c->world == 1 && !c->force_split && !c->no_fused && !xcons_active(c) &&
+        cg_tc_ok(sh.UP, sh.J, sh.N, sh.C_loc, sh.S)) {
         // b1-b5 with the cluster-summed Gram on the tensor cores (long K = C * S): one kernel
         bool launched = false;
         L.pdl = c->pdl;
@@ -822,16 +823,24 @@ extern "C" dbp_status dbp_detect_cg(dbp_ctx* c, const dbp_dims* d, const dbp_cf3
         }
         if (xc_on) return fail(DBP_ERR_CUDA, "fused CG launch with device consensus failed (rank %d)", c->rank);
     }
-    const std::vector<uint64_t> key{12, (uint64_t)sh.C, (uint64_t)sh.S, (uint64_t)sh.U, (uint64_t)sh.N, (uint64_t)sh.J, (uint64_t)T, (uint64_t)sh.ss, (uint64_t)c->force_split, (uint64_t)c->no_fused, (uint64_t)mod, fbits(rho), pbits(k.io[0].dev), pbits(k.io[1].dev),
+    const std::vector<uint64_t> key{12, (uint64_t)sh.C, (uint64_t)sh.S, (uint64_t)sh.U, (uint64_t)sh.N, (uint64_t)sh.J, (uint64_t)T, (uint64_t)sh.ss, (uint64_t)c->force_split, (uint64_t)c->no_fused, (uint64_t)c->cg_tc, (uint64_t)mod, fbits(rho), pbits(k.io[0].dev), pbits(k.io[1].dev),
                                     pbits(k.io[2].dev), pbits(k.io[3].dev), pbits(k.ws)};
     st = graphed(c, k.host, s, key, [&](cudaStream_t s) -> dbp_status {
     LaunchCtx L{s, c->d_flag, &c->launches};
     dbp_status st;
-    // b1: per-pair Gram H_c^H H_c and matched filter H_c^H y_c, then the
-    // per-GPU sums (G_loc, local y^MRC) in fixed cluster order.
-    KT("pre_cg", launch_prelr(L, sh.UP, 0, static_cast<const float2*>(k.io[0].dev),
-                              static_cast<const float2*>(k.io[1].dev), sh.S, sh.U, sh.J, sh.pairs(), 0.f, Gp, mf));
-    KT("cg_gsum", launch_cg_gsum(L, sh.UP, Gp, mf, sh.C_loc, sh.N, sh.J, const_cast<float2*>(a.Gloc), a.wbuf));
+    // b1: the per-GPU sums G_loc = sum_c H_c^H H_c and local y^MRC -- one tensor-core pass over H
+    // (k_cgg_tc), else per-pair Grams and matched filters summed in fixed cluster order.
+    bool gtc = false;
+    if (c->cg_tc && cgg_tc_ok(sh.UP, sh.J, sh.N, sh.C_loc, sh.S, sh.U))
+        KT("cgg_tc", (gtc = launch_cgg_tc(L, sh.UP, static_cast<const float2*>(k.io[0].dev),
+                                          static_cast<const float2*>(k.io[1].dev), sh.C_loc, sh.N, sh.S, sh.U,
+                                          const_cast<float2*>(a.Gloc), a.wbuf),
+                      cudaGetLastError()));
+    if (!gtc) {
+        KT("pre_cg", launch_prelr(L, sh.UP, 0, static_cast<const float2*>(k.io[0].dev),
+                                  static_cast<const float2*>(k.io[1].dev), sh.S, sh.U, sh.J, sh.pairs(), 0.f, Gp, mf));
+        KT("cg_gsum", launch_cg_gsum(L, sh.UP, Gp, mf, sh.C_loc, sh.N, sh.J, const_cast<float2*>(a.Gloc), a.wbuf));
+    }
     const size_t nw = (size_t)sh.N * sh.J * sh.UP;
     if ((st = allreduce(c, a.wbuf, nw, s))) return st;              // line 4: y^MRC consensus
     if (c->world == 1 && !c->force_split) {

@@ -268,10 +268,14 @@ k_cg_tc(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     }
 }
 
+bool cg_tc_ok(int UP, int J, int N, int C, int S) {
+    return UP == 16 && J == 1 && N > 0 && C > 0 && S > 0 && S <= 64;
+}
+
 // CG-UL at world 1, N_sym = 1, 9 <= U <= 16 (UP = 16), S <= 64: one kernel (false: not taken)
 bool launch_cg_tc(const LaunchCtx& L, int UP, const float2* H, const float2* y, int C, int N, int S, int U, int J,
                   int T, float rho, Modem md, float2* x_hat, uint8_t* hard) {
-    if (UP != 16 || J != 1 || N <= 0 || C <= 0 || S <= 0 || S > 64) return false;
+    if (!cg_tc_ok(UP, J, N, C, S)) return false;
     CgTcArgs a{};
     a.N = N; a.C = C; a.S = S; a.U = U; a.T = T; a.rho = rho; a.md = md; a.x_hat = x_hat; a.hard = hard;
     a.S16 = S <= 16 ? 16 : (S + 31) / 32 * 32;              // antenna rows per cluster: whole 32-row groups

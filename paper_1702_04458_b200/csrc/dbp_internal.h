@@ -108,6 +108,12 @@ bool launch_fused_ulj(const LaunchCtx& L, int UP, bool cg, const float2* H, cons
 // CG-UL at world 1, N_sym = 1, UP = 16: the cluster-summed Gram on the tensor cores (dbp_cgtc.cu)
 bool launch_cg_tc(const LaunchCtx& L, int UP, const float2* H, const float2* y, int C, int N, int S, int U, int J,
                   int T, float rho, Modem md, float2* x_hat, uint8_t* hard);
+// G_loc = sum_c H_c^H H_c and y^MRC_loc over the rank's clusters on the tensor cores (dbp_cgg.cu;
+// J = 1, UP = 16 / 32, U even, S <= 64): the CG split path's preprocessing
+bool launch_cgg_tc(const LaunchCtx& L, int UP, const float2* H, const float2* y, int C, int N, int S, int U,
+                   float2* G, float2* mrc);
+bool cgg_tc_ok(int UP, int J, int N, int C, int S, int U);
+bool cg_tc_ok(int UP, int J, int N, int C, int S);
 size_t prelr_smem(int UP, int S, int U, int J, bool ul);
 bool launch_prefold(const LaunchCtx& L, int UP, int mode, const float2* H, const float2* y, int S, int U, int J,
                     long npairs, float delta, float2* Gout, float2* vout);

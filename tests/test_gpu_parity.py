@@ -192,6 +192,10 @@ SMALL_CG = [
     synth.Config("tc40", "cg_ul", C=3, S=40, U=12, N=9, mod="qam64", snr_db=25),
     synth.Config("tc64", "cg_ul", C=5, S=64, U=16, N=7, mod="qam16", snr_db=20),
     synth.Config("tc1", "cg_ul", C=1, S=32, U=16, N=5, mod="qpsk", snr_db=15),
+    # k_cgg_tc (the split / two-kernel paths' G_loc at UP = 16 / 32): second user half partly
+    # out of bounds, odd C, S padded to 32 / 64 rows
+    synth.Config("g20", "cg_ul", C=5, S=24, U=20, N=9, mod="qam16", snr_db=20),
+    synth.Config("g30", "cg_ul", C=3, S=64, U=30, N=6, mod="qam64", snr_db=25),
 ]
 
 
@@ -212,13 +216,14 @@ def test_cg_iteration_counts(env, T):
 
 
 @pytest.mark.parametrize("spread", [-40, 24])
-def test_cg_cluster_scales(env, spread):
+@pytest.mark.parametrize("U", [16, 32])
+def test_cg_cluster_scales(env, spread, U):
     """Clusters at powers of two apart (2^(spread * c / C), the largest at 1 so that the FP32 CG
     recursion itself stays in range): the tensor-core Gram's per-group fp16 scaling must hold the
     paper's 1e-4 bar whatever the dynamic range across clusters -- small clusters first (24) or
     last (-40)."""
     dbp, ctx, oracle, torch = env
-    cfg = synth.CONFIGS["C"].scaled(N=11, C=8)
+    cfg = synth.CONFIGS["C"].scaled(N=11, C=8) if U == 16 else synth.CONFIGS["E"].scaled(N=5, C=8)
     H, y, _ = synth.uplink_frame(cfg)
     f = np.float32(2.0) ** (spread * np.arange(cfg.C) / cfg.C)
     f = f / f.max()
