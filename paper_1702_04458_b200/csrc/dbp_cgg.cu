@@ -46,11 +46,9 @@ struct CGG {
     static constexpr int XW = NT * 4 + 2 * NMF;              // exchange floats per lane
     static constexpr int TRI = UP * (UP + 1) / 2;
     __host__ __device__ static size_t warp_bytes(int pitch) { return (size_t)CGG_NST * pitch + 1024; }
-    static size_t smem(int pitch) {
-        // ring (+ mbarriers in the 1024-B tail) per warp | partials of warps 1.. | Z [UP][UP+1] | y^MRC [UP]
-        return 1024 + CGG_KS * warp_bytes(pitch) + (size_t)(CGG_KS - 1) * XW * 32 * 4 + (size_t)UP * (UP + 1) * 8 +
-               UP * 8;
-    }
+    // ring (+ mbarriers in the 1024-B tail) per warp; after the stream a warp's partials go to its own
+    // ring, and warp 0's ring holds Z [UP][UP+1] + y^MRC [UP]
+    static size_t smem(int pitch) { return 1024 + CGG_KS * warp_bytes(pitch); }
 };
 
 __device__ __forceinline__ unsigned h2x(unsigned a) {          // 2 a, exact in fp16
@@ -109,9 +107,11 @@ k_cgg_tc(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtens
     const int R = a.R, pitch = a.pitch;
     unsigned char* const ring = base + (size_t)warp * Q::warp_bytes(pitch);           // 1024-aligned stages
     uint64_t* const bar = reinterpret_cast<uint64_t*>(ring + (size_t)CGG_NST * pitch);
-    float* const xch = reinterpret_cast<float*>(base + (size_t)CGG_KS * Q::warp_bytes(pitch));
-    float2* const zs = reinterpret_cast<float2*>(xch + (CGG_KS - 1) * Q::XW * 32);    // [UP][UP + 1]
+    float2* const zs = reinterpret_cast<float2*>(base);                               // [UP][UP + 1], warp 0's ring
     float2* const ms = zs + UP * (UP + 1);                                             // [UP]
+    // a ring holds >= CGG_NST stages of >= UH * 4096 + 1024 bytes (32 rows of UH halves, y, 1024-B pitch)
+    static_assert((UP * (UP + 1) + UP) * 8 <= CGG_NST * (UH * 4096 + 1024) &&
+                  Q::XW * 32 * 4 <= CGG_NST * (UH * 4096 + 1024), "hand-off fits a ring");
     const int n = blockIdx.x;
     const int nmine = (a.nstages - warp + CGG_KS - 1) / CGG_KS;
 
@@ -235,7 +235,7 @@ k_cgg_tc(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtens
             mr[h][uh][1] = mfb[h][uh].x - mfb[h][uh].y;
         }
     if (warp > 0) {
-        float* xw = xch + (warp - 1) * Q::XW * 32;
+        float* xw = reinterpret_cast<float*>(ring);                         // the warp's own (drained) ring
 #pragma unroll
         for (int q = 0; q < NT * 4; ++q) xw[q * 32 + lane] = T[q >> 2][q & 3];
 #pragma unroll
@@ -243,8 +243,9 @@ k_cgg_tc(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtens
     }
     DBP_SYNCTHREADS();
     if (warp == 0) {
+        DBP_SYNCWARP();
         for (int w = 1; w < CGG_KS; ++w) {
-            const float* xw = xch + (w - 1) * Q::XW * 32;
+            const float* xw = reinterpret_cast<const float*>(base + (size_t)w * Q::warp_bytes(pitch));
 #pragma unroll
             for (int q = 0; q < NT * 4; ++q) T[q >> 2][q & 3] += xw[q * 32 + lane];
 #pragma unroll
