@@ -1021,8 +1021,15 @@ extern "C" dbp_status dbp_detect_mmse(dbp_ctx* c, const dbp_dims* d, const dbp_c
     float2* mf = reinterpret_cast<float2*>(k.ws + Lw.off[1]);
     float2* Gloc = reinterpret_cast<float2*>(k.ws + Lw.off[2]);
     float2* b = reinterpret_cast<float2*>(k.ws + Lw.off[3]);
-    KT("pre_cg", launch_prelr(L, sh.UP, 0, dH, dy, sh.S, sh.U, sh.J, sh.pairs(), 0.f, Gp, mf));
-    KT("cg_gsum", launch_cg_gsum(L, sh.UP, Gp, mf, sh.C_loc, sh.N, sh.J, Gloc, b));
+    // G = sum_c H_c^H H_c and H^H y over the rank's clusters: one tensor-core pass over H (k_cgg_tc,
+    // the CG preprocessing), else per-pair Grams summed in fixed cluster order
+    bool gtc = false;
+    if (c->cg_tc && cgg_tc_ok(sh.UP, sh.J, sh.N, sh.C_loc, sh.S, sh.U))
+        KT("cgg_tc", (gtc = launch_cgg_tc(L, sh.UP, dH, dy, sh.C_loc, sh.N, sh.S, sh.U, Gloc, b), cudaGetLastError()));
+    if (!gtc) {
+        KT("pre_cg", launch_prelr(L, sh.UP, 0, dH, dy, sh.S, sh.U, sh.J, sh.pairs(), 0.f, Gp, mf));
+        KT("cg_gsum", launch_cg_gsum(L, sh.UP, Gp, mf, sh.C_loc, sh.N, sh.J, Gloc, b));
+    }
     const size_t ng = (size_t)sh.N * sh.UP * (sh.UP + 1) / 2, nb = (size_t)sh.N * sh.J * sh.UP;
     if ((st = allreduce(c, Gloc, ng, s, false))) return st;             // gather the whole array's Gram
     if ((st = allreduce(c, b, nb, s, false))) return st;                // and matched filter
