@@ -48,7 +48,9 @@ __host__ __device__ inline size_t cgtc_warp_bytes(int R) {
     return (b + 1023) / 1024 * 1024;
 }
 static size_t cgtc_smem(int R) {
-    return 1024 + CGT_KS * cgtc_warp_bytes(R) + (CGT_KS - 1) * 20 * 32 * 4 + 16 * 17 * 8 + 16 * 8;
+    // the hand-off (a warp's partials: its own drained ring; Z' scratch + CG line: warp 0's ring) needs
+    // no memory of its own: 10 CTAs (20 warps) per SM
+    return 1024 + CGT_KS * cgtc_warp_bytes(R);
 }
 
 __device__ __forceinline__ unsigned hadd2u(unsigned a, unsigned b) {
@@ -159,9 +161,9 @@ k_cg_tc(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     unsigned char* const ring = base + (size_t)warp * cgtc_warp_bytes(R);   // 1024-aligned stages
     float2* const yring = reinterpret_cast<float2*>(ring + (size_t)CGT_NST * R * 128);
     uint64_t* const bar = reinterpret_cast<uint64_t*>(yring + (size_t)CGT_NST * R);
-    float* const xch = reinterpret_cast<float*>(base + (size_t)CGT_KS * cgtc_warp_bytes(R));
-    float2* const zs = reinterpret_cast<float2*>(xch + (CGT_KS - 1) * 20 * 32);
+    float2* const zs = reinterpret_cast<float2*>(base);    // warp 0's ring, after the stream
     float2* const P = zs + 16 * 17;
+    static_assert((16 * 17 + 16) * 8 <= CGT_NST * 32 * 128 && 20 * 32 * 4 <= CGT_NST * 32 * 128, "hand-off fits");
     const int n = blockIdx.x;
     const int nmine = (a.nstages - warp + CGT_KS - 1) / CGT_KS;   // this warp: stages warp, warp + KS, ..
 
@@ -189,7 +191,11 @@ k_cg_tc(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
         mbar_wait(&bar[sl], (uint32_t)((i / CGT_NST) & 1));
         const unsigned char* stage = ring + (size_t)sl * R * 128;
         const float2* yv = yring + (size_t)sl * R;
-        for (int gq = 0; gq < R / 32; ++gq) cgtc_group(acc, mfa, mfb, stage, yv, 2 * gq, g, t4);
+#ifndef DBP_EXP_CGTC_NOCOMP
+#define DBP_EXP_CGTC_NOCOMP 0   // experiment only: stream the stages without the Gram (wrong results)
+#endif
+        if (!DBP_EXP_CGTC_NOCOMP)
+            for (int gq = 0; gq < R / 32; ++gq) cgtc_group(acc, mfa, mfb, stage, yv, 2 * gq, g, t4);
         DBP_SYNCWARP();                                     // every lane's reads of the slot are done
         if (lane == 0 && i + CGT_NST < nmine) {
             fence_proxy_async();
@@ -199,7 +205,7 @@ k_cg_tc(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
 
     // warps 1.. hand their partials to warp 0, which adds them in warp order
     if (warp > 0) {
-        float* xw = xch + (warp - 1) * 20 * 32;
+        float* xw = reinterpret_cast<float*>(ring);      // the warp's own drained ring
 #pragma unroll
         for (int q = 0; q < 16; ++q) xw[q * 32 + lane] = acc[q >> 2][q & 3];
 #pragma unroll
@@ -211,7 +217,7 @@ k_cg_tc(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     DBP_SYNCTHREADS();
     if (warp > 0) return;
     for (int w = 1; w < CGT_KS; ++w) {
-        const float* xw = xch + (w - 1) * 20 * 32;
+        const float* xw = reinterpret_cast<const float*>(base + (size_t)w * cgtc_warp_bytes(R));
 #pragma unroll
         for (int q = 0; q < 16; ++q) acc[q >> 2][q & 3] += xw[q * 32 + lane];
 #pragma unroll
@@ -279,7 +285,10 @@ bool launch_cg_tc(const LaunchCtx& L, int UP, const float2* H, const float2* y, 
     CgTcArgs a{};
     a.N = N; a.C = C; a.S = S; a.U = U; a.T = T; a.rho = rho; a.md = md; a.x_hat = x_hat; a.hard = hard;
     a.S16 = S <= 16 ? 16 : (S + 31) / 32 * 32;              // antenna rows per cluster: whole 32-row groups
-    a.R = std::max(32, a.S16);                              // rows per stage: 32 (1 or 2 clusters) or 64
+#ifndef DBP_CGT_RMIN
+#define DBP_CGT_RMIN 32
+#endif
+    a.R = std::max(DBP_CGT_RMIN, a.S16);                    // rows per stage: 32 (1 or 2 clusters) or 64
     a.CB = a.R / a.S16;                                     // clusters per stage
     a.nstages = (C + a.CB - 1) / a.CB;                      // clusters >= C zero-filled by the TMA
     CUtensorMap tmH{}, tmY{};

@@ -25,7 +25,7 @@ NAMES = [(r"k_fused<\d+, 3>", "fused_mmse"), (r"k_fused<\d+, 4>", "fused_zf"), (
          (r"k_gram<\d+, 0, 1", "gram_ul"), (r"k_gram<\d+, 1,", "gram_dl"), (r"k_inv_ul", "inv_ul"),
          (r"k_inv_dl", "inv_dl"), (r"k_admm_gj", "admm_fused"), (r"k_bf_gj", "bf_fused"),
          (r"k_admm_it", "admm_step"), (r"k_bf_it", "bf_step"), (r"k_cg_gsum", "cg_gsum"),
-         (r"k_cg_it<\d+, 1", "cg_fused"), (r"k_cg_tc", "cg_tc"), (r"k_cg_it<\d+, 0", "cg_step"), (r"k_prox_out", "prox_out"),
+         (r"k_cg_it<\d+, 1", "cg_fused"), (r"k_cg_tc", "cg_tc"), (r"k_cgg_tc", "cgg_tc"), (r"k_cg_it<\d+, 0", "cg_step"), (r"k_prox_out", "prox_out"),
          (r"k_mf", "mf"), (r"k_slice", "slice")]
 
 
@@ -53,7 +53,8 @@ def launches(tag, path):
     BASE = ("fused_mmse", "fused_zf", "central_solve", "zf_out")
     tot = sum(sum(v) for k, v in ours.items() if short(k) not in BASE) or 1.0
     lines = [f"# {tag}: ncu launch list (gpu__time_duration.sum, --clock-control none)", "",
-             "Serialised, cold-cache per-launch times of `bench.py --steps 3 --warmup 3` (all launches of the",
+             "Serialised, cold-cache per-launch times of `" + os.environ.get(
+                 "LAUNCH_CMD", "bench.py --steps 3 --warmup 3") + "` (all launches of the",
              "process, libdbp kernels only below).  Compare SHARES with bench.py's live event timing, not",
              "absolute times.", "", "| kernel | launches | mean us | share of the step's libdbp time |", "|---|---|---|---|"]
     for k, v in sorted(ours.items(), key=lambda kv: -sum(kv[1])):
