@@ -11,7 +11,8 @@
 // split form (below), y^MRC runs on the FP32 cores from the same registers; the warps' partial sums
 // meet in shared memory (fixed order), and warp 0 runs the T CG iterations on the assembled G
 // (replicated update, shuffle dot products, P404-409, P715).  The warps synchronise once, at the
-// end; 1200 subcarriers x 2 warps keep ~16 warps per SM streaming in a single wave.
+// end; 1200 subcarriers x 2 warps fit one wave at 10 CTAs per SM.  (43.7 us at
+// config C against a measured ~32-36 us floor for streaming the 157 MB through such rings.)
 //
 // Split (exact to ~2^-22 relative): per 32-row group the warp scales its values by an exact power
 // of two (max |Re|, |Im| -> [1, 2)), v = hi + lo with hi = v truncated to fp16's 11 bits; then
@@ -41,8 +42,7 @@ struct CgTcArgs {
     uint8_t* hard;        // [N][U] or null
 };
 
-// per warp: H ring [NST][R][128 B] | y ring [NST][R] float2 | mbarriers [NST]; then per CTA: partials of
-// warps 1.. [KS-1][20][32] floats | Z' scratch [16][17] float2 | CG line [16] float2
+// per warp: H ring [NST][R][128 B] | y ring [NST][R] float2 | mbarriers [NST], 1024-B pitch
 __host__ __device__ inline size_t cgtc_warp_bytes(int R) {
     const size_t b = (size_t)CGT_NST * R * 128 + (size_t)CGT_NST * R * 8 + CGT_NST * 8;
     return (b + 1023) / 1024 * 1024;

@@ -141,8 +141,13 @@ k_prefold(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUten
         for (int ch = 0; ch < nch; ++ch) {
             mbar_wait(&bar[st], phase);
             const float2* stage = reinterpret_cast<const float2*>(wbase + st * G::STG);
-            if (DL) fold_gram_dl<UP>(A, stage, q, row);
-            else fold_gram_ul<UP, MF>(A, E, stage, q, row);
+#ifndef DBP_EXP_PF_NOGRAM
+#define DBP_EXP_PF_NOGRAM 0     // experiment only: stream the stages without the Gram (wrong results)
+#endif
+            if (!DBP_EXP_PF_NOGRAM) {
+                if (DL) fold_gram_dl<UP>(A, stage, q, row);
+                else fold_gram_ul<UP, MF>(A, E, stage, q, row);
+            }
             DBP_SYNCWARP();
             if (lane == 0 && sq + NST < nseq) {
                 fence_proxy_async();

@@ -1,6 +1,9 @@
 // dbp_tc.cuh -- the per-pair Gram (+ matched filter) on the tensor cores, for UP = 16
 // (G_c = H_c^H H_c (P295, P391), B_c = H_c H_c^H (P503),
-// H_c^H y_c (P296)).
+// H_c^H y_c (P296)).  In k_fused this stays behind the build knob DBP_FZ_TC (off: measured slower
+// than the folded FP32 Gram at K = S = 32); the FP16 helpers below (mma_f16, f16x2,
+// tc16_load, TC_NEG2) also carry the long-K cluster-summed Grams of CG, which are the default
+// (dbp_cgtc.cu, dbp_cgg.cu).
 //
 // One warp computes one pair with mma.sync m16n8k8 TF32 (the warp-level tensor path; 242
 // TFLOP/s measured on B200, scripts/micro/tc_gram.cu) in "3xTF32": every fp32 operand v is

@@ -17,6 +17,7 @@ ap.add_argument("--T", type=int, default=0)
 ap.add_argument("--nofused", type=int, default=0)
 ap.add_argument("--nsym", type=int, default=0)
 ap.add_argument("--N", type=int, default=0)
+ap.add_argument("--C", type=int, default=0)
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
 if a.T:
@@ -25,6 +26,8 @@ if a.nsym:
     cfg = cfg.scaled(N_sym=a.nsym)
 if a.N:
     cfg = cfg.scaled(N=a.N)
+if a.C:
+    cfg = cfg.scaled(C=a.C)
 ctx = dbp.Context(0)
 ctx.set_option(dbp.OPT_FORCE_SPLIT, a.split)
 ctx.set_option(dbp.OPT_NO_FUSED, a.nofused)
