@@ -5,8 +5,8 @@
 // sum over clusters, G = sum_c H_c^H H_c (P416 footnote) and y^MRC = sum_c H_c^H y_c (line 3), i.e.
 // one Gram with K = C * S antennas per subcarrier (1024 at configs B-D scale).  Unlike the per-pair
 // Grams of ADMM (K = 32, dbp_tc.cuh: measured slower than FP32 there), this long-K contraction is
-// what the tensor cores are for.  One CTA of CGT_KS warps owns one subcarrier: each warp streams every
-// CGT_KS-th stage of the subcarrier's clusters through its own TMA ring (R = 32 or 64 antenna rows x
+// what the tensor cores are for.  KS warps (2, or 1 for short K) own one subcarrier: each warp streams
+// every KS-th stage of the subcarrier's clusters through its own TMA ring (R = 32 or 64 antenna rows x
 // 16 users per stage, 128B swizzle), each 32-row group runs mma.sync m16n8k16 FP16 in dbp_tc.cuh's
 // split form (below), y^MRC runs on the FP32 cores from the same registers; the warps' partial sums
 // meet in shared memory (fixed order), and warp 0 runs the T CG iterations on the assembled G
@@ -32,7 +32,7 @@
 
 namespace dbp {
 
-constexpr int CGT_KS = 2, CGT_NST = 2;   // warps per subcarrier (K split), ring stages per warp
+constexpr int CGT_WARPS = 2, CGT_NST = 2;   // warps per CTA, ring stages per warp
 
 struct CgTcArgs {
     int N, C, S, U, T, S16, CB, R, nstages;
@@ -48,9 +48,9 @@ __host__ __device__ inline size_t cgtc_warp_bytes(int R) {
     return (b + 1023) / 1024 * 1024;
 }
 static size_t cgtc_smem(int R) {
-    // the hand-off (a warp's partials: its own drained ring; Z' scratch + CG line: warp 0's ring) needs
-    // no memory of its own: 10 CTAs (20 warps) per SM
-    return 1024 + CGT_KS * cgtc_warp_bytes(R);
+    // the hand-off (a warp's partials: its own drained ring; Z' scratch + CG line: the subcarrier's
+    // first warp's ring) needs no memory of its own: 10 CTAs (20 warps) per SM
+    return 1024 + CGT_WARPS * cgtc_warp_bytes(R);
 }
 
 __device__ __forceinline__ unsigned hadd2u(unsigned a, unsigned b) {
@@ -148,9 +148,12 @@ __device__ __forceinline__ void cgtc_group(float (&acc)[4][4], float2 (&mfa)[2],
         for (int e = 0; e < 4; ++e) acc[q4][e] = fmaf(st[q4][e], us, acc[q4][e]);
 }
 
-__global__ void __launch_bounds__(CGT_KS * 32, 9)
+// KS warps per subcarrier (K split; 2 at configs C / D, 1 when a subcarrier has few stages, e.g.
+// config B: no hand-off, and the CTA's two warps solve two subcarriers independently)
+template <int KS>
+__global__ void __launch_bounds__(CGT_WARPS * 32, 9)
 k_cg_tc(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmY, CgTcArgs a) {
-    constexpr int UP = 16;
+    constexpr int UP = 16, SPC = CGT_WARPS / KS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     DBP_POISON_SMEM(smem_raw);
     griddep_launch();
@@ -161,14 +164,17 @@ k_cg_tc(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
     unsigned char* const ring = base + (size_t)warp * cgtc_warp_bytes(R);   // 1024-aligned stages
     float2* const yring = reinterpret_cast<float2*>(ring + (size_t)CGT_NST * R * 128);
     uint64_t* const bar = reinterpret_cast<uint64_t*>(yring + (size_t)CGT_NST * R);
-    float2* const zs = reinterpret_cast<float2*>(base);    // warp 0's ring, after the stream
+    const int wk = warp % KS;                               // the warp's share of its subcarrier's stages
+    unsigned char* const lead = base + (size_t)(warp - wk) * cgtc_warp_bytes(R);   // the subcarrier's first warp
+    float2* const zs = reinterpret_cast<float2*>(lead);    // its ring, after the stream
     float2* const P = zs + 16 * 17;
     static_assert((16 * 17 + 16) * 8 <= CGT_NST * 32 * 128 && 20 * 32 * 4 <= CGT_NST * 32 * 128, "hand-off fits");
-    const int n = blockIdx.x;
-    const int nmine = (a.nstages - warp + CGT_KS - 1) / CGT_KS;   // this warp: stages warp, warp + KS, ..
+    const int n = blockIdx.x * SPC + warp / KS;
+    if (n >= a.N) return;                                   // KS = 1 only (warp-uniform; no CTA barrier then)
+    const int nmine = (a.nstages - wk + KS - 1) / KS;      // this warp: stages wk, wk + KS, ..
 
     auto issue = [&](int j) {                               // the warp's j-th stage
-        const int sl = j % CGT_NST, c0 = (warp + j * CGT_KS) * a.CB;
+        const int sl = j % CGT_NST, c0 = (wk + j * KS) * a.CB;
         mbar_arrive_expect_tx(&bar[sl], (uint32_t)(R * (128 + 8)));
         tma_load4(ring + (size_t)sl * R * 128, &tmH, 0, 0, n, c0, &bar[sl]);
         tma_load4(yring + (size_t)sl * R, &tmY, 0, 0, n, c0, &bar[sl]);
@@ -203,21 +209,23 @@ k_cg_tc(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
         }
     }
 
-    // warps 1.. hand their partials to warp 0, which adds them in warp order
-    if (warp > 0) {
-        float* xw = reinterpret_cast<float*>(ring);      // the warp's own drained ring
+    // warps 1.. of the subcarrier hand their partials to its first warp, which adds them in warp order
+    if constexpr (KS > 1) {
+        if (wk > 0) {
+            float* xw = reinterpret_cast<float*>(ring);  // the warp's own drained ring
 #pragma unroll
-        for (int q = 0; q < 16; ++q) xw[q * 32 + lane] = acc[q >> 2][q & 3];
+            for (int q = 0; q < 16; ++q) xw[q * 32 + lane] = acc[q >> 2][q & 3];
 #pragma unroll
-        for (int uh = 0; uh < 2; ++uh) {
-            xw[(16 + 2 * uh) * 32 + lane] = mfa[uh].x + mfa[uh].y;
-            xw[(17 + 2 * uh) * 32 + lane] = mfb[uh].x - mfb[uh].y;
+            for (int uh = 0; uh < 2; ++uh) {
+                xw[(16 + 2 * uh) * 32 + lane] = mfa[uh].x + mfa[uh].y;
+                xw[(17 + 2 * uh) * 32 + lane] = mfb[uh].x - mfb[uh].y;
+            }
         }
+        DBP_SYNCTHREADS();
+        if (wk > 0) return;
     }
-    DBP_SYNCTHREADS();
-    if (warp > 0) return;
-    for (int w = 1; w < CGT_KS; ++w) {
-        const float* xw = reinterpret_cast<const float*>(base + (size_t)w * cgtc_warp_bytes(R));
+    for (int w = 1; w < KS; ++w) {
+        const float* xw = reinterpret_cast<const float*>(lead + (size_t)w * cgtc_warp_bytes(R));
 #pragma unroll
         for (int q = 0; q < 16; ++q) acc[q >> 2][q & 3] += xw[q * 32 + lane];
 #pragma unroll
@@ -262,9 +270,10 @@ k_cg_tc(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtenso
         DBP_SYNCWARP();
         float2 pv[UP];
         read_vec<UP>(P, pv);
-        float2 w = make_float2(0.f, 0.f);
+        float2 w4[4] = {};                                  // four partial sums: short FMA chains
 #pragma unroll
-        for (int jc = 0; jc < UP; ++jc) c_fma(w, grow[jc], pv[jc]);
+        for (int jc = 0; jc < UP; ++jc) c_fma(w4[jc & 3], grow[jc], pv[jc]);
+        const float2 w = c_add(c_add(w4[0], w4[1]), c_add(w4[2], w4[3]));
         cg_update<UP>(x, r, p, rr, w, a.rho);
     }
     griddep_wait();
@@ -295,11 +304,13 @@ bool launch_cg_tc(const LaunchCtx& L, int UP, const float2* H, const float2* y, 
     if (!make_map4(&tmH, H, U, S, N, C, 16, a.S16, 1, a.CB, true)) return false;
     if (!make_map4(&tmY, y, S, 1, N, C, a.S16, 1, 1, a.CB)) return false;
     const size_t smem = cgtc_smem(a.R);
-    if (cudaFuncSetAttribute(k_cg_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    const int ks = a.nstages >= 8 ? 2 : 1;                 // K split only when each warp keeps >= 4 stages
+    auto k = ks == 2 ? k_cg_tc<2> : k_cg_tc<1>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
-    if (!launch_pdl(k_cg_tc, N, CGT_KS * 32, smem, L, tmH, tmY, a)) return false;
+    if (!launch_pdl(k, (N + CGT_WARPS / ks - 1) / (CGT_WARPS / ks), CGT_WARPS * 32, smem, L, tmH, tmY, a)) return false;
     L.count(1);
     return true;
 }
