@@ -858,7 +858,8 @@ def main():
         launches = st1["kernel_launches"] - st0["kernel_launches"]
         line = {"metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_step_sequential": ms_seq,
-                "schedule": ("concurrent, one stream per lane: " + " | ".join(" then ".join(l) for l in plan)
+                "schedule": (("one stream: " if len(plan) == 1 else "concurrent, one stream per lane: ")
+                             + " | ".join(" then ".join(l) for l in plan)
                              + ("; a solver may start in its lane predecessor's last wave (DBP_OPT_OVERLAP_PREV)"
                                 if overlap else "")
                              if concurrent else "sequential on one stream"),
