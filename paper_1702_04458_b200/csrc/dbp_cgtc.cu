@@ -141,7 +141,10 @@ __device__ __forceinline__ void cgtc_group(float (&acc)[4][4], float2 (&mfa)[2],
             mma_f16(st[3], ih[0], ih[1], ih[2], ih[3], Br[1] ^ TC_NEG2, Br[3] ^ TC_NEG2);
         }
     }
-    const float us = __int_as_float((126 + 2 * ex) << 23);  // 2^(2e - 1)
+    // 2^(2e - 1): an exponent field when it has one (|h| between 2^-62 and 2^64), else ldexpf (0 / inf /
+    // subnormal -- where the Gram itself leaves the FP32 range)
+    const int e2 = 2 * ex - 1;
+    const float us = (e2 >= -126 && e2 <= 127) ? __int_as_float((127 + e2) << 23) : ldexpf(1.f, e2);
 #pragma unroll
     for (int q4 = 0; q4 < 4; ++q4)
 #pragma unroll

@@ -239,6 +239,26 @@ def test_cg_cluster_scales(env, spread, U):
     set_path(env, "fused")
 
 
+@pytest.mark.parametrize("e", [-12, 12])
+def test_cg_frame_scale(env, e):
+    """The whole frame scaled by 2^e (H and y): the tensor-core Gram's power-of-two bookkeeping against the
+    fp64 oracle on every CG path.  (Much larger or smaller frames leave the FP32 range in the CG recursion
+    itself on every path: p^H G p ~ 2^(6e) overflows near e = 16, ||r||^2 ~ 2^(4e) underflows near e = -30.)"""
+    dbp, ctx, oracle, torch = env
+    for cfg in (synth.CONFIGS["C"].scaled(N=9, C=8), synth.CONFIGS["E"].scaled(N=4, C=4)):
+        H, y, _ = synth.uplink_frame(cfg)
+        f = np.float32(2.0) ** e
+        H, y = (H * f).astype(np.complex64), (y * f).astype(np.complex64)
+        x_ref, _ = oracle.detect_cg(H, y, rho=cfg.N0, mod=cfg.mod, T=cfg.T)
+        for path in CG_PATHS:
+            set_path(env, path)
+            x, _ = dbp.detect_cg(ctx, torch.from_numpy(H).cuda(), torch.from_numpy(y).cuda(), rho=cfg.N0,
+                                 mod=cfg.mod, T=cfg.T)
+            ctx.sync()
+            assert rel(x.cpu().numpy(), x_ref) < TOL, (cfg.name, path)
+    set_path(env, "fused")
+
+
 def test_cg_zero_input(env):
     dbp, ctx, oracle, torch = env
     cfg = synth.CONFIGS["B"].scaled(N=8)
