@@ -18,6 +18,7 @@ ap.add_argument("--nofused", type=int, default=0)
 ap.add_argument("--nsym", type=int, default=0)
 ap.add_argument("--N", type=int, default=0)
 ap.add_argument("--C", type=int, default=0)
+ap.add_argument("--cgtc", type=int, default=1, help="DBP_OPT_CG_TENSOR")
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
 if a.T:
@@ -31,6 +32,7 @@ if a.C:
 ctx = dbp.Context(0)
 ctx.set_option(dbp.OPT_FORCE_SPLIT, a.split)
 ctx.set_option(dbp.OPT_NO_FUSED, a.nofused)
+ctx.set_option(dbp.OPT_CG_TENSOR, a.cgtc)
 if a.solver == "bf":
     Hd, s = synth.downlink_frame(cfg)
     Hd, s = torch.from_numpy(Hd).cuda(), torch.from_numpy(s).cuda()
