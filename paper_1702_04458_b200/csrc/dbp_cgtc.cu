@@ -310,7 +310,7 @@ __device__ __forceinline__ float p2f(int e) {           // 2^e, exact, any int e
 }
 
 template <int KS>
-__global__ void __launch_bounds__(CGT_WARPS * 32, 9)
+__global__ void __maxnreg__(112)   // no spills, 9 CTAs (18 warps) per SM: 1200 subcarriers in one wave
 k_cg_tcj(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmY, CgTcjArgs aj) {
     constexpr int UP = 16, SPC = CGT_WARPS / KS;
     const CgTcArgs& a = aj.b;
