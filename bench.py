@@ -511,6 +511,8 @@ def main():
             join[i].record(sx)
             stream.wait_event(join[i])
 
+    steps_ms = {}                                      # per-step event times of the last timed region
+
     def timed_concurrent(K, T):
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
         barrier()
@@ -522,7 +524,8 @@ def main():
             ev[k][1].record(stream)
         torch.cuda.synchronize()
         barrier()
-        return sum(e0.elapsed_time(e1) for e0, e1 in ev)   # ms over K steps
+        steps_ms["step"] = [e0.elapsed_time(e1) for e0, e1 in ev]
+        return sum(steps_ms["step"])                       # ms over K steps
 
     def timed_region(K, T, names, fn=None):
         fn = fn or solver
@@ -537,11 +540,9 @@ def main():
                 ev[k][i + 1].record(stream)
         torch.cuda.synchronize()
         barrier()
-        per = np.zeros(len(names))
-        for k in range(K):
-            for i in range(len(names)):
-                per[i] += ev[k][i].elapsed_time(ev[k][i + 1])
-        return per  # ms summed over K steps, per solver
+        m = np.array([[ev[k][i].elapsed_time(ev[k][i + 1]) for i in range(len(names))] for k in range(K)])
+        steps_ms["region"] = m                             # [K][solver] ms, for the latency percentiles
+        return m.sum(axis=0)  # ms summed over K steps, per solver
 
     for _ in range(args.warmup):
         for nm in ORDER:
@@ -558,6 +559,7 @@ def main():
     ctx.kernel_times(reset=True)
     st0 = ctx.stats()
     per = timed_region(args.steps, UL.T, ORDER)        # sequential: per-solver times + kernel timer
+    seq_steps = steps_ms["region"]
     st1 = ctx.stats()
     ktimes = ctx.kernel_times(reset=True)
     ctx.set_option(dbp.OPT_KERNEL_TIMING, 0)
@@ -574,6 +576,7 @@ def main():
         step_concurrent(UL.T, join[3])                 # warm the overlapped launch path
         st0 = ctx.stats()
         conc_ms = timed_concurrent(args.steps, UL.T)
+        step_list = steps_ms["step"]
         st1 = ctx.stats()
         ctx.set_option(dbp.OPT_OVERLAP_PREV, 0)
     else:
@@ -581,6 +584,7 @@ def main():
         # every launch and disables graph replay); the timed-kernel region above gives the breakdown
         st0 = ctx.stats()
         conc_ms = float(np.sum(timed_region(args.steps, UL.T, ORDER)))
+        step_list = steps_ms["region"].sum(axis=1).tolist()
         st1 = ctx.stats()
     clocks = clk.stop()
     ctx.sync()
@@ -783,6 +787,13 @@ def main():
             del HEg, yEg
             _ = shareE
 
+    # median and p95 of the step latency (and of each solver's, sequential region), max over ranks
+    def pct(v):
+        v = np.asarray(v, dtype=float)
+        return [float(np.median(v)), float(np.percentile(v, 95))]
+    lat = {"step": dict(zip(("median", "p95"), mx(pct(step_list)).tolist()))}
+    for i, nm in enumerate(ORDER):
+        lat[nm] = dict(zip(("median", "p95"), mx(pct(seq_steps[:, i])).tolist()))
     total_ms = float(per.sum())
     ms_seq = total_ms / args.steps
     ms_step = float(mx([conc_ms])[0]) / args.steps
@@ -858,6 +869,8 @@ def main():
         launches = st1["kernel_launches"] - st0["kernel_launches"]
         line = {"metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_step_sequential": ms_seq,
+                "latency_ms": {"how": "median / p95 over the K timed steps (step: the scheduled step; solvers: the "
+                               "sequential region), max over ranks", **lat},
                 "schedule": (("one stream: " if len(plan) == 1 else "concurrent, one stream per lane: ")
                              + " | ".join(" then ".join(l) for l in plan)
                              + ("; a solver may start in its lane predecessor's last wave (DBP_OPT_OVERLAP_PREV)"
