@@ -166,9 +166,12 @@ def gen_frame(kind: str, cfg, c0: int, c1: int, n0: int = 0, n1: int | None = No
 _SAMPLES = {}
 
 
-def _oracle_sample(n_sub: int):
+_ORACLE_OUT = {}
+
+
+def _oracle_sample(n_sub: int, keep: bool = False):
     """Oracle on subcarriers [0, n_sub) of the same three frames; returns (seconds, bits).
-    The synthetic inputs are generated once per size (not timed)."""
+    The synthetic inputs are generated once per size (not timed); keep: store the outputs."""
     import oracle
     ul, cg, dl = UL.scaled(N=n_sub), CG.scaled(N=n_sub), DL.scaled(N=n_sub)
     if n_sub not in _SAMPLES:
@@ -178,20 +181,50 @@ def _oracle_sample(n_sub: int):
         _SAMPLES[n_sub] = (H, y, Hc, yc, Hd, s)
     H, y, Hc, yc, Hd, s = _SAMPLES[n_sub]
     t0 = time.perf_counter()
-    oracle.detect_admm(H, y, rho=ul.rho, N0=ul.N0, mod=ul.mod, T=ul.T)
-    oracle.beamform_admm(Hd, s, rho=dl.rho, T=dl.T)
-    oracle.detect_cg(Hc, yc, rho=cg.N0, mod=cg.mod, T=cg.T)
+    o_ul = oracle.detect_admm(H, y, rho=ul.rho, N0=ul.N0, mod=ul.mod, T=ul.T)
+    o_dl = oracle.beamform_admm(Hd, s, rho=dl.rho, T=dl.T)
+    o_cg = oracle.detect_cg(Hc, yc, rho=cg.N0, mod=cg.mod, T=cg.T)
     dt = time.perf_counter() - t0
+    if keep:
+        _ORACLE_OUT[n_sub] = (o_ul, o_cg, o_dl)
     bits = ul.bits_per_frame + cg.bits_per_frame + dl.bits_per_frame
     return dt, bits
 
 
-def cpu_baseline(budget_s: float = 10.0, n_sub: int = 240) -> dict:
+PARITY_SUB = 240                                       # subcarriers of the cpu_baseline sample
+
+
+def parity_report(gpu, n_sub: int = PARITY_SUB) -> dict:
+    """The timed step's outputs on the cpu_baseline sample against the oracle's (same frames, same
+    subcarriers): rel-L2 over the sample and the worst subcarrier, hard-bit mismatches."""
+    (s_ref, h_ref), (x_ref, hx_ref), b_ref = _ORACLE_OUT[n_sub]
+    s_g, h_g, x_g, hx_g, b_g = gpu
+
+    def rel(a, b, ax):
+        a, b = np.asarray(a), np.asarray(b)
+        whole = float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+        bb = np.moveaxis(b, ax, 0).reshape(b.shape[ax], -1)
+        aa = np.moveaxis(a, ax, 0).reshape(a.shape[ax], -1)
+        den = np.maximum(np.linalg.norm(bb, axis=1), 1e-3 * np.sqrt(np.mean(np.linalg.norm(bb, axis=1) ** 2)))
+        return whole, float(np.max(np.linalg.norm(aa - bb, axis=1) / den))
+    out = {"how": f"the timed step's outputs on subcarriers [0, {n_sub}) against the fp64 oracle's (cpu_baseline "
+                  "sample): rel-L2 over the sample / worst subcarrier; hard-bit mismatches (ties not excused)",
+           "bar": 1e-4}
+    for nm, a, b, ax, hg, hr in (("admm_ul", s_g, s_ref, 0, h_g, h_ref), ("cg_ul", x_g, x_ref, 0, hx_g, hx_ref),
+                                 ("admm_dl", b_g, b_ref, 1, None, None)):
+        w, m = rel(a, b, ax)
+        out[nm] = {"rel_l2": w, "max_subcarrier": m}
+        if hg is not None:
+            out[nm]["hard_mismatch"] = int(np.count_nonzero(np.asarray(hg) != np.asarray(hr)))
+    return out
+
+
+def cpu_baseline(budget_s: float = 10.0, n_sub: int = PARITY_SUB) -> dict:
     import oracle
     oracle.build()
     tot_t, tot_b, reps = 0.0, 0, 0
     while tot_t < budget_s and reps < 1000:
-        dt, b = _oracle_sample(n_sub)
+        dt, b = _oracle_sample(n_sub, keep=reps == 0)
         tot_t += dt
         tot_b += b
         reps += 1
@@ -567,6 +600,7 @@ def main():
     step_ms_rank = float(np.sum(per)) / args.steps
     conc_ms = None
     overlap = False
+    gpu_sample = None
     comm_stats = (st0, st1)                            # the timed-kernel region's counters (per-rank comm)
     if concurrent:                                     # the step as scheduled (headline)
         # consecutive solvers on a lane are independent frames: each may start in its predecessor's
@@ -577,6 +611,10 @@ def main():
         st0 = ctx.stats()
         conc_ms = timed_concurrent(args.steps, UL.T)
         step_list = steps_ms["step"]
+        if rank == 0 and not args.no_cpu_baseline:     # the step's outputs on the oracle sample (parity)
+            ctx.sync()
+            gpu_sample = tuple(t[:PARITY_SUB].cpu().numpy() for t in (s_hat, hard, x_hat, hard2)) + (
+                xbf[:, :PARITY_SUB].cpu().numpy(),)
         st1 = ctx.stats()
         ctx.set_option(dbp.OPT_OVERLAP_PREV, 0)
     else:
@@ -862,8 +900,11 @@ def main():
                       "host wall clock, max over ranks"}
 
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline()
+        if gpu_sample is not None:
+            parity = parity_report(gpu_sample)
 
     if rank == 0:
         launches = st1["kernel_launches"] - st0["kernel_launches"]
@@ -881,7 +922,7 @@ def main():
                 "CN(0,1) channels, uniform Gray QAM, AWGN)", "config": workload_config(world),
                 "solvers": solvers, "configs": configs, "centralized_baselines": baselines or None,
                 "paper_table2_context": table2, "multi_gpu": multi,
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roof, "cpu_baseline": cpu, "parity": parity, "e2e": e2e,
                 "gpu_launches": int(launches), "gpu_launches_per_step": launches / args.steps,
                 "consensus_rounds_per_step": (st1["consensus_rounds"] - st0["consensus_rounds"]) / args.steps,
                 "allreduce_calls_per_step": (st1["allreduce_calls"] - st0["allreduce_calls"]) / args.steps,
