@@ -633,6 +633,30 @@ def main():
     per = mx(per)
     per1 = mx(per1)
 
+    # ... and directly, per consensus round: the split path (one launch per round, the path world > 1 runs)
+    # under the kernel event timer; at world 1 forced (no collective), at world > 1 the timed-kernel region
+    split_iter = None
+    if world == 1:
+        ctx.set_option(dbp.OPT_FORCE_SPLIT, 1)
+        for nm in ORDER:
+            solver(nm, UL.T)
+        ctx.sync()
+        ctx.set_option(dbp.OPT_KERNEL_TIMING, 1)
+        ctx.kernel_times(reset=True)
+        for _ in range(K1):
+            for nm in ORDER:
+                solver(nm, UL.T)
+        ctx.sync()
+        kts = ctx.kernel_times(reset=True)
+        ctx.set_option(dbp.OPT_KERNEL_TIMING, 0)
+        ctx.set_option(dbp.OPT_FORCE_SPLIT, 0)
+    else:
+        kts = ktimes
+    split_iter = {"how": "split path, per-launch device time of each per-round kernel (kernel event timer); "
+                         + ("forced at world 1, no collective" if world == 1 else "this rank, world > 1"),
+                  **{k: 1e3 * v[1] / max(v[0], 1) for k, v in kts.items()
+                     if k in ("admm_step", "bf_step", "cg_step", "ss_ul_step", "ss_dl_step")}}
+
     def timed_fn(fn, K, flush_k=0):
         for _ in range(3):
             fn()
@@ -923,6 +947,7 @@ def main():
                 "solvers": solvers, "configs": configs, "centralized_baselines": baselines or None,
                 "paper_table2_context": table2, "multi_gpu": multi,
                 "roofline": roof, "cpu_baseline": cpu, "parity": parity, "e2e": e2e,
+                "per_iter_split_us": split_iter,
                 "gpu_launches": int(launches), "gpu_launches_per_step": launches / args.steps,
                 "consensus_rounds_per_step": (st1["consensus_rounds"] - st0["consensus_rounds"]) / args.steps,
                 "allreduce_calls_per_step": (st1["allreduce_calls"] - st0["allreduce_calls"]) / args.steps,
