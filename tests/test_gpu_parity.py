@@ -880,12 +880,18 @@ def test_admm_fused_nsym(env, cfg, reg, T):
 @pytest.mark.parametrize("cfg", [synth.CONFIGS["C"].scaled(N=13, N_sym=7),
                                  synth.Config("cj2", "cg_ul", C=5, S=12, U=8, N=9, N_sym=2, mod="qam16", snr_db=15),
                                  synth.Config("cj5", "cg_ul", C=12, S=16, U=14, N=7, N_sym=5, mod="qam64", snr_db=25),
-                                 synth.Config("cj3u4", "cg_ul", C=3, S=8, U=4, N=11, N_sym=3, mod="qpsk", snr_db=10)],
+                                 synth.Config("cj3u4", "cg_ul", C=3, S=8, U=4, N=11, N_sym=3, mod="qpsk", snr_db=10),
+                                 # k_cg_tcj: J = 8 (a full n8 MMA tile of symbols), odd C with two clusters per
+                                 # stage, S padded to 64 rows, a short K (one warp per subcarrier)
+                                 synth.Config("tj8", "cg_ul", C=7, S=14, U=12, N=10, N_sym=8, mod="qam16", snr_db=20),
+                                 synth.Config("tj3", "cg_ul", C=3, S=40, U=16, N=9, N_sym=3, mod="qam64", snr_db=25),
+                                 synth.Config("tj2", "cg_ul", C=2, S=16, U=10, N=5, N_sym=2, mod="qpsk", snr_db=15)],
                          ids=lambda c: f"{c.name}-C{c.C}S{c.S}U{c.U}N{c.N}J{c.N_sym}")
 @pytest.mark.parametrize("T", [1, 3, 5, 16])
 def test_cg_fused_nsym(env, cfg, T):
-    """k_fusedj<., 0>: CG-UL with N_sym = 2..7 in one kernel (G = sum_c G_c and the J matched filters
-    summed once per subcarrier, J CG solves on the CTA's lane groups)."""
+    """CG-UL with N_sym > 1 in one kernel: k_cg_tcj (9 <= U <= 16, J <= 8: tensor cores) or k_fusedj<., 0>
+    (G = sum_c G_c and the J matched filters summed once per subcarrier, J CG solves on the CTA's lane
+    groups)."""
     dbp, ctx, oracle, torch = env
     H, y, _ = synth.uplink_frame(cfg)
     st0 = ctx.stats()
