@@ -31,3 +31,32 @@ def test_bench_refuses_world_mismatch():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--plumbing-check"],
                        capture_output=True, text=True, timeout=120, env=env, cwd=ROOT)
     assert r.returncode != 0 and "WORLD_SIZE=1" in (r.stderr + r.stdout)
+
+
+def test_parity_report_metrics():
+    """bench.py's parity object: rel-L2 over the sample, the worst subcarrier (axis 0 for the uplink
+    [N][J][U] outputs, axis 1 for the downlink [C][N][J][S]) and hard-bit mismatch counts."""
+    import importlib.util
+    import numpy as np
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    rng = np.random.default_rng(0)
+    n = 6
+    s = rng.standard_normal((n, 1, 4)) + 1j * rng.standard_normal((n, 1, 4))
+    x = rng.standard_normal((n, 1, 4)) + 1j * rng.standard_normal((n, 1, 4))
+    b = rng.standard_normal((3, n, 1, 8)) + 1j * rng.standard_normal((3, n, 1, 8))
+    h = rng.integers(0, 16, (n, 1, 4)).astype(np.uint8)
+    bench._ORACLE_OUT[n] = ((s, h), (x, h), b)
+    s_g = s.copy()
+    s_g[2] *= 1.01                                        # one subcarrier off by 1%
+    h_g = h.copy()
+    h_g[0, 0, 0] ^= 1                                     # one hard decision flipped
+    b_g = b.copy()
+    b_g[:, 4] *= 1.001                                    # subcarrier 4 of every cluster, downlink axis 1
+    out = bench.parity_report((s_g, h_g, x, h, b_g), n_sub=n)
+    assert abs(out["admm_ul"]["max_subcarrier"] - 0.01) < 1e-12
+    assert 0 < out["admm_ul"]["rel_l2"] < 0.01
+    assert out["admm_ul"]["hard_mismatch"] == 1 and out["cg_ul"]["hard_mismatch"] == 0
+    assert out["cg_ul"]["rel_l2"] == 0.0
+    assert abs(out["admm_dl"]["max_subcarrier"] - 0.001) < 1e-12
