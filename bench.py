@@ -303,6 +303,13 @@ def algorithmic(kernel: str, C_loc: int):
     return "hbm", float(table.get(kernel, 0.0))
 
 
+def peaks_hbm():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs")
+    except Exception:
+        return None
+
+
 def load_traffic() -> dict:
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
@@ -846,6 +853,38 @@ def main():
                                 "shape": f"per-GPU share of E at G=8: C_loc={Ce} (C=128) S=32 U=32 N=4800 "
                                          f"{cfgE.mod} T={cfgE.T}; gbps = the whole frame's bits / this GPU's "
                                          f"compute time (no allreduce)"}
+            # the same share on the split path (what each rank runs at G = 8): the per-round iteration kernel
+            # against the HBM roofline (north star: >= 60% in the iteration kernel).  Algorithmic bytes of
+            # one ADMM round at gamma = 1 (w-only state): packed rho B^{-1} + y^reg + w read + w written per
+            # pair (4992 B at UP = 32); the init round (t = 1) reads y^reg and writes w only
+            ctx.set_option(dbp.OPT_FORCE_SPLIT, 1)
+            for _ in range(2):
+                dbp.detect_admm(ctx, HEg, yEg, rho=cfgE.rho, N0=cfgE.N0, mod=cfgE.mod, T=cfgE.T)
+            ctx.sync()
+            ctx.set_option(dbp.OPT_KERNEL_TIMING, 1)
+            ctx.kernel_times(reset=True)
+            for _ in range(10):
+                flush_l2(0)
+                dbp.detect_admm(ctx, HEg, yEg, rho=cfgE.rho, N0=cfgE.N0, mod=cfgE.mod, T=cfgE.T)
+            ctx.sync()
+            ktE = ctx.kernel_times(reset=True)
+            ctx.set_option(dbp.OPT_KERNEL_TIMING, 0)
+            ctx.set_option(dbp.OPT_FORCE_SPLIT, 0)
+            if "admm_step" in ktE:
+                cnt, tot = ktE["admm_step"]
+                pairs = Ce * cfgE.N
+                upE = 32
+                rnd = pairs * (upE * (upE + 1) // 2 * 8 + 3 * upE * 8) + 2 * cfgE.N * upE * 8
+                ini = pairs * 2 * upE * 8 + cfgE.N * upE * 8
+                avg_bytes = (ini + (cfgE.T - 1) * rnd) / cfgE.T
+                us = 1e3 * tot / max(cnt, 1)
+                gbs = avg_bytes / (us * 1e-6) / 1e9
+                hbm = float(peaks_hbm()) if peaks_hbm() else 6550.0
+                configs["E_share_iteration_kernel"] = {
+                    "kernel": "admm_step (k_admm_it, one launch per consensus round, split path)",
+                    "avg_us": us, "algorithmic_bytes": avg_bytes, "achieved_GBps": gbs, "peak_GBps": hbm,
+                    "frac": gbs / hbm, "shape": f"C_loc={Ce} S=32 U=32 N={cfgE.N}, T={cfgE.T} launches per call "
+                                                "(init + 4 rounds), L2 flushed before each call"}
             del HEg, yEg
             _ = shareE
 

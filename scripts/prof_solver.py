@@ -13,8 +13,11 @@ ap.add_argument("--solver", default="admm", choices=["admm", "cg", "bf"])
 ap.add_argument("--config", default="C")
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--split", type=int, default=0)
+ap.add_argument("--C", type=int, default=0)
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
+if a.C:
+    cfg = cfg.scaled(C=a.C)
 ctx = dbp.Context(0)
 ctx.set_option(dbp.OPT_FORCE_SPLIT, a.split)
 if a.solver == "bf":
