@@ -101,6 +101,15 @@ __global__ void __launch_bounds__(512, UP <= 16 ? 2 : 1) k_admm_gj(UlArgs a) {  
 // gather fewer sectors and the direct loads measured faster (C split: 22.6 vs
 // 25.3 us), so there the rows come straight from HBM.
 constexpr int split_staged(int UP) { return UP >= 32; }
+// staging depth (chunks per warp in flight + the one being read): a CTA walks only C_loc / CCH chunks
+// (4 at the E share), so a 2-deep ring leaves the first chunk's load latency exposed per CTA
+#ifndef DBP_SPLIT_NBUF
+#define DBP_SPLIT_NBUF 2
+#endif
+constexpr int SPLIT_NBUF = DBP_SPLIT_NBUF;
+__device__ __forceinline__ void cp_async_wait_nbuf() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(SPLIT_NBUF - 1) : "memory");
+}
 template <int UP>
 __device__ __forceinline__ void warp_tri_copy(float2* dst, const float2* __restrict__ Gp, int C, int N, int c0,
                                               int n0, int q0, int CCH, int lane) {
@@ -115,21 +124,33 @@ __device__ __forceinline__ void warp_tri_copy(float2* dst, const float2* __restr
     cp_async_commit();
 }
 
-// Row i of this lane's pair for chunk c0 (buffers tb[2] of 32/UP triangles each).
+// Chunks 0 .. NBUF-2 of the warp's triangles into buffers 0 .. NBUF-2 (one commit group each, empty
+// past the last chunk, so the group count stays uniform).
+template <int UP>
+__device__ __forceinline__ void warp_tri_prologue(float2* tb, const float2* __restrict__ Gp, int C, int N, int n0,
+                                                  int q0, int CCH, int lane) {
+    constexpr int WB = 32 / UP * tri(UP);
+#pragma unroll
+    for (int j = 0; j < SPLIT_NBUF - 1; ++j) {
+        if (j * CCH < C) warp_tri_copy<UP>(tb + j * WB, Gp, C, N, j * CCH, n0, q0, CCH, lane);
+        else cp_async_commit();
+    }
+}
+
+// Row i of this lane's pair for chunk c0 (buffers tb[NBUF] of 32/UP triangles each): chunk k + NBUF - 1
+// is issued into the buffer chunk k - 1 was read from, then chunk k's group is waited for.
 template <int UP>
 __device__ __forceinline__ void warp_tri_row(float2* tb, const float2* __restrict__ Gp, int C, int N, int c0, int n0,
                                              int q0, int CCH, int lane, int qi, int i, float2 (&R)[UP]) {
     constexpr int WB = 32 / UP * tri(UP);
     const int k = c0 / CCH;
     DBP_SYNCWARP();                                        // the buffer about to be refilled was read a chunk ago
-    if (c0 + CCH < C) {
-        warp_tri_copy<UP>(tb + ((k + 1) & 1) * WB, Gp, C, N, c0 + CCH, n0, q0, CCH, lane);
-        cp_async_wait_1();
-    } else {
-        cp_async_wait_all();
-    }
+    const int kn = k + SPLIT_NBUF - 1;
+    if (kn * CCH < C) warp_tri_copy<UP>(tb + (kn % SPLIT_NBUF) * WB, Gp, C, N, kn * CCH, n0, q0, CCH, lane);
+    else cp_async_commit();
+    cp_async_wait_nbuf();                                  // chunk k's group is complete
     DBP_SYNCWARP();
-    load_herm_row_s<UP>(tb + (k & 1) * WB + qi * tri(UP), i, R);
+    load_herm_row_s<UP>(tb + (k % SPLIT_NBUF) * WB + qi * tri(UP), i, R);
 }
 
 // Split path: one iteration (or the init t = 1) for all local clusters of NT
@@ -148,7 +169,7 @@ __global__ void __launch_bounds__(256) k_admm_it(UlArgs a, int CCH) {   // split
     float2* pbuf = sm;                                  // [NT*CCH][UP]
     float2* Wp = pbuf + (size_t)NT * CCH * UP;          // [NT][J][CCH][UP] per-slot partial sums
     float2* Sv = Wp + (size_t)NT * J * CCH * UP;        // [NT][J][UP]
-    float2* Tb = Sv + (size_t)NT * J * UP;              // [warps][2][32/UP][tri(UP)] staged G^{-1}
+    float2* Tb = Sv + (size_t)NT * J * UP;              // [warps][NBUF][32/UP][tri(UP)] staged G^{-1}
     const int tid = threadIdx.x;
     const int q = tid / UP, i = tid % UP;
     const int nl = q / CCH, cl = q % CCH;
@@ -157,8 +178,8 @@ __global__ void __launch_bounds__(256) k_admm_it(UlArgs a, int CCH) {   // split
     const int nn = n < a.N ? n : a.N - 1;
     float2* buf = pbuf + (size_t)q * UP;
     const int lane = tid & 31, q0 = (tid >> 5) * (32 / UP);
-    float2* tb = Tb + (size_t)(tid >> 5) * 2 * (32 / UP) * tri(UP);
-    if (split_staged(UP) && !a.init) warp_tri_copy<UP>(tb, a.Ginv, C, a.N, 0, n0, q0, CCH, lane);
+    float2* tb = Tb + (size_t)(tid >> 5) * SPLIT_NBUF * (32 / UP) * tri(UP);
+    if (split_staged(UP) && !a.init) warp_tri_prologue<UP>(tb, a.Ginv, C, a.N, n0, q0, CCH, lane);
     for (int e = tid; e < NT * J * UP; e += blockDim.x) {
         const int el = e / (J * UP);
         const bool ok = n0 + el < a.N && !a.init;
@@ -330,7 +351,7 @@ __global__ void __launch_bounds__(256, UP >= 32 ? 2 : 3) k_bf_it(DlArgs a, int C
     float2* pbuf = sm;                                  // [NT*CCH][UP]
     float2* Wp = pbuf + (size_t)NT * CCH * UP;          // [NT][J][CCH][UP] per-slot partial sums
     float2* Wv = Wp + (size_t)NT * J * CCH * UP;        // [NT][J][UP]  allreduced w^(t-1)
-    float2* Tb = Wv + (size_t)NT * J * UP;              // [warps][2][32/UP][tri(UP)] staged B^{-1}
+    float2* Tb = Wv + (size_t)NT * J * UP;              // [warps][NBUF][32/UP][tri(UP)] staged B^{-1}
     const int tid = threadIdx.x;
     const int q = tid / UP, i = tid % UP;
     const int nl = q / CCH, cl = q % CCH;
@@ -339,8 +360,8 @@ __global__ void __launch_bounds__(256, UP >= 32 ? 2 : 3) k_bf_it(DlArgs a, int C
     const int nn = n < a.N ? n : a.N - 1;
     float2* buf = pbuf + (size_t)q * UP;
     const int lane = tid & 31, q0 = (tid >> 5) * (32 / UP);
-    float2* tb = Tb + (size_t)(tid >> 5) * 2 * (32 / UP) * tri(UP);
-    if (split_staged(UP)) warp_tri_copy<UP>(tb, a.Binv, C, a.N, 0, n0, q0, CCH, lane);
+    float2* tb = Tb + (size_t)(tid >> 5) * SPLIT_NBUF * (32 / UP) * tri(UP);
+    if (split_staged(UP)) warp_tri_prologue<UP>(tb, a.Binv, C, a.N, n0, q0, CCH, lane);
     const bool fin = a.step > a.T;
     const bool first = a.step == 2;
     // the output pass reads H_c of every pair: pull the pair's tile into L2 one
@@ -487,9 +508,9 @@ cudaError_t launch_admm_gj(const LaunchCtx& L, int UP, UlArgs a) {
 
 // pbuf [NT*CCH][UP], per-slot partial sums [NT][J][CCH][UP], [NT][J][UP] consensus vector,
 size_t split_smem(int UP, int NT, int CCH, int J) {
-    // + per-warp double-buffered triangles: 2 x tri(UP) per pair slot of every (possibly partial) warp
+    // + per-warp staged triangles: NBUF x tri(UP) per pair slot of every (possibly partial) warp
     const size_t slots = split_staged(UP) ? (size_t)(NT * CCH * UP + 31) / 32 * (32 / UP) : 0;
-    return ((size_t)NT * CCH * UP * (1 + J) + (size_t)NT * J * UP + 2 * slots * tri(UP)) * 8;
+    return ((size_t)NT * CCH * UP * (1 + J) + (size_t)NT * J * UP + SPLIT_NBUF * slots * tri(UP)) * 8;
 }
 
 // Split CTA shape: CCH clusters per chunk, NT subcarriers, ~TH threads: small CTAs, so
