@@ -161,8 +161,11 @@ __device__ __forceinline__ void warp_tri_row(float2* tb, const float2* __restric
 // at the end forms the partial sum (deterministic).  Each warp therefore
 // streams its pairs' G^{-1} rows independently, and the load latency of one
 // chunk is hidden by the other warps instead of serialising the CTA.
-template <int UP>
+// INIT: the instantiation launched for the init round (t = 1, no B^{-1}); INIT = false, rounds 2..T
+// (compile-time: the round kernel carries no init branches)
+template <int UP, bool INIT>
 __global__ void __launch_bounds__(256) k_admm_it(UlArgs a, int CCH) {   // split_cfg: <= 256 threads
+    constexpr bool init = INIT;                            // a.init (measured: E share 73.3 -> 69.7 us per launch)
     extern __shared__ __align__(16) float2 sm[];
     DBP_POISON_SMEM(sm);
     const int C = a.C_loc, NT = a.NT, J = a.J;
@@ -179,10 +182,10 @@ __global__ void __launch_bounds__(256) k_admm_it(UlArgs a, int CCH) {   // split
     float2* buf = pbuf + (size_t)q * UP;
     const int lane = tid & 31, q0 = (tid >> 5) * (32 / UP);
     float2* tb = Tb + (size_t)(tid >> 5) * SPLIT_NBUF * (32 / UP) * tri(UP);
-    if (split_staged(UP) && !a.init) warp_tri_prologue<UP>(tb, a.Ginv, C, a.N, n0, q0, CCH, lane);
+    if (split_staged(UP) && !init) warp_tri_prologue<UP>(tb, a.Ginv, C, a.N, n0, q0, CCH, lane);
     for (int e = tid; e < NT * J * UP; e += blockDim.x) {
         const int el = e / (J * UP);
-        const bool ok = n0 + el < a.N && !a.init;
+        const bool ok = n0 + el < a.N && !init;
         Sv[e] = prox(ok ? a.wbuf[(size_t)n0 * J * UP + e] : make_float2(0.f, 0.f), a.px);
     }
     float2* wp = Wp + ((size_t)nl * J * CCH + cl) * UP + i;   // this lane's slot, symbol stride CCH * UP
@@ -192,8 +195,11 @@ __global__ void __launch_bounds__(256) k_admm_it(UlArgs a, int CCH) {   // split
         const int c = c0 + cl;
         const bool valid = n < a.N && c < C;
         const size_t pair = (size_t)(c < C ? c : C - 1) * a.N + nn;
+        // symbol 0's y^reg and w_c are loaded before the wait for the staged rows (their latency overlaps it)
+        const float2 yreg0 = a.yreg[pair * J * UP + i];
+        const float2 w00 = (!init && a.wonly) ? a.z[pair * J * UP + i] : make_float2(0.f, 0.f);
         float2 R[UP];
-        if (!a.init) {
+        if (!init) {
             if (split_staged(UP)) warp_tri_row<UP>(tb, a.Ginv, C, a.N, c0, n0, q0, CCH, lane, q - q0, i, R);
             else load_herm_row<UP>(a.Ginv + pair * tri(UP), i, R);
 #pragma unroll
@@ -201,9 +207,9 @@ __global__ void __launch_bounds__(256) k_admm_it(UlArgs a, int CCH) {   // split
         }
         for (int jj = 0; jj < J; ++jj) {
             const size_t o = (pair * J + jj) * UP + i;
-            const float2 yreg = a.yreg[o];
+            const float2 yreg = jj == 0 ? yreg0 : a.yreg[o];
             float2 lam, z, w;
-            if (a.init) {                                                // line 10
+            if (init) {                                                // line 10
                 lam = make_float2(0.f, 0.f);
                 z = yreg;
                 w = yreg;
@@ -211,7 +217,7 @@ __global__ void __launch_bounds__(256) k_admm_it(UlArgs a, int CCH) {   // split
                 // gamma = 1: lambda' = w - s, so z' + lambda' = y^reg + rho B^{-1} (2 s - w) + w - s
                 // (lines 12, 15, 17 with lambda and z eliminated): only w_c is carried between rounds
                 const float2 s = Sv[((size_t)nl * J + jj) * UP + i];
-                const float2 w0 = a.z[o];
+                const float2 w0 = jj == 0 ? w00 : a.z[o];
                 w = c_add(c_add(yreg, row_apply<UP>(R, buf, i, c_sub(c_scale(s, 2.f), w0))), c_sub(w0, s));
             } else {
                 const float2 s = Sv[((size_t)nl * J + jj) * UP + i];
@@ -343,7 +349,8 @@ __global__ void __launch_bounds__(512, MINB) k_bf_gj(DlArgs a) {
 // Split path step t (2..T): complete iteration t-1 (or the init when t == 2),
 // then m, w_c and the local partial sum.  step == T+1: complete, write x_c.
 // Clusters in chunks of CCH.
-template <int UP>
+// FIN: the instantiation launched for the output pass (a.step > a.T); FIN = false, the rounds
+template <int UP, bool FIN>
 __global__ void __launch_bounds__(256, UP >= 32 ? 2 : 3) k_bf_it(DlArgs a, int CCH) {   // split_cfg: <= 256 threads
     extern __shared__ __align__(16) float2 sm[];
     DBP_POISON_SMEM(sm);
@@ -362,7 +369,9 @@ __global__ void __launch_bounds__(256, UP >= 32 ? 2 : 3) k_bf_it(DlArgs a, int C
     const int lane = tid & 31, q0 = (tid >> 5) * (32 / UP);
     float2* tb = Tb + (size_t)(tid >> 5) * SPLIT_NBUF * (32 / UP) * tri(UP);
     if (split_staged(UP)) warp_tri_prologue<UP>(tb, a.Binv, C, a.N, n0, q0, CCH, lane);
-    const bool fin = a.step > a.T;
+    // the step kernels know they are not the output pass (compile time: measured faster, 24.5 -> 21.2 us at
+    // config D); the output pass keeps the runtime test (its compile-time twin measured slower, 107.7 -> 119.7)
+    const bool fin = FIN && a.step > a.T;
     const bool first = a.step == 2;
     // the output pass reads H_c of every pair: pull the pair's tile into L2 one
     // chunk ahead (all chunks up front overflows L2 at C_loc = 128: 8x slower)
@@ -397,7 +406,7 @@ __global__ void __launch_bounds__(256, UP >= 32 ? 2 : 3) k_bf_it(DlArgs a, int C
                 lam = make_float2(0.f, 0.f);
                 qv = c_scale(sv, a.a0);
             } else {                                                     // lines 14-15 of t-1
-                const float2 mo = a.m[o], lo = a.lam[o];
+                const float2 mo = a.m[o], lo = a.lam[o];   // (preloading them before the wait measured slower here)
                 const float2 w = c_sub(mo, lo);
                 const float2 d = c_sub(sv, Wv[((size_t)nl * J + jj) * UP + i]);
                 const float f = lemma2_scale(group_sum<UP>(c_norm2(d)), a.eps, a.inv_c);
@@ -530,8 +539,13 @@ void split_cfg(int UP, int C_loc, int N, int J, int* NT, int* CCH) {
 
 cudaError_t launch_admm_it(const LaunchCtx& L, int UP, UlArgs a, int CCH) {
     const size_t smem = split_smem(UP, a.NT, CCH, a.J);
-    DBP_DISPATCH_UP(UP, big_smem(k_admm_it<UPc>, smem);
-                    k_admm_it<UPc><<<cdiv_i(a.N, a.NT), a.NT * CCH * UPc, smem, L.stream>>>(a, CCH));
+    if (a.init) {
+        DBP_DISPATCH_UP(UP, big_smem(k_admm_it<UPc, true>, smem);
+                        k_admm_it<UPc, true><<<cdiv_i(a.N, a.NT), a.NT * CCH * UPc, smem, L.stream>>>(a, CCH));
+    } else {
+        DBP_DISPATCH_UP(UP, big_smem(k_admm_it<UPc, false>, smem);
+                        k_admm_it<UPc, false><<<cdiv_i(a.N, a.NT), a.NT * CCH * UPc, smem, L.stream>>>(a, CCH));
+    }
     L.count(1);
     return cudaGetLastError();
 }
@@ -576,8 +590,13 @@ cudaError_t launch_zf_out(const LaunchCtx& L, int UP, const float2* Hd, const fl
 
 cudaError_t launch_bf_it(const LaunchCtx& L, int UP, DlArgs a, int CCH) {
     const size_t smem = split_smem(UP, a.NT, CCH, a.J);
-    DBP_DISPATCH_UP(UP, big_smem(k_bf_it<UPc>, smem);
-                    k_bf_it<UPc><<<cdiv_i(a.N, a.NT), a.NT * CCH * UPc, smem, L.stream>>>(a, CCH));
+    if (a.step > a.T) {
+        DBP_DISPATCH_UP(UP, big_smem(k_bf_it<UPc, true>, smem);
+                        k_bf_it<UPc, true><<<cdiv_i(a.N, a.NT), a.NT * CCH * UPc, smem, L.stream>>>(a, CCH));
+    } else {
+        DBP_DISPATCH_UP(UP, big_smem(k_bf_it<UPc, false>, smem);
+                        k_bf_it<UPc, false><<<cdiv_i(a.N, a.NT), a.NT * CCH * UPc, smem, L.stream>>>(a, CCH));
+    }
     L.count(1);
     return cudaGetLastError();
 }
