@@ -30,6 +30,31 @@
 #endif
 namespace dbp {
 
+// The fused iteration kernels' B^{-1} rows (k_admm_gj / k_bf_gj).  At UP = 32 a warp is one pair: its packed
+// triangle is staged through shared memory with coalesced 16-B cp.async (lane-row loads straight from HBM
+// touch 32 sectors per warp instruction, see warp_tri_copy); below that the rows come straight from HBM.
+#ifndef DBP_GJ_STAGED_MIN
+#define DBP_GJ_STAGED_MIN 32
+#endif
+constexpr bool gj_staged(int UP) { return UP >= DBP_GJ_STAGED_MIN; }
+template <int UP>
+__device__ __forceinline__ void gj_load_rows(const float2* __restrict__ Gp, size_t pair, float2* stage, int q, int i,
+                                             float2 (&R)[UP]) {
+    if constexpr (gj_staged(UP)) {
+        static_assert(UP == 32, "one pair per warp");
+        float2* tb = stage + (size_t)q * tri(UP);
+        const float2* src = Gp + pair * tri(UP);
+        for (int e = i; e < tri(UP) / 2; e += 32) cp_async16(tb + 2 * e, src + 2 * e);
+        cp_async_commit();
+        cp_async_wait_all();
+        DBP_SYNCWARP();
+        load_herm_row_s<UP>(tb, i, R);
+    } else {
+        load_herm_row<UP>(Gp + pair * tri(UP), i, R);
+    }
+}
+
+
 // ============================================================ ADMM-UL
 
 
@@ -53,7 +78,7 @@ __global__ void __launch_bounds__(512, UP <= 16 ? 2 : 1) k_admm_gj(UlArgs a) {  
     float2* buf = pbuf + (size_t)q * UP;
 
     float2 R[UP];
-    load_herm_row<UP>(a.Ginv + pair * tri(UP), i, R); // row i of B_c^{-1} (k_prefold / k_prelr)
+    gj_load_rows<UP>(a.Ginv, pair, sm + (size_t)2 * NT * C * UP + (size_t)NT * UP, q, i, R);   // row i of B_c^{-1}
 #pragma unroll
     for (int j = 0; j < UP; ++j) R[j] = c_scale(R[j], a.rho);   // rho B_c^{-1} (eq. (3))
 
@@ -295,7 +320,7 @@ __global__ void __launch_bounds__(512, MINB) k_bf_gj(DlArgs a) {
                          "r"((uint32_t)bytes) : "memory");
     }
     float2 R[UP];
-    load_herm_row<UP>(a.Binv + pair * tri(UP), i, R);  // row i of B_c^{-1} (k_prefold / k_prelr)
+    gj_load_rows<UP>(a.Binv, pair, sm + (size_t)2 * NT * C * UP + (size_t)NT * UP, q, i, R);   // row i of B_c^{-1}
 
     for (int jj = 0; jj < a.J; ++jj) {
         const float2 sv = i < a.U ? a.s[((size_t)nn * a.J + jj) * a.U + i] : make_float2(0.f, 0.f);
@@ -489,6 +514,10 @@ __global__ void __launch_bounds__(256) k_zf_out(const float2* __restrict__ Hd, c
 static int cdiv_i(long x, long y) { return (int)((x + y - 1) / y); }
 
 size_t iter_smem(int UP, int NT, int C) { return ((size_t)2 * NT * C * UP + (size_t)NT * UP) * 8; }
+// + the staged triangles of gj_load_rows (UP = 32: one per pair)
+static size_t gj_smem(int UP, int NT, int C) {
+    return iter_smem(UP, NT, C) + (gj_staged(UP) ? (size_t)NT * C * tri(UP) * 8 : 0);
+}
 
 // CTA shape: NT subcarriers x C_loc clusters x UP lanes (<= 1024 threads).
 bool iter_cfg(int UP, int C_loc, int N, int max_smem, int* NT) {
@@ -508,7 +537,7 @@ static void big_smem(K k, size_t smem) {
 }
 
 cudaError_t launch_admm_gj(const LaunchCtx& L, int UP, UlArgs a) {
-    const size_t smem = iter_smem(UP, a.NT, a.C_loc);
+    const size_t smem = gj_smem(UP, a.NT, a.C_loc);
     DBP_DISPATCH_UP(UP, big_smem(k_admm_gj<UPc>, smem);
                     k_admm_gj<UPc><<<cdiv_i(a.N, a.NT), a.NT * a.C_loc * UPc, smem, L.stream>>>(a));
     L.count(1);
@@ -551,7 +580,7 @@ cudaError_t launch_admm_it(const LaunchCtx& L, int UP, UlArgs a, int CCH) {
 }
 
 cudaError_t launch_bf_gj(const LaunchCtx& L, int UP, DlArgs a) {
-    const size_t smem = iter_smem(UP, a.NT, a.C_loc);
+    const size_t smem = gj_smem(UP, a.NT, a.C_loc);
     const int grid = cdiv_i(a.N, a.NT), nthr = a.NT * a.C_loc * UP;
     DBP_DISPATCH_UP(UP,
         if constexpr (UPc <= 16) {
