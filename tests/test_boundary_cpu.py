@@ -100,3 +100,20 @@ def test_binding_validates_shapes_and_dtypes():
     for f in bad:
         with _pt.raises(ValueError):
             f()
+
+
+def test_missing_library_fails_loudly():
+    """No CPU fallback: with the shared library absent the binding raises (DbpError), it never
+    computes anything itself."""
+    import subprocess
+    import sys
+    code = ("from paper_1702_04458_b200 import dbp\n"
+            "try:\n"
+            "    dbp.load()\n"
+            "except dbp.DbpError as e:\n"
+            "    print('raised', e)\n"
+            "else:\n"
+            "    print('loaded')\n")
+    env = dict(os.environ, DBP_LIB=os.path.join(ROOT, "build_var", "does_not_exist.so"))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=ROOT, timeout=120)
+    assert r.returncode == 0 and r.stdout.startswith("raised") and "not built" in r.stdout, r.stdout + r.stderr
