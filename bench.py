@@ -981,7 +981,11 @@ def main():
                                 if overlap else "")
                              if concurrent else "sequential on one stream"),
                 "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Philox-4x32: i.i.d. Rayleigh "
+                "vs_baseline": None, "dtype": "f32",
+                "dtype_note": "fp32 storage and arithmetic; CG-UL's cluster-summed Gram runs on fp16 tensor cores as an "
+                              "exact power-of-two-scaled hi/lo split with fp32 accumulation (~2^-22 relative; see "
+                              "parity)",
+                "data": "synthetic (seeded Philox-4x32: i.i.d. Rayleigh "
                 "CN(0,1) channels, uniform Gray QAM, AWGN)", "config": workload_config(world),
                 "solvers": solvers, "configs": configs, "centralized_baselines": baselines or None,
                 "paper_table2_context": table2, "multi_gpu": multi,
