@@ -21,6 +21,8 @@ CASES = {
     "C": synth.CONFIGS["C"].scaled(N=24),
     "Cj3": synth.CONFIGS["C"].scaled(N=10, N_sym=3, mod="qam16"),
     "ss": synth.Config("ss", "admm_ul", C=6, S=8, U=16, N=12, mod="qam16", snr_db=20),   # S x S form
+    # UP = 32 (config E's users): staged split-path rounds and the tensor-core G_loc at UP = 32
+    "u32": synth.CONFIGS["E"].scaled(N=6, C=4),
 }
 
 
