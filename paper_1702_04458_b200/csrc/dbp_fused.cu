@@ -633,8 +633,7 @@ static bool launch_fz_t(const LaunchCtx& L, const float2* H, const float2* y, Fu
         a.stage_bytes = Z::G::BYTES;
         a.wreg = Z::WREG;
     }
-    static const size_t pad = [] { const char* e = getenv("DBP_EXP_SMEM_PAD"); return e ? (size_t)strtol(e, nullptr, 0) : 0; }();
-    const size_t SMEM = Z::smem(a.wreg) + pad;     // experiment knob: lower the CTAs per SM
+    const size_t SMEM = Z::smem(a.wreg);
     if (!g_sms_fz) {
         int dev = 0;
         cudaGetDevice(&dev);
