@@ -140,8 +140,9 @@ typedef enum {
     /* 1 (default): the cluster-summed Gram sum_c H_c^H H_c and y^MRC = sum_c H_c^H y_c are formed on
      * the tensor cores (fp16 mma.sync on an exact power-of-two-scaled hi/lo split, FP32 accumulation;
      * error ~2^-22 relative to the Gram, within the 1e-4 parity bar):
-     *   - dbp_detect_cg at world == 1, N_sym == 1, 9 <= U <= 16, S <= 64 (no FORCE_SPLIT / NO_FUSED /
-     *     DEVICE_CONSENSUS): the whole solve in one kernel (k_cg_tc);
+     *   - dbp_detect_cg at world == 1, N_sym <= 8, 9 <= U <= 16, U and S even, S <= 64 (no FORCE_SPLIT /
+     *     NO_FUSED / DEVICE_CONSENSUS): the whole solve in one kernel (k_cg_tc; k_cg_tcj for N_sym > 1, the
+     *     J matched filters on the tensor cores too);
      *   - the split / two-kernel dbp_detect_cg path (world > 1, U up to 32) and the non-fused
      *     dbp_detect_mmse path, N_sym == 1, U even, S <= 64: the rank's G_loc and y^MRC_loc (k_cgg_tc).
      * 0: the FP32 kernels (k_fused; per-pair Grams + fixed-order sum).  The two agree to rounding,
