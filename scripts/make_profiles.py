@@ -24,7 +24,7 @@ NAMES = [(r"k_fused<\d+, 3>", "fused_mmse"), (r"k_fused<\d+, 4>", "fused_zf"), (
          (r"k_prelr<\d+, 0, 0", "pre_cg"), (r"k_prelr<\d+, 0, 1", "pre_ul"), (r"k_prelr<\d+, 1, 2", "pre_dl"),
          (r"k_gram<\d+, 0, 1", "gram_ul"), (r"k_gram<\d+, 1,", "gram_dl"), (r"k_inv_ul", "inv_ul"),
          (r"k_inv_dl", "inv_dl"), (r"k_admm_gj", "admm_fused"), (r"k_bf_gj", "bf_fused"),
-         (r"k_admm_it", "admm_step"), (r"k_bf_it", "bf_step"), (r"k_cg_gsum", "cg_gsum"),
+         (r"k_admm_it", "admm_step"), (r"k_bf_it<\d+, 1>", "bf_final"), (r"k_bf_it", "bf_step"), (r"k_cg_gsum", "cg_gsum"),
          (r"k_cg_it<\d+, 1", "cg_fused"), (r"k_cg_tc", "cg_tc"), (r"k_cgg_tc", "cgg_tc"), (r"k_cg_it<\d+, 0", "cg_step"), (r"k_prox_out", "prox_out"),
          (r"k_mf", "mf"), (r"k_slice", "slice")]
 
@@ -49,8 +49,10 @@ def launches(tag, path):
         v = v / 1e3 if r[ui] in ("nsecond", "ns") else v * 1e3 if r[ui] in ("msecond", "ms") else v
         agg.setdefault(r[ki], []).append(v)
     ours = {k: v for k, v in agg.items() if "dbp::" in k}
-    # shares over the timed step's kernels; the centralized baselines bench.py times afterwards are listed apart
-    BASE = ("fused_mmse", "fused_zf", "central_solve", "zf_out")
+    # shares over the timed step's kernels; everything else bench.py runs afterwards (the split path's per-round
+    # timing, the centralized baselines) is listed apart
+    STEP = ("fused_ul", "fused_dl", "fused_cg", "cg_tc")
+    BASE = tuple(short(k) for k in ours if short(k) not in STEP)
     tot = sum(sum(v) for k, v in ours.items() if short(k) not in BASE) or 1.0
     lines = [f"# {tag}: ncu launch list (gpu__time_duration.sum, --clock-control none)", "",
              "Serialised, cold-cache per-launch times of `" + os.environ.get(
@@ -58,7 +60,7 @@ def launches(tag, path):
              "process, libdbp kernels only below).  Compare SHARES with bench.py's live event timing, not",
              "absolute times.", "", "| kernel | launches | mean us | share of the step's libdbp time |", "|---|---|---|---|"]
     for k, v in sorted(ours.items(), key=lambda kv: -sum(kv[1])):
-        sh = "baseline (not in the step)" if short(k) in BASE else f"{sum(v)/tot:.3f}"
+        sh = "not in the step" if short(k) in BASE else f"{sum(v)/tot:.3f}"
         lines.append(f"| {short(k)} (`{k.split('(')[0]}`) | {len(v)} | {sum(v)/len(v):.1f} | {sh} |")
     others = {k: v for k, v in agg.items() if "dbp::" not in k}
     lines += ["", "Non-libdbp launches in the same process (torch flush / setup): " +
