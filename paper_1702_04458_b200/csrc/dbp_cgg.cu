@@ -312,17 +312,13 @@ bool launch_cgg_tc(const LaunchCtx& L, int UP, const float2* H, const float2* y,
     CUtensorMap tmH{}, tmY{};
     if (!make_map4(&tmH, H, U, S, N, C, 16, a.S16, 1, a.CB, true)) return false;
     if (!make_map4(&tmY, y, S, 1, N, C, a.S16, 1, 1, a.CB)) return false;
-    if (UP == 16) {
-        const size_t smem = CGG<16>::smem(a.pitch);
-        if (cudaFuncSetAttribute(k_cgg_tc<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-            return cudaGetLastError(), false;
-        if (!launch_pdl(k_cgg_tc<16>, N, CGG_KS * 32, smem, L, tmH, tmY, a)) return false;
-    } else {
-        const size_t smem = CGG<32>::smem(a.pitch);
-        if (cudaFuncSetAttribute(k_cgg_tc<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-            return cudaGetLastError(), false;
-        if (!launch_pdl(k_cgg_tc<32>, N, CGG_KS * 32, smem, L, tmH, tmY, a)) return false;
+    const size_t smem = UP == 16 ? CGG<16>::smem(a.pitch) : CGG<32>::smem(a.pitch);
+    auto k = UP == 16 ? k_cgg_tc<16> : k_cgg_tc<32>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
     }
+    if (!launch_pdl(k, N, CGG_KS * 32, smem, L, tmH, tmY, a)) return false;
     L.count(1);
     return true;
 }
