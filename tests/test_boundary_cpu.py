@@ -117,3 +117,17 @@ def test_missing_library_fails_loudly():
     env = dict(os.environ, DBP_LIB=os.path.join(ROOT, "build_var", "does_not_exist.so"))
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=ROOT, timeout=120)
     assert r.returncode == 0 and r.stdout.startswith("raised") and "not built" in r.stdout, r.stdout + r.stderr
+
+
+def test_binding_option_constants_match_header():
+    """Every DBP_OPT_* value of include/dbp.h has the same value as the binding's OPT_* constant."""
+    from paper_1702_04458_b200 import dbp
+    src = open(os.path.join(ROOT, "include", "dbp.h")).read()
+    opts = dict((k, int(v)) for k, v in re.findall(r"DBP_OPT_(\w+)\s*=\s*(\d+)", src))
+    assert len(opts) >= 8
+    for k, v in opts.items():
+        assert getattr(dbp, "OPT_" + k) == v, k
+
+
+def test_set_option_rejects_unknown_without_gpu(lib):
+    assert lib.dbp_set_option(None, 8, 1) == 1              # null context: invalid argument
