@@ -60,3 +60,19 @@ def test_parity_report_metrics():
     assert out["admm_ul"]["hard_mismatch"] == 1 and out["cg_ul"]["hard_mismatch"] == 0
     assert out["cg_ul"]["rel_l2"] == 0.0
     assert abs(out["admm_dl"]["max_subcarrier"] - 0.001) < 1e-12
+
+
+def test_reference_arm_line():
+    """`bench.py --impl reference` (the fp64 oracle on the host, no GPU needed): one JSON line with the
+    base contract's keys, the oracle described as the cpu_baseline of this run, and an e2e without copies."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "0", "--ref-subcarriers", "2"], capture_output=True, text=True, timeout=600,
+                       cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[-1])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "Gbit/s" and d["higher_is_better"]
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["config"]["C"] == 32 and d["config"]["N"] == 1200
